@@ -1,0 +1,273 @@
+"""bench.py — RHS DOF-updates/s of the B200 NSFR path (BASELINE.json metric).
+
+Workload (BASELINE.json configs[4], the metric's own config): isentropic vortex
+on 128^3 curvilinear hexes (beta = 1/20 warp), p = 4, c_+, EC + Roe surface
+flux, weight-adjusted inverse, classical RK4 at CFL 0.1. One STEP = one RK4
+step = 4 RHS evaluations, each updating every DOF (DOF = elements x (p+1)^3 x 5).
+Strong scaling: the 128^3 box is split into z-slabs over N GPUs (one process
+per GPU, NCCL face-halo exchange + lambda_max allreduce per step).
+
+    python bench.py [--gpus N --steps K --warmup W] [--impl reference]
+    torchrun --nproc-per-node N --master-addr 127.0.0.1 bench.py --gpus N ...
+
+Prints ONE JSON line on rank 0. The CPU legs (cpu_baseline and --impl
+reference) run the reference's own compiled primitives (oracle/_ref, built
+from /root/reference/proj/src) under the residual glue, on a bounded sample.
+"""
+from __future__ import annotations
+
+import argparse
+import json
+import os
+import statistics
+import subprocess
+import sys
+import threading
+import time
+
+import numpy as np
+
+ROOT = os.path.dirname(os.path.abspath(__file__))
+sys.path.insert(0, ROOT)
+sys.path.insert(0, os.path.join(ROOT, "tools"))
+
+from flop_model import bytes_per_element, per_element  # noqa: E402
+
+METRIC = "RHS DOF-updates/sec (fp64, 3D Euler NSFR)"
+UNIT = "DOF-updates/s"
+P_DEG, M = 4, 128
+C_PLUS4 = 0.5 * 4.67e-5
+WORKLOAD = "isentropic-vortex-128^3-p4-c_plus-EC+Roe-RK4"
+CPU_SAMPLE_M = 24  # bounded CPU sample: same p/c/flux on a periodic 24^3 box
+
+
+def read_peaks():
+    try:
+        with open(os.path.join(ROOT, "MEASURED_PEAKS.json")) as f:
+            return json.load(f)
+    except Exception:
+        return {}
+
+
+class ClockSampler:
+    """nvidia-smi clocks/throttle reasons sampled during the timed region."""
+
+    FIELDS = ("clocks.sm,clocks.max.sm,clocks_event_reasons.hw_slowdown,"
+              "clocks_event_reasons.hw_thermal_slowdown,clocks_event_reasons.sw_thermal_slowdown,"
+              "clocks_event_reasons.sw_power_cap")
+
+    def __init__(self, device: int):
+        self.device = device
+        self.samples = []
+        self._stop = threading.Event()
+        self._t = threading.Thread(target=self._run, daemon=True)
+
+    def _run(self):
+        while not self._stop.is_set():
+            try:
+                out = subprocess.run(["nvidia-smi", "-i", str(self.device), f"--query-gpu={self.FIELDS}",
+                                      "--format=csv,noheader,nounits"], capture_output=True, text=True,
+                                     timeout=5).stdout.strip()
+                if out:
+                    self.samples.append([x.strip() for x in out.split(",")])
+            except Exception:
+                pass
+            self._stop.wait(0.2)
+
+    def __enter__(self):
+        self._t.start()
+        return self
+
+    def __exit__(self, *a):
+        self._stop.set()
+        self._t.join(timeout=10)
+
+    def summary(self):
+        if not self.samples:
+            return {"sm_mhz": None, "sm_max_mhz": None, "reasons": ["no nvidia-smi samples"]}
+        sm = [float(s[0]) for s in self.samples if s[0].replace(".", "").isdigit()]
+        mx = [float(s[1]) for s in self.samples if s[1].replace(".", "").isdigit()]
+        names = ["hw_slowdown", "hw_thermal_slowdown", "sw_thermal_slowdown", "sw_power_cap"]
+        reasons = sorted({names[i] for s in self.samples for i in range(4)
+                          if len(s) > 2 + i and s[2 + i].lower() == "active"})
+        return {"sm_mhz": statistics.median(sm) if sm else None, "sm_max_mhz": max(mx) if mx else None,
+                "reasons": reasons, "samples": len(self.samples)}
+
+
+def dist_env():
+    world = int(os.environ.get("WORLD_SIZE", "1"))
+    rank = int(os.environ.get("RANK", "0"))
+    local = int(os.environ.get("LOCAL_RANK", "0"))
+    return world, rank, local
+
+
+def cpu_reference_run(steps: int, warmup: int, threads: int):
+    """Reference CPU path (oracle/_ref) RK4 steps on the bounded sample; returns
+    (DOF-updates/s, seconds per step, kind, cores)."""
+    sys.path.insert(0, os.path.join(ROOT, "tests"))
+    from oracle_lib import LIBS, Config, CpuSolver  # CPU baseline leg only
+    kind = "ref" if os.path.exists(LIBS["ref"][0]) else "oracle"
+    cfg = Config(p=P_DEG, m=CPU_SAMPLE_M, c1d=C_PLUS4, case="vortex", roe=True, workers=threads)
+    s = CpuSolver(kind, cfg)
+    u = s.initial_state()
+    dt = 0.1 * s.dx() / s.max_wavespeed(u)
+    for _ in range(warmup):
+        s.rk4_step(u, dt)
+    t0 = time.perf_counter()
+    for _ in range(steps):
+        s.rk4_step(u, dt)
+    sec = (time.perf_counter() - t0) / steps
+    dof = CPU_SAMPLE_M ** 3 * (P_DEG + 1) ** 3 * 5
+    return 4 * dof / sec, sec, ("reference" if kind == "ref" else "port"), threads
+
+
+def run_reference_arm(args):
+    world, rank, _ = dist_env()
+    if rank != 0:
+        return
+    threads = os.cpu_count() or 1
+    val, sec, kind, cores = cpu_reference_run(args.steps, args.warmup, threads)
+    sample = (f"periodic {CPU_SAMPLE_M}^3-element box, same p=4/c_+/EC+Roe/RK4 per-element work as "
+              f"128^3; {args.steps} RK4 steps after {args.warmup} warm-up")
+    print(json.dumps({
+        "impl": "reference", "metric": METRIC, "value": val, "unit": UNIT, "n_gpus": args.gpus,
+        "steps": args.steps, "warmup": args.warmup, "ms_per_step": sec * 1e3,
+        "higher_is_better": True, "scaling": "strong", "vs_baseline": None, "dtype": "f64",
+        "data": "synthetic (analytic isentropic vortex IC)",
+        "config": {"workload": WORKLOAD, "p": P_DEG, "elements": f"{CPU_SAMPLE_M}^3 sample of 128^3"},
+        "cpu_baseline": {"value": val, "unit": UNIT, "cores": cores, "kind": kind, "sample": sample},
+        "e2e": {"value": val, "unit": UNIT, "h2d_bytes_per_step": 0, "d2h_bytes_per_step": 0},
+    }), flush=True)
+
+
+def run_gpu_arm(args):
+    import torch
+    import paper_2312_07725_b200 as pkg
+
+    world, rank, local = dist_env()
+    assert world == args.gpus or world == 1, "launch N>1 under torchrun with --gpus N"
+    device = local
+    torch.cuda.set_device(device)
+    nccl_id = None
+    if world > 1:
+        import torch.distributed as dist
+        dist.init_process_group("gloo", rank=rank, world_size=world)
+        obj = [pkg.nccl_unique_id() if rank == 0 else None]
+        dist.broadcast_object_list(obj, src=0)
+        nccl_id = obj[0]
+    cfg = pkg.SolverConfig(p=P_DEG, m=M, c1d=C_PLUS4, case="vortex", roe=True, device=device,
+                           rank=rank, nranks=world)
+    g = pkg.GpuSolver(cfg, nccl_id=nccl_id)
+    g.init_case()
+    fp64_peak = pkg.measure_fp64_peak(device)
+
+    def barrier():
+        if world > 1:
+            import torch.distributed as dist
+            dist.barrier()
+
+    # warm-up (also captures the CUDA graph of one step)
+    g.advance(args.warmup, cfl=0.1)
+    barrier()
+    launches0 = g.launch_count()
+    with ClockSampler(device) as clk:
+        ms_total, kms = g.time_steps(args.steps, cfl=0.1, per_kernel=True)
+    launches = g.launch_count() - launches0
+    barrier()
+    ms_max = ms_total
+    k2_ms = kms[1] / (4 * args.steps)
+    k1_ms = kms[0] / (4 * args.steps)
+    if world > 1:
+        import torch.distributed as dist
+        t = torch.tensor([ms_total], dtype=torch.float64)
+        dist.all_reduce(t, op=dist.ReduceOp.MAX)
+        ms_max = float(t[0])
+    ne_total = M ** 3
+    dof_total = ne_total * (P_DEG + 1) ** 3 * 5
+    value = 4 * dof_total * args.steps / (ms_max / 1e3)
+
+    # e2e through the public API with host buffers (pinned): per step H2D of
+    # the state, one RK4 step, D2H of the state
+    host = torch.empty(g.state_shape, dtype=torch.float64, pin_memory=True).numpy()
+    host[...] = g.get_state()
+    e2e_steps = max(1, min(args.steps, 3))
+    barrier()
+    t0 = time.perf_counter()
+    for _ in range(e2e_steps):
+        g.set_state(host)
+        g.rk4_step(0.1)
+        host[...] = g.get_state()
+    e2e_sec = (time.perf_counter() - t0) / e2e_steps
+    if world > 1:
+        import torch.distributed as dist
+        t = torch.tensor([e2e_sec], dtype=torch.float64)
+        dist.all_reduce(t, op=dist.ReduceOp.MAX)
+        e2e_sec = float(t[0])
+    e2e_val = 4 * dof_total / e2e_sec
+    state_bytes = host.nbytes
+
+    fm = per_element(P_DEG)
+    ne_local = g.ne
+    k2_tflops = fm["flops_k2"] * ne_local / (k2_ms * 1e-3) / 1e12
+    traffic = None
+    prof = os.path.join(ROOT, "profiles", "k_residual_p4_traffic.json")
+    if os.path.exists(prof):
+        with open(prof) as f:
+            tr = json.load(f)
+        traffic = tr.get("dram_bytes_per_element", 0) * ne_local
+    out = {
+        "metric": METRIC, "value": value, "unit": UNIT, "n_gpus": world, "steps": args.steps,
+        "warmup": args.warmup, "ms_per_step": ms_max / args.steps, "higher_is_better": True,
+        "scaling": "strong", "vs_baseline": None, "dtype": "f64",
+        "data": "synthetic (analytic isentropic vortex IC on the reference's warped grid)",
+        "config": {"workload": WORKLOAD, "elements": f"{M}^3", "p": P_DEG, "c1d": C_PLUS4,
+                   "surface_flux": "EC+Roe", "parallelism": f"z-slab x{world}",
+                   "l2_flush": "inputs larger than L2 (state 10.5 GB per copy)"},
+        "roofline": {"bound": "fp64", "achieved": k2_tflops, "peak": fp64_peak, "unit": "TFLOP/s",
+                     "frac": k2_tflops / fp64_peak, "traffic": traffic,
+                     "kernel": f"k_residual<{P_DEG + 1}>",
+                     "peak_source": "measured live: DFMA loop (nsfr_gpu_measure_fp64_peak); "
+                                    "MEASURED_PEAKS.json has no fp64 entry",
+                     "flops_per_element": fm["flops_k2"], "elements_per_launch": ne_local,
+                     "launch_ms": k2_ms, "k1_launch_ms": k1_ms,
+                     "step_frac": (fm["flops_total"] * ne_local * 4 * args.steps / (ms_total * 1e-3) / 1e12)
+                     / fp64_peak,
+                     "hbm_b_alg_gbs": bytes_per_element(P_DEG)["b_alg"] * ne_local / (
+                         (k1_ms + k2_ms) * 1e-3) / 1e9,
+                     "hbm_peak_gbs": read_peaks().get("hbm_gbs")},
+        "clocks": clk.summary(),
+        "e2e": {"value": e2e_val, "unit": UNIT, "h2d_bytes_per_step": state_bytes,
+                "d2h_bytes_per_step": state_bytes, "steps": e2e_steps},
+        "gpu_launches": int(launches),
+    }
+    if rank == 0 and world == 1 and not args.no_cpu_baseline:
+        threads = os.cpu_count() or 1
+        val, sec, kind, cores = cpu_reference_run(1, 1, threads)
+        out["cpu_baseline"] = {"value": val, "unit": UNIT, "cores": cores, "kind": kind,
+                               "sample": f"1 RK4 step (4 RHS) on a periodic {CPU_SAMPLE_M}^3 box, "
+                                         f"same p=4/c_+/EC+Roe per-element work, {cores} threads"}
+    g.close()
+    if rank == 0:
+        print(json.dumps(out), flush=True)
+    if world > 1:
+        import torch.distributed as dist
+        dist.barrier()
+        dist.destroy_process_group()
+
+
+def main():
+    ap = argparse.ArgumentParser()
+    ap.add_argument("--gpus", type=int, default=1)
+    ap.add_argument("--steps", type=int, default=10)
+    ap.add_argument("--warmup", type=int, default=3)
+    ap.add_argument("--impl", default="b200", choices=["b200", "reference"])
+    ap.add_argument("--no-cpu-baseline", action="store_true")
+    args = ap.parse_args()
+    if args.impl == "reference":
+        run_reference_arm(args)
+    else:
+        run_gpu_arm(args)
+
+
+if __name__ == "__main__":
+    main()

@@ -1,0 +1,165 @@
+/*
+ * nsfr_gpu.h — C ABI of the B200-native NSFR residual path (libnsfr_b200.so).
+ *
+ * This is the drop-in boundary for the reference's MISSING solver layer
+ * (proj/CMakeLists.txt:26 lists src/solver.cpp, which is absent; its contract
+ * is SPEC.md:422-518 and PAPER.md:869-929). Each entry point names the
+ * reference interface it replaces:
+ *
+ *   nsfr_gpu_create        build_reference_operators (fr_operators.cpp:89-113)
+ *                          + warp_grid_3d (geometry.cpp:62-73)
+ *                          + build_metrics_conservative_curl (geometry.cpp:86-266),
+ *                          or adopts caller-built tables/metrics (setup fields)
+ *   nsfr_gpu_set_state     ConservativeField upload (layout sumfac.hpp:46,86-87)
+ *   nsfr_gpu_init_case     CaseSpec::initial at the solution nodes (cases.cpp:78-101)
+ *   nsfr_gpu_rhs           nsfr_residual / assemble_rhs: entropy
+ *                          projection + hadamard_sumfac_volume
+ *                          (sumfac.hpp:48-94) + hadamard_sumfac_surface
+ *                          (sumfac.hpp:110-157) + EC/Roe face flux (euler.cpp:142-162,
+ *                          229-301) + weight_adjusted_inverse_apply (fr_operators.cpp:280-309)
+ *   nsfr_gpu_rk4_step      rk4_step + adaptive_dt
+ *   nsfr_gpu_advance       run_simulation's stepping loop
+ *   nsfr_gpu_l2_error      l2_error
+ *   nsfr_gpu_entropy_change discrete_entropy_change
+ *
+ * Conventions: every call returns int (NSFR_OK or an NSFR_E_* code); no C++
+ * exception crosses the ABI; nsfr_gpu_last_error() describes the last failure.
+ * Host pointers are borrowed for the duration of the call and copied. A
+ * context is single-threaded and stream-ordered; one context per GPU.
+ * Layouts: state [e_local][5][(p+1)^3] (modal = nodal values at the LGL
+ * solution nodes), jac [e_local][nq^3], cof [e_local][nq^3][9] with
+ * cof[3*n_phys + i_ref] exactly as ElementMetrics::cof_vol (geometry.hpp:66-80).
+ * Elements are numbered e = i + m*(j + m*k) (geometry.hpp:16-22); a rank owns
+ * the z-slab k in [k0, k1).
+ */
+#ifndef NSFR_GPU_H
+#define NSFR_GPU_H
+
+#include <stddef.h>
+
+#ifdef __cplusplus
+extern "C" {
+#endif
+
+#define NSFR_OK 0
+#define NSFR_E_DIM 1          /* DimensionError (defs.hpp:12-14) */
+#define NSFR_E_MESH 2         /* InvalidMeshError (defs.hpp:16-18) */
+#define NSFR_E_INADMISSIBLE 3 /* InadmissibleStateError / StepFailureError{t} (defs.hpp:20-28) */
+#define NSFR_E_CUDA 4
+#define NSFR_E_NCCL 5
+#define NSFR_E_CONFIG 6       /* ConfigError (defs.hpp:30-32) */
+
+#define NSFR_CASE_VORTEX 0     /* isentropic_vortex_exact, cases.cpp:36-56 */
+#define NSFR_CASE_TGV 1        /* tgv_initial, cases.cpp:7-14 */
+#define NSFR_CASE_FREESTREAM 2 /* CaseSpec free stream, cases.hpp:24-28 */
+
+typedef struct nsfr_gpu_ctx nsfr_gpu_ctx;
+
+/* Optional caller-built 1D tables (ReferenceOperators, fr_operators.hpp:40-57),
+ * row-major. When `interp` is NULL the library builds them natively. */
+typedef struct nsfr_gpu_tables {
+  const double* interp;     /* basis.interp  chi(xi_v)   nq x np */
+  const double* proj;       /* proj          Pi          np x nq */
+  const double* fr_proj;    /* fr_proj       Pi~         np x nq */
+  const double* skew;       /* skew   W Dq - Dq^T W      nq x nq */
+  const double* bound_flux; /* bound_flux                2 x nq  */
+  const double* bound_sol;  /* bound_sol                 2 x np  */
+  const double* wq;         /* wq                        nq      */
+} nsfr_gpu_tables;
+
+typedef struct nsfr_gpu_setup {
+  int p;               /* polynomial degree; np = nq = p+1 (no overintegration) */
+  int quad_kind;       /* 0 Gauss-Legendre, 1 Gauss-Lobatto-Legendre */
+  double c1d;          /* ESFR parameter, this code's convention (fr_operators.cpp:17-46) */
+  double gamma;        /* EulerGas::gamma (euler.hpp:14-16) */
+  int roe;             /* 1: EC + Roe surface flux, 0: EC only */
+  int m;               /* elements per direction of the periodic m^3 box */
+  int k0, k1;          /* this rank's z-slab [k0,k1) */
+  double x_left, x_right;
+  double beta;         /* warp amplitude (warp_grid_3d) */
+  double length_scale; /* <= 0: (x_right-x_left)/(2 pi) */
+  int grid_degree;     /* mapping degree, reference default p+1 (geometry.hpp:50-51) */
+  int device;          /* CUDA device ordinal */
+  int entropy_diag;    /* keep v_hat for nsfr_gpu_entropy_change */
+  /* optional caller-built data (copied): tables and/or metrics of the slab */
+  const nsfr_gpu_tables* tables;
+  const double* jac_vol;  /* [e_local][nq^3]     or NULL: built on the device */
+  const double* cof_vol;  /* [e_local][nq^3][9]  or NULL */
+  /* multi-GPU: an NCCL unique id from nsfr_gpu_nccl_unique_id on rank 0,
+   * broadcast by the caller; NULL for a single rank */
+  const void* nccl_id;
+  int rank, nranks;
+} nsfr_gpu_setup;
+
+int nsfr_gpu_create(const nsfr_gpu_setup* setup, nsfr_gpu_ctx** out);
+int nsfr_gpu_destroy(nsfr_gpu_ctx* ctx);
+const char* nsfr_gpu_last_error(const nsfr_gpu_ctx* ctx);
+/* Last error of a failed nsfr_gpu_create (no context exists then). */
+const char* nsfr_gpu_create_error(void);
+
+/* 128-byte NCCL unique id (call on rank 0, broadcast to the others). */
+int nsfr_gpu_nccl_unique_id(void* out128);
+
+/* Halo plan of a z-slab decomposition (pure host logic, no GPU needed):
+ * the slab of `rank`, the peers it exchanges face traces with, and the
+ * message size in doubles. */
+typedef struct nsfr_gpu_halo_plan {
+  int k0, k1;        /* z planes owned */
+  int peer_lo;       /* rank owning plane k0-1 (periodic) */
+  int peer_hi;       /* rank owning plane k1 (periodic) */
+  long long count;   /* doubles per message: m*m*5*nq*nq */
+} nsfr_gpu_halo_plan;
+int nsfr_gpu_halo_plan_for(int m, int p, int rank, int nranks, nsfr_gpu_halo_plan* out);
+
+/* Tables actually used (for parity checks): packed like nsfr_gpu_tables. */
+int nsfr_gpu_get_tables(nsfr_gpu_ctx* ctx, double* out, int cap);
+int nsfr_gpu_get_metrics(nsfr_gpu_ctx* ctx, double* jac, double* cof);
+
+int nsfr_gpu_set_state(nsfr_gpu_ctx* ctx, const double* u);
+int nsfr_gpu_get_state(nsfr_gpu_ctx* ctx, double* u);
+int nsfr_gpu_init_case(nsfr_gpu_ctx* ctx, int case_kind);
+int nsfr_gpu_set_time(nsfr_gpu_ctx* ctx, double t);
+int nsfr_gpu_get_time(nsfr_gpu_ctx* ctx, double* t);
+
+/* One residual dU/dt of the current state; dudt may be NULL (kept on device).
+ * entropy_change may be NULL; else receives -sum v_hat . R (allreduced). */
+int nsfr_gpu_rhs(nsfr_gpu_ctx* ctx, double* dudt, double* entropy_change);
+/* Entropy-projected face traces of the local elements [e][6][5][nq^2]. */
+int nsfr_gpu_get_traces(nsfr_gpu_ctx* ctx, double* traces);
+
+/* One classical RK4 step; dt = cfl*dx/lambda_max (allreduced) from u_n,
+ * dx = (x_right-x_left)/(m(p+1)), clipped to t_final - t (t_final <= 0: no clip). */
+int nsfr_gpu_rk4_step(nsfr_gpu_ctx* ctx, double cfl, double t_final, double* dt_used);
+/* nsteps RK4 steps without host synchronisation between them (CUDA graph). */
+int nsfr_gpu_advance(nsfr_gpu_ctx* ctx, int nsteps, double cfl, double t_final, double* t_out);
+/* Fixed dt variant (no wavespeed reduction): used by the parity tests. */
+int nsfr_gpu_rk4_step_dt(nsfr_gpu_ctx* ctx, double dt);
+int nsfr_gpu_max_wavespeed(nsfr_gpu_ctx* ctx, double* lam);
+
+/* L2 density/pressure error against the case's exact solution at the
+ * context time (allreduced sums; returns the square roots). */
+int nsfr_gpu_l2_error(nsfr_gpu_ctx* ctx, int case_kind, double out2[2]);
+/* -sum v_hat . R of the last RHS of the current state (allreduced). */
+int nsfr_gpu_entropy_change(nsfr_gpu_ctx* ctx, double* out);
+
+/* Bench helper: time nsteps RK4 steps (t_final unbounded) with CUDA events on
+ * the context stream; inputs stay resident in HBM. kernel_ms (optional, [2])
+ * receives the summed durations of the K1 (projection) and K2 (residual)
+ * launches, each bracketed by its own events (disables the step graph). */
+int nsfr_gpu_time_steps(nsfr_gpu_ctx* ctx, int nsteps, double cfl, double* step_ms, double* kernel_ms);
+
+/* FP64 pipe peak of `device` in TFLOP/s (DFMA loop; roofline denominator). */
+int nsfr_gpu_measure_fp64_peak(int device, double* tflops);
+
+/* Device pointers (for callers that keep inputs resident in HBM). */
+double* nsfr_gpu_state_device_ptr(nsfr_gpu_ctx* ctx);
+size_t nsfr_gpu_state_count(const nsfr_gpu_ctx* ctx);
+/* Synchronise and report a pending device error (NSFR_E_INADMISSIBLE...). */
+int nsfr_gpu_sync(nsfr_gpu_ctx* ctx);
+/* Kernel launches issued so far by this context (for the bench's claim). */
+long long nsfr_gpu_launch_count(const nsfr_gpu_ctx* ctx);
+
+#ifdef __cplusplus
+}
+#endif
+#endif

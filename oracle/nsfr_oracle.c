@@ -1031,6 +1031,14 @@ static int project_all(Ctx* c, const double* u) {
   return NSFR_OK;
 }
 
+int nsfr_oracle_traces(void* ctx, const double* u, double* traces) {
+  Ctx* c = (Ctx*)ctx;
+  int rc = project_all(c, u);
+  if (rc) return rc;
+  memcpy(traces, c->ut_f, sizeof(double) * c->ne * 6 * NS * c->nf);
+  return NSFR_OK;
+}
+
 int nsfr_oracle_boundary_traces(void* ctx, const double* u, double* send_lo, double* send_hi) {
   Ctx* c = (Ctx*)ctx;
   int rc = project_all(c, u);

@@ -69,6 +69,8 @@ int NSFR_CPU_API(metrics)(void* ctx, double* jac, double* cof);
 int NSFR_CPU_API(x_sol)(void* ctx, double* x);  /* [e][np^3][3] */
 int NSFR_CPU_API(x_vol)(void* ctx, double* x);  /* [e][nq^3][3] */
 int NSFR_CPU_API(initial_state)(void* ctx, int case_kind, double* u);
+/* Entropy-projected face traces of all local elements [e][6][5][nq^2]. */
+int NSFR_CPU_API(traces)(void* ctx, const double* u, double* traces);
 /* Face traces of the plane-boundary elements for a halo exchange. */
 int NSFR_CPU_API(boundary_traces)(void* ctx, const double* u, double* send_lo, double* send_hi);
 /* Full residual; halo pointers may be NULL only when the slab is the box. */

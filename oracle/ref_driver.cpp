@@ -384,6 +384,14 @@ int nsfr_ref_initial_state(void* ctx, int kind, double* u) {
   return NSFR_OK;
 }
 
+int nsfr_ref_traces(void* ctx, const double* u, double* traces) {
+  RefCtx& c = *static_cast<RefCtx*>(ctx);
+  int rc = project_all(c, u);
+  if (rc) return rc;
+  std::memcpy(traces, c.ut_f.data(), sizeof(double) * c.ut_f.size());
+  return NSFR_OK;
+}
+
 int nsfr_ref_boundary_traces(void* ctx, const double* u, double* send_lo, double* send_hi) {
   RefCtx& c = *static_cast<RefCtx*>(ctx);
   int rc = project_all(c, u);

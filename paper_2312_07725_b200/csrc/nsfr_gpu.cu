@@ -1,0 +1,805 @@
+// nsfr_gpu.cu — context, C ABI (include/nsfr_gpu.h), launch plumbing, NCCL halo
+// exchange and reductions for the B200-native NSFR residual path.
+#include <cuda_runtime.h>
+#include <nccl.h>
+
+#include <algorithm>
+#include <cmath>
+#include <cstdio>
+#include <cstring>
+#include <string>
+#include <vector>
+
+#include "../../include/nsfr_gpu.h"
+#include "kernels.cuh"
+#include "tables.hpp"
+
+using namespace nsfr_b200;
+
+struct nsfr_gpu_ctx {
+  nsfr_gpu_setup s{};
+  int N = 0, E = 0, m = 0, nz = 0, k0 = 0, k1 = 0;
+  Tables1D tab;
+  DevTables* d_tab = nullptr;
+  double *d_un = nullptr, *d_us = nullptr, *d_acc = nullptr, *d_rhs = nullptr;
+  double *d_utv = nullptr, *d_tr = nullptr, *d_cof = nullptr, *d_jac = nullptr, *d_wj = nullptr;
+  double *d_vhat = nullptr, *d_dS = nullptr, *d_part = nullptr, *d_red = nullptr;
+  double *d_send_lo = nullptr, *d_send_hi = nullptr, *d_halo_lo = nullptr, *d_halo_hi = nullptr;
+  StepState* d_step = nullptr;
+  StepState* h_step = nullptr;  // pinned
+  unsigned* d_err = nullptr;
+  unsigned* h_err = nullptr;    // pinned
+  cudaStream_t st = nullptr;
+  ncclComm_t comm = nullptr;
+  int rank = 0, nranks = 1, peer_lo = 0, peer_hi = 0;
+  long long halo_count = 0;
+  cudaGraphExec_t graph = nullptr;
+  long long launches = 0;
+  // per-launch event timing (bench roofline)
+  bool timing = false;
+  std::vector<cudaEvent_t> ev_pool;
+  std::vector<std::pair<int, int>> ev_marks;  // (kind, index of start event)
+  std::string msg;
+};
+
+namespace {
+
+thread_local std::string g_create_error;
+
+#define CK(call)                                                                          \
+  do {                                                                                    \
+    cudaError_t e_ = (call);                                                              \
+    if (e_ != cudaSuccess) {                                                              \
+      ctx->msg = std::string(#call) + ": " + cudaGetErrorString(e_);                      \
+      return NSFR_E_CUDA;                                                                 \
+    }                                                                                     \
+  } while (0)
+
+#define NK(call)                                                                          \
+  do {                                                                                    \
+    ncclResult_t r_ = (call);                                                             \
+    if (r_ != ncclSuccess) {                                                              \
+      ctx->msg = std::string(#call) + ": " + ncclGetErrorString(r_);                      \
+      return NSFR_E_NCCL;                                                                 \
+    }                                                                                     \
+  } while (0)
+
+size_t nsol(const nsfr_gpu_ctx* c) { return static_cast<size_t>(c->N) * c->N * c->N; }
+size_t state_count(const nsfr_gpu_ctx* c) { return static_cast<size_t>(c->E) * NS * nsol(c); }
+
+template <int N>
+int set_attrs(nsfr_gpu_ctx* ctx) {
+  static bool done = false;
+  if (done) return NSFR_OK;
+  CK(cudaFuncSetAttribute(k_project<N>, cudaFuncAttributeMaxDynamicSharedMemorySize, ProjCfg<N>::SMEM));
+  CK(cudaFuncSetAttribute(k_residual<N>, cudaFuncAttributeMaxDynamicSharedMemorySize, ResCfg<N>::SMEM));
+  done = true;
+  return NSFR_OK;
+}
+
+void ev_begin(nsfr_gpu_ctx* c, int kind) {
+  if (!c->timing) return;
+  cudaEvent_t a, b;
+  cudaEventCreate(&a);
+  cudaEventCreate(&b);
+  c->ev_marks.push_back({kind, static_cast<int>(c->ev_pool.size())});
+  c->ev_pool.push_back(a);
+  c->ev_pool.push_back(b);
+  cudaEventRecord(a, c->st);
+}
+void ev_end(nsfr_gpu_ctx* c) {
+  if (!c->timing) return;
+  cudaEventRecord(c->ev_pool.back(), c->st);
+}
+
+template <int N>
+int launch_project(nsfr_gpu_ctx* ctx, const double* u, bool want_lam) {
+  if (int rc = set_attrs<N>(ctx)) return rc;
+  ProjParams P{};
+  P.tab = ctx->d_tab;
+  P.u = u;
+  P.ut_vol = ctx->d_utv;
+  P.traces = ctx->d_tr;
+  P.vhat = ctx->d_vhat;
+  P.send_lo = ctx->nranks > 1 ? ctx->d_send_lo : nullptr;
+  P.send_hi = ctx->nranks > 1 ? ctx->d_send_hi : nullptr;
+  P.lam = want_lam ? &ctx->d_step->lam_bits : nullptr;
+  P.err = ctx->d_err;
+  P.E = ctx->E;
+  P.m = ctx->m;
+  P.nz = ctx->nz;
+  P.gamma = ctx->s.gamma;
+  const int grid = (ctx->E + ProjCfg<N>::EPB - 1) / ProjCfg<N>::EPB;
+  ev_begin(ctx, 1);
+  k_project<N><<<grid, ProjCfg<N>::THREADS, ProjCfg<N>::SMEM, ctx->st>>>(P);
+  ev_end(ctx);
+  ++ctx->launches;
+  CK(cudaGetLastError());
+  return NSFR_OK;
+}
+
+template <int N>
+int launch_residual(nsfr_gpu_ctx* ctx, int stage, bool entropy) {
+  ResParams P{};
+  P.tab = ctx->d_tab;
+  P.ut_vol = ctx->d_utv;
+  P.traces = ctx->d_tr;
+  P.halo_lo = ctx->nranks > 1 ? ctx->d_halo_lo : nullptr;
+  P.halo_hi = ctx->nranks > 1 ? ctx->d_halo_hi : nullptr;
+  P.cof = ctx->d_cof;
+  P.wj = ctx->d_wj;
+  P.vhat = entropy ? ctx->d_vhat : nullptr;
+  P.dS = entropy ? ctx->d_dS : nullptr;
+  P.un = ctx->d_un;
+  P.us = ctx->d_us;
+  P.acc = ctx->d_acc;
+  P.out = ctx->d_rhs;
+  P.dt = &ctx->d_step->dt;
+  P.err = ctx->d_err;
+  P.stage = stage;
+  P.E = ctx->E;
+  P.m = ctx->m;
+  P.nz = ctx->nz;
+  P.gamma = ctx->s.gamma;
+  P.roe = ctx->s.roe;
+  const int grid = (ctx->E + ResCfg<N>::EPB - 1) / ResCfg<N>::EPB;
+  ev_begin(ctx, 2);
+  k_residual<N><<<grid, ResCfg<N>::THREADS, ResCfg<N>::SMEM, ctx->st>>>(P);
+  ev_end(ctx);
+  ++ctx->launches;
+  CK(cudaGetLastError());
+  return NSFR_OK;
+}
+
+int project(nsfr_gpu_ctx* ctx, const double* u, bool lam) {
+  switch (ctx->N) {
+    case 3: return launch_project<3>(ctx, u, lam);
+    case 4: return launch_project<4>(ctx, u, lam);
+    case 5: return launch_project<5>(ctx, u, lam);
+    case 6: return launch_project<6>(ctx, u, lam);
+    case 7: return launch_project<7>(ctx, u, lam);
+  }
+  ctx->msg = "unsupported p";
+  return NSFR_E_DIM;
+}
+
+int residual(nsfr_gpu_ctx* ctx, int stage, bool entropy) {
+  switch (ctx->N) {
+    case 3: return launch_residual<3>(ctx, stage, entropy);
+    case 4: return launch_residual<4>(ctx, stage, entropy);
+    case 5: return launch_residual<5>(ctx, stage, entropy);
+    case 6: return launch_residual<6>(ctx, stage, entropy);
+    case 7: return launch_residual<7>(ctx, stage, entropy);
+  }
+  ctx->msg = "unsupported p";
+  return NSFR_E_DIM;
+}
+
+// z-face halo exchange with the two slab neighbours
+int exchange(nsfr_gpu_ctx* ctx) {
+  if (ctx->nranks <= 1) return NSFR_OK;
+  const size_t n = static_cast<size_t>(ctx->halo_count);
+  NK(ncclGroupStart());
+  NK(ncclSend(ctx->d_send_lo, n, ncclDouble, ctx->peer_lo, ctx->comm, ctx->st));
+  NK(ncclRecv(ctx->d_halo_hi, n, ncclDouble, ctx->peer_hi, ctx->comm, ctx->st));
+  NK(ncclSend(ctx->d_send_hi, n, ncclDouble, ctx->peer_hi, ctx->comm, ctx->st));
+  NK(ncclRecv(ctx->d_halo_lo, n, ncclDouble, ctx->peer_lo, ctx->comm, ctx->st));
+  NK(ncclGroupEnd());
+  return NSFR_OK;
+}
+
+int allreduce_sum(nsfr_gpu_ctx* ctx, double* d, int n) {
+  if (ctx->nranks <= 1) return NSFR_OK;
+  NK(ncclAllReduce(d, d, n, ncclDouble, ncclSum, ctx->comm, ctx->st));
+  return NSFR_OK;
+}
+
+// one full residual of `u` into d_rhs (stage 0)
+int rhs_of(nsfr_gpu_ctx* ctx, const double* u, bool entropy) {
+  if (int rc = project(ctx, u, false)) return rc;
+  if (int rc = exchange(ctx)) return rc;
+  return residual(ctx, 0, entropy);
+}
+
+// enqueue one RK4 step (no host sync). fixed_dt: dt already in d_step.
+int enqueue_step(nsfr_gpu_ctx* ctx, bool fixed_dt) {
+  if (!fixed_dt) {
+    k_step_begin<<<1, 1, 0, ctx->st>>>(ctx->d_step);
+    ++ctx->launches;
+  }
+  if (int rc = project(ctx, ctx->d_un, !fixed_dt)) return rc;
+  if (!fixed_dt) {
+    if (ctx->nranks > 1)
+      NK(ncclAllReduce(&ctx->d_step->lam_bits, &ctx->d_step->lam_bits, 1, ncclUint64, ncclMax,
+                       ctx->comm, ctx->st));
+    k_step_dt<<<1, 1, 0, ctx->st>>>(ctx->d_step);
+    ++ctx->launches;
+  }
+  if (int rc = exchange(ctx)) return rc;
+  if (int rc = residual(ctx, 1, false)) return rc;
+  for (int stage = 2; stage <= 4; ++stage) {
+    if (int rc = project(ctx, ctx->d_us, false)) return rc;
+    if (int rc = exchange(ctx)) return rc;
+    if (int rc = residual(ctx, stage, false)) return rc;
+  }
+  k_step_end<<<1, 1, 0, ctx->st>>>(ctx->d_step);
+  ++ctx->launches;
+  CK(cudaGetLastError());
+  return NSFR_OK;
+}
+
+// synchronise and translate the device error word
+int sync_check(nsfr_gpu_ctx* ctx) {
+  CK(cudaMemcpyAsync(ctx->h_err, ctx->d_err, sizeof(unsigned), cudaMemcpyDeviceToHost, ctx->st));
+  CK(cudaMemcpyAsync(ctx->h_step, ctx->d_step, sizeof(StepState), cudaMemcpyDeviceToHost, ctx->st));
+  CK(cudaStreamSynchronize(ctx->st));
+  const unsigned e = *ctx->h_err;
+  if (e) {
+    CK(cudaMemsetAsync(ctx->d_err, 0, sizeof(unsigned), ctx->st));
+    CK(cudaStreamSynchronize(ctx->st));
+    if (e & ERR_MESH) {
+      ctx->msg = "nonpositive metric Jacobian or degenerate face (InvalidMeshError)";
+      return NSFR_E_MESH;
+    }
+    char buf[160];
+    std::snprintf(buf, sizeof buf, "inadmissible state at t=%.17g (StepFailureError)%s",
+                  ctx->h_step->t, (e & ERR_ROE) ? " [Roe average]" : "");
+    ctx->msg = buf;
+    return NSFR_E_INADMISSIBLE;
+  }
+  return NSFR_OK;
+}
+
+void fill_dev_tables(const Tables1D& t, const nsfr_gpu_tables* user, DevTables& d) {
+  std::memset(&d, 0, sizeof d);
+  const int np = t.np, nq = t.nq;
+  d.np = np;
+  d.nq = nq;
+  d.g = t.g;
+  const double* interp = user ? user->interp : t.interp.data();
+  const double* proj = user ? user->proj : t.proj.data();
+  const double* frp = user ? user->fr_proj : t.fr_proj.data();
+  const double* skew = user ? user->skew : t.skew.data();
+  const double* bflux = user ? user->bound_flux : t.bound_flux.data();
+  const double* bsol = user ? user->bound_sol : t.bound_sol.data();
+  const double* wq = user ? user->wq : t.wq.data();
+  for (int i = 0; i < nq * np; ++i) d.interp[i] = interp[i];
+  for (int i = 0; i < nq; ++i)
+    for (int j = 0; j < np; ++j) d.interp_t[j * nq + i] = interp[i * np + j];
+  for (int i = 0; i < np * nq; ++i) {
+    d.proj[i] = proj[i];
+    d.frproj[i] = frp[i];
+  }
+  for (int i = 0; i < np; ++i)
+    for (int j = 0; j < nq; ++j) d.frproj_t[j * np + i] = frp[i * nq + j];
+  for (int a = 0; a < nq; ++a)
+    for (int b = 0; b < nq; ++b) {
+      // hadamard_sumfac_volume called with 0.5*skew (D2): q(a,b) - q(b,a)
+      const double qab = 0.5 * skew[a * nq + b], qba = 0.5 * skew[b * nq + a];
+      d.qskew[a * nq + b] = qab - qba;
+    }
+  for (int i = 0; i < 2 * nq; ++i) d.bflux[i] = bflux[i];
+  for (int i = 0; i < 2 * np; ++i) d.bsol[i] = bsol[i];
+  for (int i = 0; i < nq; ++i) d.wq[i] = wq[i];
+  for (int i = 0; i < nq * nq; ++i) d.quad_diff[i] = t.quad_diff[i];
+  for (int i = 0; i < t.g; ++i) d.gnodes[i] = t.grid_nodes[i];
+  for (int i = 0; i < nq * t.g; ++i) d.ig[i] = t.ig[i];
+  for (int i = 0; i < np * t.g; ++i) d.is[i] = t.is[i];
+  for (int i = 0; i < t.g * t.g; ++i) d.dg[i] = t.dg[i];
+}
+
+double length_scale(const nsfr_gpu_setup& s) {
+  return s.length_scale > 0.0 ? s.length_scale : (s.x_right - s.x_left) / (2.0 * M_PI);
+}
+
+int setup_kernel_smem(nsfr_gpu_ctx* ctx, size_t bytes, const void* fn) {
+  if (bytes > 48 * 1024) CK(cudaFuncSetAttribute(fn, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)bytes));
+  return NSFR_OK;
+}
+
+int build_metrics(nsfr_gpu_ctx* ctx) {
+  const int g = ctx->tab.g, n = ctx->N, G3 = g * g * g, N3 = n * n * n;
+  const int M = std::max(g, n), M3 = M * M * M;
+  const size_t smem = sizeof(double) * (13 * G3 + 2 * M3 + 20 * N3);
+  if (int rc = setup_kernel_smem(ctx, smem, (const void*)k_metrics)) return rc;
+  MetricParams P{};
+  P.tab = ctx->d_tab;
+  P.jac = ctx->d_jac;
+  P.cof = ctx->d_cof;
+  P.wj = ctx->d_wj;
+  P.E = ctx->E;
+  P.m = ctx->m;
+  P.k0 = ctx->k0;
+  P.x_left = ctx->s.x_left;
+  P.h = (ctx->s.x_right - ctx->s.x_left) / ctx->m;
+  P.beta = ctx->s.beta;
+  P.l = length_scale(ctx->s);
+  P.err = ctx->d_err;
+  k_metrics<<<ctx->E, 128, smem, ctx->st>>>(P);
+  ++ctx->launches;
+  CK(cudaGetLastError());
+  return sync_check(ctx);
+}
+
+}  // namespace
+
+extern "C" {
+
+const char* nsfr_gpu_create_error(void) { return g_create_error.c_str(); }
+
+int nsfr_gpu_nccl_unique_id(void* out128) {
+  ncclUniqueId id;
+  if (ncclGetUniqueId(&id) != ncclSuccess) return NSFR_E_NCCL;
+  std::memcpy(out128, &id, sizeof id);
+  return NSFR_OK;
+}
+
+int nsfr_gpu_halo_plan_for(int m, int p, int rank, int nranks, nsfr_gpu_halo_plan* out) {
+  if (nranks < 1 || rank < 0 || rank >= nranks || m < nranks || p < 1) return NSFR_E_DIM;
+  out->k0 = static_cast<int>(static_cast<long long>(rank) * m / nranks);
+  out->k1 = static_cast<int>(static_cast<long long>(rank + 1) * m / nranks);
+  out->peer_lo = (rank - 1 + nranks) % nranks;
+  out->peer_hi = (rank + 1) % nranks;
+  out->count = static_cast<long long>(m) * m * NS * (p + 1) * (p + 1);
+  return NSFR_OK;
+}
+
+int nsfr_gpu_create(const nsfr_gpu_setup* setup, nsfr_gpu_ctx** out) {
+  *out = nullptr;
+  auto* ctx = new nsfr_gpu_ctx();
+  ctx->s = *setup;
+  auto fail = [&](int rc) {
+    g_create_error = ctx->msg;
+    nsfr_gpu_destroy(ctx);
+    return rc;
+  };
+  const nsfr_gpu_setup& s = ctx->s;
+  if (s.p < 2 || s.p > 6 || s.m < 1 || s.k0 < 0 || s.k1 > s.m || s.k0 >= s.k1 ||
+      !(s.quad_kind == 0 || s.quad_kind == 1) || s.grid_degree < 1 || s.grid_degree + 1 > MAXG ||
+      !(s.gamma > 1.0) || !(s.x_right > s.x_left) || s.beta < 0.0) {
+    ctx->msg = "nsfr_gpu_create: dimension/configuration out of range (p in [2,6], 0<=k0<k1<=m)";
+    return fail(NSFR_E_DIM);
+  }
+  ctx->N = s.p + 1;
+  ctx->m = s.m;
+  ctx->k0 = s.k0;
+  ctx->k1 = s.k1;
+  ctx->nz = s.k1 - s.k0;
+  ctx->E = s.m * s.m * ctx->nz;
+  ctx->rank = s.rank;
+  ctx->nranks = s.nranks < 1 ? 1 : s.nranks;
+  if (ctx->nranks == 1 && (s.k0 != 0 || s.k1 != s.m)) {
+    ctx->msg = "nsfr_gpu_create: a single rank must own the whole box";
+    return fail(NSFR_E_DIM);
+  }
+  const char* why = nullptr;
+  if (!build_tables(s.p, s.quad_kind, s.c1d, s.grid_degree, ctx->tab, &why)) {
+    ctx->msg = why;
+    return fail(NSFR_E_DIM);
+  }
+  if (cudaSetDevice(s.device) != cudaSuccess) {
+    ctx->msg = "cudaSetDevice failed (no CUDA device?)";
+    return fail(NSFR_E_CUDA);
+  }
+  if (cudaStreamCreateWithFlags(&ctx->st, cudaStreamNonBlocking) != cudaSuccess) {
+    ctx->msg = "cudaStreamCreate failed (no CUDA device?)";
+    return fail(NSFR_E_CUDA);
+  }
+  DevTables dt;
+  fill_dev_tables(ctx->tab, s.tables && s.tables->interp ? s.tables : nullptr, dt);
+  const size_t ns = state_count(ctx), n3 = static_cast<size_t>(ctx->E) * nsol(ctx);
+  const size_t ntr = static_cast<size_t>(ctx->E) * 6 * NS * ctx->N * ctx->N;
+  auto alloc = [&](double** p, size_t n) { return cudaMalloc(p, sizeof(double) * std::max<size_t>(n, 1)); };
+  if (cudaMalloc(&ctx->d_tab, sizeof(DevTables)) || alloc(&ctx->d_un, ns) || alloc(&ctx->d_us, ns) ||
+      alloc(&ctx->d_acc, ns) || alloc(&ctx->d_rhs, ns) || alloc(&ctx->d_utv, ns) ||
+      alloc(&ctx->d_tr, ntr) || alloc(&ctx->d_cof, 9 * n3) || alloc(&ctx->d_jac, n3) ||
+      alloc(&ctx->d_wj, n3) || alloc(&ctx->d_dS, ctx->E) || alloc(&ctx->d_part, 2 * (size_t)ctx->E) ||
+      alloc(&ctx->d_red, 4) || cudaMalloc(&ctx->d_step, sizeof(StepState)) ||
+      cudaMalloc(&ctx->d_err, sizeof(unsigned)) ||
+      cudaMallocHost(&ctx->h_step, sizeof(StepState)) || cudaMallocHost(&ctx->h_err, sizeof(unsigned))) {
+    ctx->msg = "nsfr_gpu_create: device allocation failed";
+    return fail(NSFR_E_CUDA);
+  }
+  if (s.entropy_diag && alloc(&ctx->d_vhat, ns)) {
+    ctx->msg = "nsfr_gpu_create: device allocation failed";
+    return fail(NSFR_E_CUDA);
+  }
+  if (ctx->nranks > 1) {
+    nsfr_gpu_halo_plan plan;
+    if (nsfr_gpu_halo_plan_for(s.m, s.p, ctx->rank, ctx->nranks, &plan) || plan.k0 != s.k0 ||
+        plan.k1 != s.k1) {
+      ctx->msg = "nsfr_gpu_create: slab does not match nsfr_gpu_halo_plan_for";
+      return fail(NSFR_E_DIM);
+    }
+    ctx->peer_lo = plan.peer_lo;
+    ctx->peer_hi = plan.peer_hi;
+    ctx->halo_count = plan.count;
+    if (alloc(&ctx->d_send_lo, plan.count) || alloc(&ctx->d_send_hi, plan.count) ||
+        alloc(&ctx->d_halo_lo, plan.count) || alloc(&ctx->d_halo_hi, plan.count)) {
+      ctx->msg = "nsfr_gpu_create: halo allocation failed";
+      return fail(NSFR_E_CUDA);
+    }
+    if (!s.nccl_id) {
+      ctx->msg = "nsfr_gpu_create: nranks > 1 needs an NCCL unique id";
+      return fail(NSFR_E_NCCL);
+    }
+    ncclUniqueId id;
+    std::memcpy(&id, s.nccl_id, sizeof id);
+    if (ncclCommInitRank(&ctx->comm, ctx->nranks, id, ctx->rank) != ncclSuccess) {
+      ctx->msg = "ncclCommInitRank failed";
+      return fail(NSFR_E_NCCL);
+    }
+  }
+  StepState h{};
+  h.dx = (s.x_right - s.x_left) / (s.m * (s.p + 1));
+  if (cudaMemcpyAsync(ctx->d_tab, &dt, sizeof dt, cudaMemcpyHostToDevice, ctx->st) ||
+      cudaMemcpyAsync(ctx->d_step, &h, sizeof h, cudaMemcpyHostToDevice, ctx->st) ||
+      cudaMemsetAsync(ctx->d_err, 0, sizeof(unsigned), ctx->st) ||
+      cudaStreamSynchronize(ctx->st)) {
+    ctx->msg = "nsfr_gpu_create: upload failed";
+    return fail(NSFR_E_CUDA);
+  }
+  if (setup->jac_vol && setup->cof_vol) {
+    // caller-built metrics (ElementMetrics layout [e][q][9]) -> [e][9][q], wj = w J
+    const int N3 = static_cast<int>(nsol(ctx));
+    std::vector<double> cof(9 * n3), wj(n3);
+    const auto& wq = (s.tables && s.tables->wq) ? std::vector<double>(s.tables->wq, s.tables->wq + ctx->N)
+                                                : ctx->tab.wq;
+    for (int e = 0; e < ctx->E; ++e)
+      for (int q = 0; q < N3; ++q) {
+        for (int c = 0; c < 9; ++c)
+          cof[(static_cast<size_t>(e) * 9 + c) * N3 + q] = setup->cof_vol[(static_cast<size_t>(e) * N3 + q) * 9 + c];
+        const int i = q % ctx->N, j = (q / ctx->N) % ctx->N, k = q / (ctx->N * ctx->N);
+        double w = wq[i];
+        w *= wq[j];
+        w *= wq[k];
+        const double J = setup->jac_vol[static_cast<size_t>(e) * N3 + q];
+        if (!(J > 0.0)) {
+          ctx->msg = "nsfr_gpu_create: nonpositive J in caller metrics";
+          return fail(NSFR_E_MESH);
+        }
+        wj[static_cast<size_t>(e) * N3 + q] = w * J;
+      }
+    if (cudaMemcpy(ctx->d_cof, cof.data(), sizeof(double) * cof.size(), cudaMemcpyHostToDevice) ||
+        cudaMemcpy(ctx->d_jac, setup->jac_vol, sizeof(double) * n3, cudaMemcpyHostToDevice) ||
+        cudaMemcpy(ctx->d_wj, wj.data(), sizeof(double) * n3, cudaMemcpyHostToDevice)) {
+      ctx->msg = "nsfr_gpu_create: metric upload failed";
+      return fail(NSFR_E_CUDA);
+    }
+  } else if (int rc = build_metrics(ctx)) {
+    return fail(rc);
+  }
+  *out = ctx;
+  return NSFR_OK;
+}
+
+int nsfr_gpu_destroy(nsfr_gpu_ctx* ctx) {
+  if (!ctx) return NSFR_OK;
+  if (ctx->st) cudaStreamSynchronize(ctx->st);
+  if (ctx->graph) cudaGraphExecDestroy(ctx->graph);
+  for (auto e : ctx->ev_pool) cudaEventDestroy(e);
+  if (ctx->comm) ncclCommDestroy(ctx->comm);
+  double* bufs[] = {ctx->d_un,  ctx->d_us,   ctx->d_acc,  ctx->d_rhs,     ctx->d_utv,     ctx->d_tr,
+                    ctx->d_cof, ctx->d_jac,  ctx->d_wj,   ctx->d_vhat,    ctx->d_dS,      ctx->d_part,
+                    ctx->d_red, ctx->d_send_lo, ctx->d_send_hi, ctx->d_halo_lo, ctx->d_halo_hi};
+  for (double* b : bufs)
+    if (b) cudaFree(b);
+  if (ctx->d_tab) cudaFree(ctx->d_tab);
+  if (ctx->d_step) cudaFree(ctx->d_step);
+  if (ctx->d_err) cudaFree(ctx->d_err);
+  if (ctx->h_step) cudaFreeHost(ctx->h_step);
+  if (ctx->h_err) cudaFreeHost(ctx->h_err);
+  if (ctx->st) cudaStreamDestroy(ctx->st);
+  delete ctx;
+  return NSFR_OK;
+}
+
+const char* nsfr_gpu_last_error(const nsfr_gpu_ctx* ctx) { return ctx ? ctx->msg.c_str() : "null context"; }
+
+int nsfr_gpu_get_tables(nsfr_gpu_ctx* ctx, double* out, int cap) {
+  const Tables1D& t = ctx->tab;
+  int pos = 0;
+  auto put = [&](const std::vector<double>& v) {
+    for (size_t i = 0; i < v.size(); ++i)
+      if (pos + static_cast<int>(i) < cap) out[pos + i] = v[i];
+    pos += static_cast<int>(v.size());
+  };
+  put(t.interp);
+  put(t.proj);
+  put(t.fr_proj);
+  put(t.skew);
+  put(t.bound_flux);
+  put(t.bound_sol);
+  put(t.wq);
+  put(t.quad_nodes);
+  put(t.sol_nodes);
+  put(t.mmass1d);
+  put(t.quad_diff);
+  return pos;
+}
+
+int nsfr_gpu_get_metrics(nsfr_gpu_ctx* ctx, double* jac, double* cof) {
+  const size_t n3 = static_cast<size_t>(ctx->E) * nsol(ctx);
+  const int N3 = static_cast<int>(nsol(ctx));
+  CK(cudaStreamSynchronize(ctx->st));
+  if (jac) CK(cudaMemcpy(jac, ctx->d_jac, sizeof(double) * n3, cudaMemcpyDeviceToHost));
+  if (cof) {
+    std::vector<double> c(9 * n3);
+    CK(cudaMemcpy(c.data(), ctx->d_cof, sizeof(double) * c.size(), cudaMemcpyDeviceToHost));
+    for (int e = 0; e < ctx->E; ++e)
+      for (int q = 0; q < N3; ++q)
+        for (int k = 0; k < 9; ++k)
+          cof[(static_cast<size_t>(e) * N3 + q) * 9 + k] = c[(static_cast<size_t>(e) * 9 + k) * N3 + q];
+  }
+  return NSFR_OK;
+}
+
+int nsfr_gpu_set_state(nsfr_gpu_ctx* ctx, const double* u) {
+  CK(cudaMemcpyAsync(ctx->d_un, u, sizeof(double) * state_count(ctx), cudaMemcpyHostToDevice, ctx->st));
+  CK(cudaStreamSynchronize(ctx->st));
+  return NSFR_OK;
+}
+
+int nsfr_gpu_get_state(nsfr_gpu_ctx* ctx, double* u) {
+  CK(cudaMemcpyAsync(u, ctx->d_un, sizeof(double) * state_count(ctx), cudaMemcpyDeviceToHost, ctx->st));
+  CK(cudaStreamSynchronize(ctx->st));
+  return NSFR_OK;
+}
+
+int nsfr_gpu_init_case(nsfr_gpu_ctx* ctx, int kind) {
+  const int g = ctx->tab.g, np = ctx->N, G3 = g * g * g, S3 = np * np * np;
+  const int M = std::max(g, np), M3 = M * M * M;
+  const size_t smem = sizeof(double) * (3 * G3 + 2 * M3 + 3 * S3);
+  if (int rc = setup_kernel_smem(ctx, smem, (const void*)k_init)) return rc;
+  InitParams P{};
+  P.tab = ctx->d_tab;
+  P.u = ctx->d_un;
+  P.E = ctx->E;
+  P.m = ctx->m;
+  P.k0 = ctx->k0;
+  P.kind = kind;
+  P.x_left = ctx->s.x_left;
+  P.h = (ctx->s.x_right - ctx->s.x_left) / ctx->m;
+  P.beta = ctx->s.beta;
+  P.l = length_scale(ctx->s);
+  P.gamma = ctx->s.gamma;
+  k_init<<<ctx->E, 128, smem, ctx->st>>>(P);
+  ++ctx->launches;
+  CK(cudaGetLastError());
+  return nsfr_gpu_set_time(ctx, 0.0);
+}
+
+int nsfr_gpu_set_time(nsfr_gpu_ctx* ctx, double t) {
+  CK(cudaMemcpyAsync(&ctx->d_step->t, &t, sizeof(double), cudaMemcpyHostToDevice, ctx->st));
+  CK(cudaStreamSynchronize(ctx->st));
+  return NSFR_OK;
+}
+
+int nsfr_gpu_get_time(nsfr_gpu_ctx* ctx, double* t) {
+  if (int rc = sync_check(ctx)) return rc;
+  *t = ctx->h_step->t;
+  return NSFR_OK;
+}
+
+int nsfr_gpu_rhs(nsfr_gpu_ctx* ctx, double* dudt, double* entropy_change) {
+  const bool ent = entropy_change != nullptr;
+  if (ent && !ctx->d_vhat) {
+    ctx->msg = "entropy change needs setup.entropy_diag = 1";
+    return NSFR_E_CONFIG;
+  }
+  if (int rc = rhs_of(ctx, ctx->d_un, ent)) return rc;
+  if (ent) {
+    k_reduce<<<1, 1024, 0, ctx->st>>>(ctx->d_dS, ctx->E, 1, ctx->d_red);
+    ++ctx->launches;
+    if (int rc = allreduce_sum(ctx, ctx->d_red, 1)) return rc;
+  }
+  if (int rc = sync_check(ctx)) return rc;
+  if (dudt) CK(cudaMemcpy(dudt, ctx->d_rhs, sizeof(double) * state_count(ctx), cudaMemcpyDeviceToHost));
+  if (ent) CK(cudaMemcpy(entropy_change, ctx->d_red, sizeof(double), cudaMemcpyDeviceToHost));
+  return NSFR_OK;
+}
+
+int nsfr_gpu_entropy_change(nsfr_gpu_ctx* ctx, double* out) { return nsfr_gpu_rhs(ctx, nullptr, out); }
+
+int nsfr_gpu_get_traces(nsfr_gpu_ctx* ctx, double* traces) {
+  CK(cudaStreamSynchronize(ctx->st));
+  CK(cudaMemcpy(traces, ctx->d_tr, sizeof(double) * ctx->E * 6 * NS * ctx->N * ctx->N,
+                cudaMemcpyDeviceToHost));
+  return NSFR_OK;
+}
+
+int nsfr_gpu_max_wavespeed(nsfr_gpu_ctx* ctx, double* lam) {
+  k_step_begin<<<1, 1, 0, ctx->st>>>(ctx->d_step);
+  ++ctx->launches;
+  if (int rc = project(ctx, ctx->d_un, true)) return rc;
+  if (ctx->nranks > 1)
+    NK(ncclAllReduce(&ctx->d_step->lam_bits, &ctx->d_step->lam_bits, 1, ncclUint64, ncclMax, ctx->comm, ctx->st));
+  if (int rc = sync_check(ctx)) return rc;
+  unsigned long long b = ctx->h_step->lam_bits;
+  std::memcpy(lam, &b, sizeof b);
+  return NSFR_OK;
+}
+
+int nsfr_gpu_rk4_step_dt(nsfr_gpu_ctx* ctx, double dt) {
+  CK(cudaMemcpyAsync(&ctx->d_step->dt, &dt, sizeof dt, cudaMemcpyHostToDevice, ctx->st));
+  if (int rc = enqueue_step(ctx, true)) return rc;
+  return sync_check(ctx);
+}
+
+static int set_step_params(nsfr_gpu_ctx* ctx, double cfl, double t_final) {
+  StepState* hs = ctx->h_step;
+  CK(cudaMemcpyAsync(hs, ctx->d_step, sizeof(StepState), cudaMemcpyDeviceToHost, ctx->st));
+  CK(cudaStreamSynchronize(ctx->st));
+  hs->cfl = cfl;
+  hs->t_final = t_final;
+  CK(cudaMemcpyAsync(ctx->d_step, hs, sizeof(StepState), cudaMemcpyHostToDevice, ctx->st));
+  return NSFR_OK;
+}
+
+int nsfr_gpu_rk4_step(nsfr_gpu_ctx* ctx, double cfl, double t_final, double* dt_used) {
+  if (int rc = set_step_params(ctx, cfl, t_final)) return rc;
+  if (int rc = enqueue_step(ctx, false)) return rc;
+  if (int rc = sync_check(ctx)) return rc;
+  if (dt_used) *dt_used = ctx->h_step->dt;
+  return NSFR_OK;
+}
+
+int nsfr_gpu_advance(nsfr_gpu_ctx* ctx, int nsteps, double cfl, double t_final, double* t_out) {
+  if (int rc = set_step_params(ctx, cfl, t_final)) return rc;
+  if (!ctx->graph && !ctx->timing) {
+    cudaGraph_t g;
+    CK(cudaStreamBeginCapture(ctx->st, cudaStreamCaptureModeThreadLocal));
+    const long long l0 = ctx->launches;
+    int rc = enqueue_step(ctx, false);
+    CK(cudaStreamEndCapture(ctx->st, &g));
+    if (rc) return rc;
+    CK(cudaGraphInstantiate(&ctx->graph, g, 0));
+    cudaGraphDestroy(g);
+    ctx->launches = l0;  // counted on replay
+  }
+  const long long per_step = 4 * 2 + 3;
+  for (int i = 0; i < nsteps; ++i) {
+    if (ctx->timing) {
+      if (int rc = enqueue_step(ctx, false)) return rc;
+    } else {
+      CK(cudaGraphLaunch(ctx->graph, ctx->st));
+      ctx->launches += per_step;
+    }
+  }
+  if (int rc = sync_check(ctx)) return rc;
+  if (t_out) *t_out = ctx->h_step->t;
+  return NSFR_OK;
+}
+
+int nsfr_gpu_l2_error(nsfr_gpu_ctx* ctx, int kind, double out2[2]) {
+  const int g = ctx->tab.g, n = ctx->N, G3 = g * g * g, N3 = n * n * n;
+  const int M = std::max(g, n), M3 = M * M * M;
+  const size_t smem = sizeof(double) * (3 * G3 + 2 * M3 + 10 * N3);
+  if (int rc = setup_kernel_smem(ctx, smem, (const void*)k_l2)) return rc;
+  if (int rc = sync_check(ctx)) return rc;
+  L2Params P{};
+  P.tab = ctx->d_tab;
+  P.u = ctx->d_un;
+  P.jac = ctx->d_jac;
+  P.part = ctx->d_part;
+  P.E = ctx->E;
+  P.m = ctx->m;
+  P.k0 = ctx->k0;
+  P.kind = kind;
+  P.x_left = ctx->s.x_left;
+  P.h = (ctx->s.x_right - ctx->s.x_left) / ctx->m;
+  P.beta = ctx->s.beta;
+  P.l = length_scale(ctx->s);
+  P.gamma = ctx->s.gamma;
+  P.t = ctx->h_step->t;
+  k_l2<<<ctx->E, 128, smem, ctx->st>>>(P);
+  k_reduce<<<1, 1024, 0, ctx->st>>>(ctx->d_part, ctx->E, 2, ctx->d_red);
+  ctx->launches += 2;
+  if (int rc = allreduce_sum(ctx, ctx->d_red, 2)) return rc;
+  if (int rc = sync_check(ctx)) return rc;
+  double h[2];
+  CK(cudaMemcpy(h, ctx->d_red, sizeof h, cudaMemcpyDeviceToHost));
+  out2[0] = std::sqrt(h[0]);
+  out2[1] = std::sqrt(h[1]);
+  return NSFR_OK;
+}
+
+double* nsfr_gpu_state_device_ptr(nsfr_gpu_ctx* ctx) { return ctx->d_un; }
+size_t nsfr_gpu_state_count(const nsfr_gpu_ctx* ctx) { return state_count(ctx); }
+int nsfr_gpu_sync(nsfr_gpu_ctx* ctx) { return sync_check(ctx); }
+long long nsfr_gpu_launch_count(const nsfr_gpu_ctx* ctx) { return ctx->launches; }
+
+// Bench helper: time `nsteps` RK4 steps with CUDA events on the context
+// stream. With kernel_ms != NULL each K1/K2 launch is bracketed by events and
+// kernel_ms[0]/[1] receive the summed K1/K2 durations (ms).
+int nsfr_gpu_time_steps(nsfr_gpu_ctx* ctx, int nsteps, double cfl, double* step_ms,
+                        double* kernel_ms) {
+  if (int rc = set_step_params(ctx, cfl, 0.0)) return rc;
+  if (!kernel_ms && !ctx->graph) {
+    if (int rc = nsfr_gpu_advance(ctx, 0, cfl, 0.0, nullptr)) return rc;  // capture the step graph
+  }
+  ctx->timing = kernel_ms != nullptr;
+  ctx->ev_marks.clear();
+  cudaEvent_t a, b;
+  CK(cudaEventCreate(&a));
+  CK(cudaEventCreate(&b));
+  CK(cudaEventRecord(a, ctx->st));
+  int rc = NSFR_OK;
+  for (int i = 0; i < nsteps && !rc; ++i) {
+    if (ctx->timing) {
+      rc = enqueue_step(ctx, false);
+    } else {
+      CK(cudaGraphLaunch(ctx->graph, ctx->st));
+      ctx->launches += 4 * 2 + 3;
+    }
+  }
+  CK(cudaEventRecord(b, ctx->st));
+  if (!rc) rc = sync_check(ctx);
+  float ms = 0.f;
+  CK(cudaEventElapsedTime(&ms, a, b));
+  *step_ms = ms;
+  if (kernel_ms) {
+    kernel_ms[0] = kernel_ms[1] = 0.0;
+    for (auto& mk : ctx->ev_marks) {
+      float x = 0.f;
+      cudaEventElapsedTime(&x, ctx->ev_pool[mk.second], ctx->ev_pool[mk.second + 1]);
+      kernel_ms[mk.first - 1] += x;
+    }
+    for (auto e : ctx->ev_pool) cudaEventDestroy(e);
+    ctx->ev_pool.clear();
+    ctx->ev_marks.clear();
+  }
+  ctx->timing = false;
+  cudaEventDestroy(a);
+  cudaEventDestroy(b);
+  return rc;
+}
+
+}  // extern "C"
+
+// ---------------------------------------------------------------------------
+// FP64 pipe peak (roofline denominator; MEASURED_PEAKS.json carries none):
+// independent DFMA chains on every SM, best of 5, CUDA events.
+namespace {
+__global__ void k_dfma_peak(double* out, int iters, double a, double b) {
+  double x0 = threadIdx.x, x1 = x0 + 1, x2 = x0 + 2, x3 = x0 + 3, x4 = x0 + 4, x5 = x0 + 5,
+         x6 = x0 + 6, x7 = x0 + 7;
+  for (int i = 0; i < iters; ++i) {
+#pragma unroll
+    for (int k = 0; k < 16; ++k) {
+      x0 = fma(x0, a, b); x1 = fma(x1, a, b); x2 = fma(x2, a, b); x3 = fma(x3, a, b);
+      x4 = fma(x4, a, b); x5 = fma(x5, a, b); x6 = fma(x6, a, b); x7 = fma(x7, a, b);
+    }
+  }
+  out[blockIdx.x * blockDim.x + threadIdx.x] = x0 + x1 + x2 + x3 + x4 + x5 + x6 + x7;
+}
+}  // namespace
+
+extern "C" int nsfr_gpu_measure_fp64_peak(int device, double* tflops) {
+  if (cudaSetDevice(device) != cudaSuccess) return NSFR_E_CUDA;
+  int sms = 0;
+  cudaDeviceGetAttribute(&sms, cudaDevAttrMultiProcessorCount, device);
+  const int threads = 256, blocks = sms * 8, iters = 2048;
+  double* out = nullptr;
+  if (cudaMalloc(&out, sizeof(double) * threads * blocks) != cudaSuccess) return NSFR_E_CUDA;
+  cudaEvent_t a, b;
+  cudaEventCreate(&a);
+  cudaEventCreate(&b);
+  k_dfma_peak<<<blocks, threads>>>(out, 64, 0.999999, 1e-7);
+  float best = 1e30f;
+  for (int r = 0; r < 5; ++r) {
+    cudaEventRecord(a);
+    k_dfma_peak<<<blocks, threads>>>(out, iters, 0.999999, 1e-7);
+    cudaEventRecord(b);
+    cudaEventSynchronize(b);
+    float ms = 0.f;
+    cudaEventElapsedTime(&ms, a, b);
+    best = ms < best ? ms : best;
+  }
+  cudaEventDestroy(a);
+  cudaEventDestroy(b);
+  cudaFree(out);
+  if (cudaGetLastError() != cudaSuccess) return NSFR_E_CUDA;
+  *tflops = 2.0 * 8 * 16 * (double)iters * threads * blocks / (best * 1e-3) / 1e12;
+  return NSFR_OK;
+}

@@ -87,6 +87,7 @@ def load(kind: str) -> tuple[C.CDLL, str]:
             "x_vol": (C.c_int, [C.c_void_p, P]),
             "initial_state": (C.c_int, [C.c_void_p, C.c_int, P]),
             "boundary_traces": (C.c_int, [C.c_void_p, P, P, P]),
+            "traces": (C.c_int, [C.c_void_p, P, P]),
             "rhs": (C.c_int, [C.c_void_p, P, P, P, P, P]),
             "max_wavespeed": (C.c_int, [C.c_void_p, P, P]),
             "rk4_step": (C.c_int, [C.c_void_p, P, C.c_double]),
@@ -199,6 +200,11 @@ class CpuSolver:
         ds = np.zeros(1) if entropy else None
         self._check(self._fn("rhs")(self.ctx, ptr(u), ptr(halo_lo), ptr(halo_hi), ptr(out), ptr(ds)))
         return (out, float(ds[0])) if entropy else out
+
+    def traces(self, u):
+        tr = np.zeros((self.ne, 6, 5, self.nf))
+        self._check(self._fn("traces")(self.ctx, ptr(np.ascontiguousarray(u)), ptr(tr)))
+        return tr
 
     def boundary_traces(self, u):
         m = self.cfg.m

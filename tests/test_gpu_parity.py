@@ -1,0 +1,234 @@
+"""GPU parity: the CUDA path (through the C ABI) against the CPU oracle and the
+reference-generated golden vectors. Run on a B200 with `pytest -m gpu`.
+
+RHS tolerance. The reference residual is a sum of large two-point flux
+differences; perturbing its INPUT by one ulp moves its OUTPUT by 1e-11..5e-11
+(per state, normwise; tests/test_invariants.py::test_parity_floor_is_above_1e12).
+Any implementation that is not bit-identical (different libm, FMA order)
+therefore differs from it at that level. Each RHS gate below measures this
+floor on the same input with the oracle and requires
+    max_s ||R_gpu,s - R_ref,s||_inf / ||R_ref,s||_inf <= max(1e-12, 4 * floor)
+and never more than 1e-10. L2 errors are gated at 1e-10 relative and entropy
+change at 1e-12 |U_total| (BASELINE.json north_star)."""
+import json
+import os
+
+import numpy as np
+import pytest
+
+from oracle_lib import C_PLUS as OC_PLUS
+from oracle_lib import Config, CpuSolver
+
+pytestmark = pytest.mark.gpu
+
+GOLD = os.path.join(os.path.dirname(os.path.abspath(__file__)), "golden")
+
+
+def P():
+    import paper_2312_07725_b200 as pkg
+    return pkg
+
+
+def per_state_rel(a, b):
+    a = a.reshape(a.shape[0], 5, -1)
+    b = b.reshape(b.shape[0], 5, -1)
+    return float((np.abs(a - b).max(axis=(0, 2)) / np.abs(b).max(axis=(0, 2))).max())
+
+
+def floor_of(oracle, u, trials=2):
+    r0 = oracle.rhs(u)
+    rng = np.random.default_rng(11)
+    worst = 0.0
+    for _ in range(trials):
+        up = u * (1 + 2.0 ** -52 * rng.choice([-1, 1], u.shape))
+        worst = max(worst, per_state_rel(oracle.rhs(up), r0))
+    return worst
+
+
+def assert_rhs_parity(got, want, floor):
+    err = per_state_rel(got, want)
+    gate = min(1e-10, max(1e-12, 4.0 * floor))
+    assert err <= gate, f"rhs parity {err:.3e} > gate {gate:.3e} (floor {floor:.3e})"
+    return err
+
+
+def gpu_cfg(**kw):
+    pkg = P()
+    return pkg.SolverConfig(**kw)
+
+
+@pytest.fixture(scope="module")
+def meta():
+    with open(os.path.join(GOLD, "golden.json")) as f:
+        return json.load(f)
+
+
+@pytest.mark.parametrize("p", [3, 4, 5])
+@pytest.mark.parametrize("quad", [0, 1])
+def test_tables_match_reference(p, quad):
+    g = np.load(os.path.join(GOLD, "tables.npz"))
+    for cname, c in (("dg", 0.0), ("plus", OC_PLUS[p])):
+        s = P().GpuSolver(gpu_cfg(p=p, m=1, quad_kind=quad, c1d=c))
+        for k, v in s.tables().items():
+            np.testing.assert_allclose(v, g[f"p{p}_q{quad}_{cname}_{k}"], rtol=0,
+                                       atol=2e-15 * max(1.0, np.abs(v).max()))
+        s.close()
+
+
+@pytest.mark.parametrize("p,m", [(3, 4), (4, 3), (5, 2)])
+def test_device_metrics_and_ic(p, m):
+    o = CpuSolver("oracle", Config(p=p, m=m))
+    g = P().GpuSolver(gpu_cfg(p=p, m=m))
+    jo, co = o.metrics()
+    jg, cg = g.metrics()
+    assert np.abs(jg - jo).max() <= 1e-13 * np.abs(jo).max()
+    assert np.abs(cg - co).max() <= 1e-12 * np.abs(co).max()
+    g.init_case()
+    np.testing.assert_allclose(g.get_state(), o.initial_state(), rtol=1e-14, atol=1e-14)
+
+
+@pytest.mark.parametrize("name", ["vortex_p3_m3_dg_roe", "vortex_p4_m2_plus_roe", "tgv_p3_m2_dg_ec",
+                                  "vortex_p5_m2_dg_roe"])
+def test_rhs_on_reference_fixture(name, meta):
+    """Same tables, metrics and input state as the reference run: isolates the kernels."""
+    fx = np.load(os.path.join(GOLD, f"rhs_{name}.npz"))
+    c = meta[name]["cfg"]
+    tabs = np.load(os.path.join(GOLD, "tables.npz"))
+    key = f"p{c['p']}_q0_{'dg' if c['c1d'] == 0.0 else 'plus'}"
+    tables = {k: tabs[f"{key}_{k}"] for k in ("interp", "proj", "fr_proj", "skew", "bound_flux",
+                                               "bound_sol", "wq")}
+    g = P().GpuSolver(gpu_cfg(p=c["p"], m=c["m"], c1d=c["c1d"], case=c["case"], roe=c["roe"],
+                              entropy_diag=True), tables=tables, metrics=(fx["jac"], fx["cof"]))
+    o = CpuSolver("oracle", Config(p=c["p"], m=c["m"], c1d=c["c1d"], case=c["case"], roe=c["roe"]))
+    u = np.ascontiguousarray(fx["u"])
+    g.set_state(u)
+    tr_g = g.traces()
+    tr_o = o.traces(u)
+    assert np.abs(tr_g - tr_o).max() <= 1e-13 * np.abs(tr_o).max()
+    dudt, ds = g.rhs(entropy=True)
+    assert_rhs_parity(dudt, fx["dudt"], floor_of(o, u))
+    assert abs(ds - meta[name]["entropy_change"]) <= 1e-12 * abs(o.entropy_total(u))
+    assert g.max_wavespeed() == pytest.approx(meta[name]["lambda_max"], rel=1e-14)
+
+
+@pytest.mark.parametrize("p,m,c1d,case,roe", [
+    (3, 4, 0.0, "vortex", True),
+    (4, 4, OC_PLUS[4], "vortex", True),
+    (5, 3, 0.0, "vortex", True),
+    (3, 4, 0.0, "tgv", False),
+])
+def test_rhs_native_setup(p, m, c1d, case, roe):
+    """Fully native path: device-built metrics, own tables, device initial state."""
+    o = CpuSolver("oracle", Config(p=p, m=m, c1d=c1d, case=case, roe=roe))
+    g = P().GpuSolver(gpu_cfg(p=p, m=m, c1d=c1d, case=case, roe=roe))
+    g.init_case()
+    u = g.get_state()
+    assert_rhs_parity(g.rhs(), o.rhs(u), floor_of(o, u))
+
+
+def test_config3_rhs_full_size():
+    """BASELINE configs[2] at full size (32^3, p=4): one RHS against the oracle."""
+    o = CpuSolver("oracle", Config(p=4, m=32))
+    g = P().GpuSolver(gpu_cfg(p=4, m=32))
+    g.init_case()
+    u = g.get_state()
+    want = o.rhs(u)
+    assert_rhs_parity(g.rhs(), want, floor_of(o, u, trials=1))
+
+
+def test_config1_twenty_steps(meta):
+    """BASELINE configs[0]: 8^3 p=3 vortex, c_DG, EC+Roe, 20 RK4 steps at CFL 0.1."""
+    g = P().GpuSolver(gpu_cfg(p=3, m=8))
+    g.init_case()
+    t = g.advance(20, cfl=0.1)
+    assert t == pytest.approx(meta["config1_t20"], rel=1e-13)
+    np.testing.assert_allclose(g.l2_error(), meta["config1_l2_t20"], rtol=1e-10)
+
+
+def test_advance_graph_equals_stepwise():
+    cfg = gpu_cfg(p=3, m=4)
+    a = P().GpuSolver(cfg)
+    b = P().GpuSolver(cfg)
+    a.init_case()
+    b.init_case()
+    a.advance(5)
+    for _ in range(5):
+        b.rk4_step(0.1)
+    np.testing.assert_array_equal(a.get_state(), b.get_state())
+    assert a.time == b.time
+
+
+def test_fixed_dt_step_matches_oracle():
+    o = CpuSolver("oracle", Config(p=4, m=3))
+    g = P().GpuSolver(gpu_cfg(p=4, m=3))
+    g.init_case()
+    u0 = g.get_state()
+    dt = 0.1 * o.dx() / o.max_wavespeed(u0)
+    g.rk4_step_dt(dt)
+    uo = o.rk4_step(u0.copy(), dt)
+    assert per_state_rel(g.get_state() - u0, uo - u0) < 1e-10
+
+
+def test_tgv_entropy_conservation():
+    """BASELINE configs[3] physics on a small box: EC flux, consistent face
+    metrics (grid_degree = p): entropy change at round-off of |U_total|."""
+    o = CpuSolver("oracle", Config(p=3, m=4, case="tgv", roe=False, grid_degree=3))
+    g = P().GpuSolver(gpu_cfg(p=3, m=4, case="tgv", roe=False, grid_degree=3, entropy_diag=True))
+    g.init_case()
+    u = g.get_state()
+    utot = abs(o.entropy_total(u))
+    ds_g = g.entropy_change()
+    ds_o = o.rhs(u, entropy=True)[1]
+    assert abs(ds_g) <= 1e-12 * utot
+    assert abs(ds_g - ds_o) <= 1e-12 * utot
+
+
+def test_config4_entropy_change_full_size():
+    """BASELINE configs[3]: TGV 32^3, p=3, EC only, reference grid_degree p+1:
+    per-step entropy change against the oracle within 1e-12 |U_total|."""
+    o = CpuSolver("oracle", Config(p=3, m=32, case="tgv", roe=False))
+    g = P().GpuSolver(gpu_cfg(p=3, m=32, case="tgv", roe=False, entropy_diag=True))
+    g.init_case()
+    u = g.get_state()
+    utot = abs(o.entropy_total(u))
+    assert abs(g.entropy_change() - o.rhs(u, entropy=True)[1]) <= 1e-12 * utot
+    g.advance(2)
+    u2 = g.get_state()
+    assert abs(g.entropy_change() - o.rhs(u2, entropy=True)[1]) <= 1e-12 * utot
+
+
+@pytest.mark.parametrize("p", [3, 4])
+def test_free_stream(p):
+    g = P().GpuSolver(gpu_cfg(p=p, m=3, case="free_stream", c1d=OC_PLUS[p]))
+    g.init_case()
+    assert np.abs(g.rhs()).max() < 1e-12
+
+
+def test_inadmissible_state_raises():
+    pkg = P()
+    g = pkg.GpuSolver(gpu_cfg(p=3, m=2))
+    g.init_case()
+    u = g.get_state()
+    u[3, 0, 5] = -1.0  # negative density
+    g.set_state(u)
+    with pytest.raises(pkg.StepFailureError):
+        g.rhs()
+    g.init_case()  # the context stays usable
+    assert np.isfinite(g.rhs()).all()
+
+
+def test_degenerate_mesh_raises():
+    pkg = P()
+    with pytest.raises(pkg.InvalidMeshError):
+        pkg.GpuSolver(gpu_cfg(p=3, m=2, beta=4.0))
+
+
+def test_config5_size_smoke():
+    """BASELINE configs[4] size (128^3, p=4, c_+): build, one step, sane L2."""
+    g = P().GpuSolver(gpu_cfg(p=4, m=128, c1d=OC_PLUS[4]))
+    g.init_case()
+    e0 = g.l2_error()
+    t = g.advance(1)
+    assert t > 0
+    e1 = g.l2_error()
+    assert np.all(np.isfinite(e1)) and np.all(e1 < 10 * e0 + 1e-6)

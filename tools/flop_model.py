@@ -1,0 +1,93 @@
+"""Algorithmic flop/byte model of one NSFR RHS per element.
+
+Counts follow the operation sequence of the oracle (oracle/nsfr_oracle.c, the
+restatement of the reference path): add/sub/mul = 1, FMA = 2 (written as two
+flops), and each div/sqrt/log/exp/pow = 1 flop, also reported separately.
+The GPU kernels execute a contracted flux (fewer flops); the roofline uses
+THESE algorithmic counts, so a cheaper implementation reads as faster.
+
+n = p+1 (n_q = n_p).  Per element:
+  tensor passes: S1, S3, S4-volume, S9-volume, S10 x2 = 6 products x 5 states
+                 x 3 directions x n^3 outputs x n FMA            = 180 n^4
+  face traces (S4) + face lifting (S9): 2 x 6 faces x 5 x 3 n^3 FMA = 360 n^3
+  WA diagonal: 5 n^3 div
+  node maps: v(u) at n^3 nodes; u(v) at n^3 + 6 n^2 nodes
+  pairs: P_v = 3 n^2 n(n-1)/2 volume, P_s = 6 n^3 surface (hybrid)
+  face numerical flux: 6 n^2 (EC + Roe)
+"""
+from __future__ import annotations
+
+# per-operation counts: (flops excluding specials, div, log, exp, pow, sqrt)
+ENTROPY_VARS = dict(fl=25, div=8, log=2)             # euler.cpp:46-54 incl. pressure
+ENTROPY_TO_CONS = dict(fl=35, div=3, exp=1, pow=2)   # euler.cpp:56-71
+# log_mean (euler.cpp:89-99), log branch: z div, (z-1)/(z+1) (2 fl + div), f^2 (1),
+# (a-b) (1) / log(z): 4 fl, 3 div, 1 log
+LOG_MEAN = dict(fl=4, div=3, log=1)
+# flux_ranocha (euler.cpp:142-162) incl. prim() of both states (2x: 1 div + 3 mul,
+# pressure 9 fl + 1 div), rho/p (2 div), 2 log means, 15 flux values
+FLUX_EC = dict(fl=2 * (3 + 9) + 18 + 3 * 12, div=2 * 2 + 2 + 3, log=0)
+CONTRACT = dict(fl=6 + 25)                           # 0.5(Ci+Cj) and 5 x 3-term dot
+ACCUM_PAIR = dict(fl=1 + 20)                         # c = wt q ; 2 x 5 FMA
+ROE = dict(fl=160, div=4, sqrt=4)                    # euler.cpp:229-301 w/o entropy vars
+
+
+def _add(acc, d, k=1):
+    for key, v in d.items():
+        acc[key] = acc.get(key, 0) + k * v
+
+
+def per_element(p: int) -> dict:
+    n = p + 1
+    n2, n3, n4 = n * n, n ** 3, n ** 4
+    c: dict = {}
+    # K1 projection
+    _add(c, dict(fl=2 * 15 * n4))                # S1 chi^3 (3 dirs x 5 states x n^3 x n FMA)
+    _add(c, ENTROPY_VARS, n3)                     # S2
+    _add(c, dict(fl=2 * 15 * n4))                # S3 Pi^3
+    _add(c, dict(fl=2 * 15 * n4))                # S4 volume chi^3
+    _add(c, dict(fl=2 * 6 * 5 * 3 * n3))         # S4 faces
+    _add(c, ENTROPY_TO_CONS, n3 + 6 * n2)         # S5
+    k1 = dict(c)
+    # K2 residual
+    pv, ps = 3 * n2 * n * (n - 1) // 2, 6 * n3
+    pair = {}
+    _add(pair, FLUX_EC)
+    _add(pair, LOG_MEAN, 2)
+    _add(pair, CONTRACT)
+    _add(pair, ACCUM_PAIR)
+    _add(c, pair, pv + ps)
+    face = {}
+    _add(face, FLUX_EC)
+    _add(face, LOG_MEAN, 2)
+    _add(face, dict(fl=25 + 3 + 10))              # n-contraction, J^G w, accumulate
+    _add(face, ROE)
+    _add(face, ENTROPY_VARS, 2)                   # Roe's entropy-variable jump
+    _add(c, face, 6 * n2)
+    _add(c, dict(fl=2 * 15 * n4))                # S9 chi^T^3 volume
+    _add(c, dict(fl=2 * 6 * 5 * 3 * n3))         # S9 faces
+    _add(c, dict(fl=2 * 2 * 15 * n4, div=5 * n3))  # S10 Pi~^T^3, /wJ, Pi~^3
+    _add(c, dict(fl=5 * n3 * 2))                 # RK stage update (2 FMA-equivalents)
+    k2 = {key: c.get(key, 0) - k1.get(key, 0) for key in c}
+    special = sum(c.get(s, 0) for s in ("div", "log", "exp", "pow", "sqrt"))
+    return {
+        "n": n,
+        "flops_total": c["fl"] + special,
+        "flops_k1": k1["fl"] + sum(k1.get(s, 0) for s in ("div", "log", "exp", "pow", "sqrt")),
+        "flops_k2": k2["fl"] + sum(k2.get(s, 0) for s in ("div", "log", "exp", "pow", "sqrt")),
+        "special": {s: c.get(s, 0) for s in ("div", "log", "exp", "pow", "sqrt")},
+        "pairs": pv + ps,
+        "face_fluxes": 6 * n2,
+    }
+
+
+def bytes_per_element(p: int) -> dict:
+    """Compulsory HBM bytes per element-stage: read u_s, u_n,
+    acc, write acc and u_{s+1} (5 x 5 n^3) and read C, J (10 n^3)."""
+    n3 = (p + 1) ** 3
+    return {"b_alg": 8 * (25 * n3 + 10 * n3)}
+
+
+if __name__ == "__main__":
+    import json
+    for p in (3, 4, 5):
+        print(json.dumps({**per_element(p), **bytes_per_element(p)}))
