@@ -5,8 +5,8 @@ ABI of include/nsfr_gpu.h); this package is its Python mirror.
 """
 from .solver import (C_PLUS, CASES, ConfigError, DeviceError, DimensionError, GpuSolver,
                      InvalidMeshError, NsfrError, SolverConfig, StepFailureError, halo_plan,
-                     load_library, nccl_unique_id)
+                     load_library, measure_fp64_peak, nccl_unique_id)
 
 __all__ = ["C_PLUS", "CASES", "ConfigError", "DeviceError", "DimensionError", "GpuSolver",
            "InvalidMeshError", "NsfrError", "SolverConfig", "StepFailureError", "halo_plan",
-           "load_library", "nccl_unique_id"]
+           "load_library", "measure_fp64_peak", "nccl_unique_id"]

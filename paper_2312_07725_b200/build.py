@@ -1,6 +1,7 @@
 """Build libnsfr_b200.so in-tree (nvcc, sm_100a) — used by __graft_entry__.build()."""
 from __future__ import annotations
 
+import glob
 import os
 import subprocess
 import sys
@@ -9,8 +10,7 @@ HERE = os.path.dirname(os.path.abspath(__file__))
 ROOT = os.path.dirname(HERE)
 LIB = os.path.join(HERE, "libnsfr_b200.so")
 SOURCES = [os.path.join(HERE, "csrc", f) for f in ("nsfr_gpu.cu", "tables.cpp")]
-DEPS = SOURCES + [os.path.join(HERE, "csrc", f) for f in ("kernels.cuh", "physics.cuh", "tables.hpp")] + [
-    os.path.join(ROOT, "include", "nsfr_gpu.h")]
+DEPS = sorted(glob.glob(os.path.join(HERE, "csrc", "*"))) + [os.path.join(ROOT, "include", "nsfr_gpu.h")]
 
 NVCC_FLAGS = [
     "-std=c++17", "-O3", "-lineinfo",

@@ -1,0 +1,227 @@
+// K1: entropy projection S1-S5.
+//
+//   u_q = chi^3 u_hat;  v_q = v(u_q);  v_hat = Pi^3 v_q;
+//   v~ = chi^3 v_hat at the volume, (bs_side (x) chi (x) chi) v_hat at each face;
+//   u~ = u(v~)                                   (euler.cpp:46-71)
+// plus lambda_max = max(|u| + a) over the volume nodes for adaptive dt.
+//
+// EPB elements per CTA, element blocks staged in shared memory. Every
+// directional contraction is a LINE pass: one thread per 1D line loads its N
+// inputs once and writes N outputs (fma chain in the reference's order,
+// apply_operator_dir sumfac.cpp:7-55). The 1D operators travel in the kernel
+// parameter (constant) bank, so each FMA takes its coefficient as an operand.
+#pragma once
+#include "physics.cuh"
+#include "setup_kernels.cuh"
+
+namespace nsfr_b200 {
+
+struct ProjParams {
+  const double* u;       // [E][5][N^3] stage input
+  double* ut_vol;        // [E][5][N^3] entropy-projected conservative (volume)
+  double* traces;        // [E][6][5][N^2]
+  double* vhat;          // [E][5][N^3] or nullptr
+  double* send_lo;       // [m*m][5][N^2] face 4 of plane 0, or nullptr
+  double* send_hi;       // [m*m][5][N^2] face 5 of plane nz-1, or nullptr
+  unsigned long long* lam;  // lambda_max bits or nullptr
+  unsigned* err;
+  int E, m, nz;
+  double gamma;
+};
+
+template <int N>
+struct ProjOps {
+  double interp[N * N];  // chi   (nq x np)
+  double proj[N * N];    // Pi    (np x nq)
+  double bsol[2 * N];    // bound_sol rows at xi = -1, +1
+};
+
+template <int N>
+struct ProjCfg {
+  static constexpr int N2 = N * N, N3 = N * N * N;
+  static constexpr int EPB = N3 <= 32 ? 8 : (N3 <= 64 ? 4 : (N3 <= 128 ? 2 : 1));
+  static constexpr int THREADS = ((EPB * N3 + 31) / 32) * 32;
+  // smem doubles per element: A, B, V, C4 (5 N3 each) + T0, T0b, T1, F2, F1, F0 (10 N2 each)
+  static constexpr int PER_EL = 20 * N3 + 60 * N2;
+  static constexpr int SMEM = EPB * PER_EL * 8;
+};
+
+// One thread per 1D line along D of a [batch][N^3] tensor; out[r] = sum_a op[r][a] x[a].
+// FACE: also contract the same line with the two boundary rows into fo[batch][side][N2].
+template <int N, int D, bool FACE>
+__device__ __forceinline__ void line_pass(const double (&op)[N * N], const double* in, double* out,
+                                          const double (&bs)[2 * N], double* fo, int nbs, int tid,
+                                          int nthr) {
+  constexpr int N2 = N * N, N3 = N * N * N;
+  constexpr int stride = D == 0 ? 1 : (D == 1 ? N : N2);
+  for (int it = tid; it < nbs * N2; it += nthr) {
+    const int bsi = it / N2, l = it - bsi * N2;
+    const int l0 = l % N, l1 = l / N;
+    const int base = D == 0 ? N * (l0 + N * l1) : (D == 1 ? l0 + N2 * l1 : l0 + N * l1);
+    const double* src = in + bsi * N3 + base;
+    double x[N];
+#pragma unroll
+    for (int a = 0; a < N; ++a) x[a] = src[a * stride];
+    double* dst = out + bsi * N3 + base;
+#pragma unroll
+    for (int r = 0; r < N; ++r) {
+      double acc = 0.0;
+#pragma unroll
+      for (int a = 0; a < N; ++a) acc = fma(op[r * N + a], x[a], acc);
+      dst[r * stride] = acc;
+    }
+    if (FACE) {
+#pragma unroll
+      for (int side = 0; side < 2; ++side) {
+        double acc = 0.0;
+#pragma unroll
+        for (int a = 0; a < N; ++a) acc = fma(bs[side * N + a], x[a], acc);
+        fo[(bsi * 2 + side) * N2 + l] = acc;
+      }
+    }
+  }
+}
+
+// Line pass on face arrays [batch][N2] (index t1 + N t2) along t1 (T=0) or t2 (T=1).
+template <int N, int T>
+__device__ __forceinline__ void face_pass(const double (&op)[N * N], const double* in, double* out,
+                                          int nbatch, int tid, int nthr) {
+  constexpr int N2 = N * N;
+  constexpr int stride = T == 0 ? 1 : N;
+  for (int it = tid; it < nbatch * N; it += nthr) {
+    const int bi = it / N, l = it - bi * N;
+    const int base = T == 0 ? N * l : l;
+    const double* src = in + bi * N2 + base;
+    double x[N];
+#pragma unroll
+    for (int a = 0; a < N; ++a) x[a] = src[a * stride];
+    double* dst = out + bi * N2 + base;
+#pragma unroll
+    for (int r = 0; r < N; ++r) {
+      double acc = 0.0;
+#pragma unroll
+      for (int a = 0; a < N; ++a) acc = fma(op[r * N + a], x[a], acc);
+      dst[r * stride] = acc;
+    }
+  }
+}
+
+template <int N>
+__global__ void __launch_bounds__(ProjCfg<N>::THREADS) k_project(ProjParams P, ProjOps<N> O) {
+  using Cfg = ProjCfg<N>;
+  constexpr int N2 = Cfg::N2, N3 = Cfg::N3, EPB = Cfg::EPB;
+  extern __shared__ double sm[];
+  double* A = sm;
+  double* B = A + EPB * 5 * N3;
+  double* V = B + EPB * 5 * N3;
+  double* C4 = V + EPB * 5 * N3;
+  double* T0 = C4 + EPB * 5 * N3;   // [EPB*5][2][N2]  bs_xi v_hat          (index j + N k)
+  double* T0b = T0 + EPB * 10 * N2; // [EPB*5][2][N2]  chi_eta T0
+  double* T1 = T0b + EPB * 10 * N2; // [EPB*5][2][N2]  bs_eta X             (index i + N k)
+  double* F2 = T1 + EPB * 10 * N2;  // [EPB*5][2][N2]  dir-2 faces: bs_zeta XY (index i + N j)
+  double* F1 = F2 + EPB * 10 * N2;  // [EPB*5][2][N2]  dir-1 faces: chi_zeta T1
+  double* F0 = F1 + EPB * 10 * N2;  // [EPB*5][2][N2]  dir-0 faces: chi_zeta T0b
+  const int tid = threadIdx.x, nthr = blockDim.x;
+  const int e0 = blockIdx.x * EPB;
+  const int nb = min(EPB, P.E - e0);
+  const double g = P.gamma;
+  {
+    const double* src = P.u + (size_t)e0 * 5 * N3;
+    for (int i = tid; i < nb * 5 * N3; i += nthr) A[i] = src[i];
+  }
+  __syncthreads();
+  const int nbs = nb * 5;
+  // S1 u_q = chi^3 u_hat (xi, eta, zeta passes: apply_tensor_product order)
+  line_pass<N, 0, false>(O.interp, A, B, O.bsol, nullptr, nbs, tid, nthr);
+  __syncthreads();
+  line_pass<N, 1, false>(O.interp, B, A, O.bsol, nullptr, nbs, tid, nthr);
+  __syncthreads();
+  line_pass<N, 2, false>(O.interp, A, B, O.bsol, nullptr, nbs, tid, nthr);
+  __syncthreads();
+  // S2 v(u_q), and the wavespeed for adaptive dt
+  double lam = 0.0;
+  for (int it = tid; it < nb * N3; it += nthr) {
+    const int b = it / N3, q = it - b * N3;
+    double uu[NS], vv[NS];
+#pragma unroll
+    for (int s = 0; s < NS; ++s) uu[s] = B[(b * 5 + s) * N3 + q];
+    if (!d_entropy_vars(g, uu, vv)) {
+      atomicOr(P.err, ERR_STATE);
+#pragma unroll
+      for (int s = 0; s < NS; ++s) vv[s] = (s == 4) ? -1.0 : 0.0;
+    } else if (P.lam) {
+      const double vx = uu[1] / uu[0], vy = uu[2] / uu[0], vz = uu[3] / uu[0];
+      const double speed = sqrt(vx * vx + vy * vy + vz * vz);
+      const double a = sqrt(g * d_pressure(g, uu) / uu[0]);
+      lam = fmax(lam, speed + a);
+    }
+#pragma unroll
+    for (int s = 0; s < NS; ++s) B[(b * 5 + s) * N3 + q] = vv[s];
+  }
+  if (P.lam) {
+    for (int o = 16; o > 0; o >>= 1) lam = fmax(lam, __shfl_xor_sync(0xffffffffu, lam, o));
+    if ((tid & 31) == 0 && lam > 0.0) atomicMax(P.lam, dbl_bits(lam));
+  }
+  __syncthreads();
+  // S3 v_hat = Pi^3 v_q
+  line_pass<N, 0, false>(O.proj, B, A, O.bsol, nullptr, nbs, tid, nthr);
+  __syncthreads();
+  line_pass<N, 1, false>(O.proj, A, B, O.bsol, nullptr, nbs, tid, nthr);
+  __syncthreads();
+  line_pass<N, 2, false>(O.proj, B, V, O.bsol, nullptr, nbs, tid, nthr);
+  __syncthreads();
+  if (P.vhat) {
+    double* dst = P.vhat + (size_t)e0 * 5 * N3;
+    for (int i = tid; i < nb * 5 * N3; i += nthr) dst[i] = V[i];
+  }
+  // S4 in the apply_tensor_product order (xi, eta, zeta) with the bound_sol row
+  // in each face's normal direction (sumfac.cpp:57-69):
+  //   X = chi_xi V, T0 = bs_xi V (same xi-lines)
+  line_pass<N, 0, true>(O.interp, V, A, O.bsol, T0, nbs, tid, nthr);
+  __syncthreads();
+  //   XY = chi_eta X, T1 = bs_eta X (same eta-lines); T0b = chi_eta T0
+  line_pass<N, 1, true>(O.interp, A, B, O.bsol, T1, nbs, tid, nthr);
+  face_pass<N, 0>(O.interp, T0, T0b, nbs * 2, tid, nthr);
+  __syncthreads();
+  //   v~_vol = chi_zeta XY, F2 = bs_zeta XY (same zeta-lines); F1 = chi_zeta T1; F0 = chi_zeta T0b
+  line_pass<N, 2, true>(O.interp, B, C4, O.bsol, F2, nbs, tid, nthr);
+  face_pass<N, 1>(O.interp, T1, F1, nbs * 2, tid, nthr);
+  face_pass<N, 1>(O.interp, T0b, F0, nbs * 2, tid, nthr);
+  __syncthreads();
+  // S5 u~ = u(v~) at volume and face nodes
+  for (int it = tid; it < nb * N3; it += nthr) {
+    const int b = it / N3, q = it - b * N3;
+    double vv[NS], uu[NS];
+#pragma unroll
+    for (int s = 0; s < NS; ++s) vv[s] = C4[(b * 5 + s) * N3 + q];
+    if (!d_entropy_to_cons(g, vv, uu)) atomicOr(P.err, ERR_STATE);
+    double* dst = P.ut_vol + (size_t)(e0 + b) * 5 * N3 + q;
+#pragma unroll
+    for (int s = 0; s < NS; ++s) dst[s * N3] = uu[s];
+  }
+  for (int it = tid; it < nb * 6 * N2; it += nthr) {
+    const int b = it / (6 * N2), r = it - b * 6 * N2, f = r / N2, k = r - f * N2;
+    const int dir = f / 2, side = f % 2;
+    const double* Fd = dir == 0 ? F0 : (dir == 1 ? F1 : F2);
+    double vv[NS], uu[NS];
+#pragma unroll
+    for (int s = 0; s < NS; ++s) vv[s] = Fd[((b * 5 + s) * 2 + side) * N2 + k];
+    if (!d_entropy_to_cons(g, vv, uu)) atomicOr(P.err, ERR_STATE);
+    const int e = e0 + b;
+    double* dst = P.traces + ((size_t)e * 6 + f) * 5 * N2 + k;
+#pragma unroll
+    for (int s = 0; s < NS; ++s) dst[s * N2] = uu[s];
+    // boundary planes also go to the halo send buffers
+    const int mm = P.m * P.m, kl = e / mm, plane = e - kl * mm;
+    if (P.send_lo && f == 4 && kl == 0) {
+#pragma unroll
+      for (int s = 0; s < NS; ++s) P.send_lo[((size_t)plane * 5 + s) * N2 + k] = uu[s];
+    }
+    if (P.send_hi && f == 5 && kl == P.nz - 1) {
+#pragma unroll
+      for (int s = 0; s < NS; ++s) P.send_hi[((size_t)plane * 5 + s) * N2 + k] = uu[s];
+    }
+  }
+}
+
+}  // namespace nsfr_b200

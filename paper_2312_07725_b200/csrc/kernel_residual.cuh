@@ -1,0 +1,445 @@
+// K2: residual S6-S10 for one RK stage, fused:
+//   S6  volume Hadamard flux differencing   (sumfac.hpp:48-94, 0.5*skew -> skew(a,b), D2)
+//   S7  hybrid surface-volume Hadamard      (sumfac.hpp:110-157, own face cofactor, D1)
+//   S8  EC + Roe face flux vs the neighbour's trace (euler.cpp:142-162, 229-301; D3)
+//   S9  chi^T lifting of volume and face rows
+//   S10 weight-adjusted inverse -Pi~ (W J)^-1 Pi~^T R (fr_operators.cpp:280-309, D6)
+//   + the classical RK4 stage update (D4).
+//
+// Thread mapping. Line phase: one thread per 1D line (dir, t1, t2) of an
+// element does every two-point evaluation touching that line: the n(n-1)/2
+// volume pairs, the 2n hybrid pairs with the two faces it pierces and the two
+// face fluxes. Each node belongs to exactly one line per direction, so the
+// per-direction accumulators need no atomics (deterministic).
+//
+// Tail. S9 and the first half of S10 are both tensor products, so
+//   Pi~^T^3 R = M^3 vol + sum_f (b_f (x) M (x) M) facc_f,  M = Pi~^T chi^T, b_f = Pi~^T bs_f
+// runs as three LINE passes with the face lifts injected into the pass of
+// their normal direction, the 1/(w J) scaling fused into the last one, then
+// three Pi~ passes with the RK update fused into the last. (The entropy
+// diagnostic needs R itself: that path lifts with chi^T first.)
+// All 1D operators travel in the kernel parameter (constant) bank.
+#pragma once
+#include "kernel_project.cuh"
+#include "physics.cuh"
+
+namespace nsfr_b200 {
+
+struct ResParams {
+  const double* ut_vol;   // [E][5][N^3]
+  const double* traces;   // [E][6][5][N^2]
+  const double* halo_lo;  // [m*m][5][N^2] face 5 of plane k0-1 (nullptr: wrap locally)
+  const double* halo_hi;  // [m*m][5][N^2] face 4 of plane k1
+  const double* cof;      // [E][9][N^3]
+  const double* wj;       // [E][N^3]
+  const double* vhat;     // [E][5][N^3] or nullptr
+  double* dS;             // [E] or nullptr
+  double* un;             // RK base state (stage 4 writes it)
+  double* us;             // next stage state
+  double* acc;            // RK accumulator
+  double* out;            // stage 0: dU/dt
+  const double* dt;       // device scalar
+  unsigned* err;
+  int stage, E, m, nz;
+  double gamma;
+  int roe;
+};
+
+template <int N>
+struct ResOps {
+  double M[N * N];       // Pi~^T chi^T          (lift + project, hot path)
+  double bm[2 * N];      // Pi~^T bound_sol_side
+  double fr[N * N];      // Pi~                  (np x nq)
+  double frt[N * N];     // Pi~^T                (entropy-diagnostic path)
+  double it[N * N];      // chi^T                (entropy-diagnostic path)
+  double bs[2 * N];      // bound_sol            (entropy-diagnostic path)
+  double q[N * N];       // skew(a,b) = q(a,b) - q(b,a), q = 0.5 skew
+  double bflux[2 * N];   // flux basis at -1, +1
+  double wq[N];          // quadrature weights
+};
+
+template <int N>
+struct ResCfg {
+  static constexpr int N2 = N * N, N3 = N * N * N;
+  static constexpr int LINES = 3 * N2;
+  static constexpr int EPB = LINES <= 32 ? 6 : (LINES <= 64 ? 4 : 2);
+  static constexpr int THREADS = ((EPB * LINES + 31) / 32) * 32;
+  // WORK: line phase = 8 N3 node primitives + 9 N3 half cofactors;
+  //       tail = 10 N3 pass buffers + 30 N2 face-lift buffers
+  static constexpr int WORK = (17 * N3 > 10 * N3 + 30 * N2) ? 17 * N3 : 10 * N3 + 30 * N2;
+  static constexpr int PER_EL = 15 * N3 + WORK + N3;  // ACCV (3 x 5 N3) + WORK + w J
+  static constexpr int SMEM = EPB * PER_EL * 8;
+#ifdef NSFR_RES_MINB
+  static constexpr int MINB = NSFR_RES_MINB;
+#else
+  static constexpr int MINB = SMEM <= 56 * 1024 ? 4 : (SMEM <= 75 * 1024 ? 3 : (SMEM <= 112 * 1024 ? 2 : 1));
+#endif
+  static constexpr int LPT = (EPB * 5 * N2 + THREADS - 1) / THREADS;  // epilogue lines per thread
+};
+
+// Line pass along D over nb*5 tensors [N^3] with element strides; optional
+// injection of a face array (two sides, [s][side][N2] per element) through the
+// boundary vectors bvec[side][r], and optional division by w J (smem).
+template <int N, int D, bool INJ, bool DIV>
+__device__ __forceinline__ void tail_pass(const double (&op)[N * N], const double (&bvec)[2 * N],
+                                          const double* inj, int inj_es, const double* in, int in_es,
+                                          double* out, int out_es, const double* wj, int nbs,
+                                          int tid, int nthr) {
+  constexpr int N2 = N * N, N3 = N * N * N;
+  constexpr int stride = D == 0 ? 1 : (D == 1 ? N : N2);
+  for (int it = tid; it < nbs * N2; it += nthr) {
+    const int bsi = it / N2, l = it - bsi * N2;
+    const int b = bsi / 5, s = bsi - 5 * b;
+    const int l0 = l % N, l1 = l / N;
+    const int base = D == 0 ? N * (l0 + N * l1) : (D == 1 ? l0 + N2 * l1 : l0 + N * l1);
+    const double* src = in + b * in_es + s * N3 + base;
+    double x[N];
+#pragma unroll
+    for (int a = 0; a < N; ++a) x[a] = src[a * stride];
+    double f0 = 0.0, f1 = 0.0;
+    if (INJ) {
+      f0 = inj[b * inj_es + (s * 2 + 0) * N2 + l];
+      f1 = inj[b * inj_es + (s * 2 + 1) * N2 + l];
+    }
+    double* dst = out + b * out_es + s * N3 + base;
+#pragma unroll
+    for (int r = 0; r < N; ++r) {
+      double acc = 0.0;
+#pragma unroll
+      for (int a = 0; a < N; ++a) acc = fma(op[r * N + a], x[a], acc);
+      if (INJ) {
+        acc = fma(bvec[r], f0, acc);
+        acc = fma(bvec[N + r], f1, acc);
+      }
+      if (DIV) acc = acc / wj[b * N3 + base + r * stride];
+      dst[r * stride] = acc;
+    }
+  }
+}
+
+// Face-array pass (10 arrays [s][side] of N2 per element) along t1 (T=0) or t2 (T=1).
+template <int N, int T>
+__device__ __forceinline__ void tail_face_pass(const double (&op)[N * N], const double* in, int in_es,
+                                               double* out, int out_es, int nb, int tid, int nthr) {
+  constexpr int N2 = N * N;
+  constexpr int stride = T == 0 ? 1 : N;
+  for (int it = tid; it < nb * 10 * N; it += nthr) {
+    const int b = it / (10 * N), r = it - b * 10 * N, bi = r / N, l = r - bi * N;
+    const int base = T == 0 ? N * l : l;
+    const double* src = in + b * in_es + bi * N2 + base;
+    double x[N];
+#pragma unroll
+    for (int a = 0; a < N; ++a) x[a] = src[a * stride];
+    double* dst = out + b * out_es + bi * N2 + base;
+#pragma unroll
+    for (int rr = 0; rr < N; ++rr) {
+      double acc = 0.0;
+#pragma unroll
+      for (int a = 0; a < N; ++a) acc = fma(op[rr * N + a], x[a], acc);
+      dst[rr * stride] = acc;
+    }
+  }
+}
+
+template <int N>
+__global__ void __launch_bounds__(ResCfg<N>::THREADS, ResCfg<N>::MINB)
+    k_residual(ResParams P, ResOps<N> O) {
+  using Cfg = ResCfg<N>;
+  constexpr int N2 = Cfg::N2, N3 = Cfg::N3, EPB = Cfg::EPB, LINES = Cfg::LINES;
+  constexpr int AS = 15 * N3;     // element stride of ACCV
+  constexpr int WS = Cfg::WORK;   // element stride of WORK
+  extern __shared__ double sm[];
+  double* ACCV = sm;                    // [EPB][3][5][N3]
+  double* WORK = ACCV + EPB * AS;       // [EPB][WS]
+  double* WJ = WORK + EPB * WS;         // [EPB][N3]
+  const int tid = threadIdx.x, nthr = blockDim.x;
+  const int e0 = blockIdx.x * EPB;
+  const int nb = min(EPB, P.E - e0);
+  const double g = P.gamma, gm1 = g - 1.0;
+  // stage element data: node primitives (+ reciprocals) of u~, 0.5*C and w J
+  for (int it = tid; it < nb * N3; it += nthr) {
+    const int b = it / N3, q = it - b * N3;
+    const double* src = P.ut_vol + (size_t)(e0 + b) * 5 * N3 + q;
+    double uc[NS];
+#pragma unroll
+    for (int s = 0; s < NS; ++s) uc[s] = src[s * N3];
+    const PrimX pr = d_primx(g, uc);
+    double* Pd = WORK + b * WS;
+    Pd[0 * N3 + q] = pr.rho;
+    Pd[1 * N3 + q] = pr.u;
+    Pd[2 * N3 + q] = pr.v;
+    Pd[3 * N3 + q] = pr.w;
+    Pd[4 * N3 + q] = pr.p;
+    Pd[5 * N3 + q] = pr.rp;
+    Pd[6 * N3 + q] = pr.ir;
+    Pd[7 * N3 + q] = pr.irp;
+    const double wjq = P.wj[(size_t)(e0 + b) * N3 + q];
+    if (!(wjq > 0.0)) atomicOr(P.err, ERR_MESH);
+    WJ[b * N3 + q] = wjq;
+  }
+  for (int it = tid; it < nb * 9 * N3; it += nthr) {
+    const int b = it / (9 * N3), r = it - b * 9 * N3;
+    WORK[b * WS + 8 * N3 + r] = 0.5 * P.cof[(size_t)(e0 + b) * 9 * N3 + r];
+  }
+  __syncthreads();
+
+  // ---- line phase: one thread owns one 1D line (dir, t1, t2) ----
+  double fout0[NS], fout1[NS];  // face rows of the two faces this line pierces (registers)
+  const int lb = tid / LINES;
+  const int ll = tid - lb * LINES;
+  const int ldir = ll / N2, lrem = ll - ldir * N2;
+  if (lb < nb) {
+    const int b = lb, e = e0 + b, dir = ldir, t1 = lrem % N, t2 = lrem / N;
+    const int stride = dir == 0 ? 1 : (dir == 1 ? N : N2);
+    const int lbase = dir == 0 ? N * (t1 + N * t2) : (dir == 1 ? t1 + N2 * t2 : t1 + N * t2);
+    const double* Pd = WORK + b * WS;
+    const double* Ch = Pd + 8 * N3;
+    double* acc = ACCV + b * AS + dir * 5 * N3;
+    const double wt = O.wq[t1] * O.wq[t2];
+#pragma unroll
+    for (int a = 0; a < N; ++a)
+#pragma unroll
+      for (int s = 0; s < NS; ++s) acc[s * N3 + lbase + a * stride] = 0.0;
+    // S6 volume pairs a<b (sumfac.hpp:76-89)
+#pragma unroll 1
+    for (int a = 0; a < N - 1; ++a) {
+      const int ia = lbase + a * stride;
+      const PrimX pa{Pd[ia], Pd[N3 + ia], Pd[2 * N3 + ia], Pd[3 * N3 + ia],
+                     Pd[4 * N3 + ia], Pd[5 * N3 + ia], Pd[6 * N3 + ia], Pd[7 * N3 + ia]};
+      const double ca0 = Ch[(0 + dir) * N3 + ia], ca1 = Ch[(3 + dir) * N3 + ia],
+                   ca2 = Ch[(6 + dir) * N3 + ia];
+      double fa[NS] = {0.0, 0.0, 0.0, 0.0, 0.0};
+#pragma unroll 1
+      for (int bb = a + 1; bb < N; ++bb) {
+        const int ib = lbase + bb * stride;
+        const PrimX pb{Pd[ib], Pd[N3 + ib], Pd[2 * N3 + ib], Pd[3 * N3 + ib],
+                       Pd[4 * N3 + ib], Pd[5 * N3 + ib], Pd[6 * N3 + ib], Pd[7 * N3 + ib]};
+        double f[NS];
+        d_flux_contract_x(gm1, pa, pb, ca0 + Ch[(0 + dir) * N3 + ib], ca1 + Ch[(3 + dir) * N3 + ib],
+                          ca2 + Ch[(6 + dir) * N3 + ib], f);
+        const double c = wt * O.q[a * N + bb];
+#pragma unroll
+        for (int s = 0; s < NS; ++s) {
+          fa[s] = fma(c, f[s], fa[s]);
+          acc[s * N3 + ib] = fma(-c, f[s], acc[s * N3 + ib]);
+        }
+      }
+#pragma unroll
+      for (int s = 0; s < NS; ++s) acc[s * N3 + ia] += fa[s];
+    }
+    // S7 hybrid surface pairs + S8 face flux for the two faces this line pierces
+#pragma unroll 1
+    for (int side = 0; side < 2; ++side) {
+      const int f = 2 * dir + side;
+      const double sign = side ? 1.0 : -1.0;
+      const int k = t1 + N * t2;
+      double uf[NS], un[NS];
+      const double* tr = P.traces + ((size_t)e * 6 + f) * 5 * N2 + k;
+#pragma unroll
+      for (int s = 0; s < NS; ++s) uf[s] = tr[s * N2];
+      {  // neighbour across face f (geometry.hpp:24-29), its face f^1, same node k
+        const int mm = P.m;
+        int i = e % mm, j = (e / mm) % mm, kl = e / (mm * mm);
+        const int step = side ? 1 : -1;
+        const double* nt = nullptr;
+        if (dir == 0) i = (i + step + mm) % mm;
+        if (dir == 1) j = (j + step + mm) % mm;
+        if (dir == 2) {
+          kl += step;
+          if (kl < 0 || kl >= P.nz) {
+            const double* halo = kl < 0 ? P.halo_lo : P.halo_hi;
+            if (halo) nt = halo + (size_t)(i + mm * j) * 5 * N2 + k;
+            kl = (kl + P.nz) % P.nz;
+          }
+        }
+        if (!nt) nt = P.traces + (((size_t)(i + mm * (j + mm * kl))) * 6 + (f ^ 1)) * 5 * N2 + k;
+#pragma unroll
+        for (int s = 0; s < NS; ++s) un[s] = nt[s * N2];
+      }
+      const PrimX pf = d_primx(g, uf);
+      // own face cofactor column C_f[:,dir] = sum_a bound_flux(side,a) C_a (geometry.cpp:218-226)
+      double cf0 = 0.0, cf1 = 0.0, cf2 = 0.0;
+#pragma unroll
+      for (int a = 0; a < N; ++a) {
+        const int ia = lbase + a * stride;
+        const double w = O.bflux[side * N + a];
+        cf0 = fma(w, 2.0 * Ch[(0 + dir) * N3 + ia], cf0);
+        cf1 = fma(w, 2.0 * Ch[(3 + dir) * N3 + ia], cf1);
+        cf2 = fma(w, 2.0 * Ch[(6 + dir) * N3 + ia], cf2);
+      }
+      const double ch0 = 0.5 * cf0, ch1 = 0.5 * cf1, ch2 = 0.5 * cf2;
+      double ff[NS] = {0.0, 0.0, 0.0, 0.0, 0.0};
+#pragma unroll 1
+      for (int a = 0; a < N; ++a) {
+        const int ia = lbase + a * stride;
+        const PrimX pa{Pd[ia], Pd[N3 + ia], Pd[2 * N3 + ia], Pd[3 * N3 + ia],
+                       Pd[4 * N3 + ia], Pd[5 * N3 + ia], Pd[6 * N3 + ia], Pd[7 * N3 + ia]};
+        double fl[NS];
+        d_flux_contract_x(gm1, pa, pf, Ch[(0 + dir) * N3 + ia] + ch0, Ch[(3 + dir) * N3 + ia] + ch1,
+                          Ch[(6 + dir) * N3 + ia] + ch2, fl);
+        const double c = sign * O.bflux[side * N + a] * wt;
+#pragma unroll
+        for (int s = 0; s < NS; ++s) {
+          acc[s * N3 + ia] = fma(c, fl[s], acc[s * N3 + ia]);
+          ff[s] = fma(-c, fl[s], ff[s]);
+        }
+      }
+      // S8 f*.n with the own unit normal and J^Gamma (geometry.cpp:227-236)
+      const double v0 = sign * cf0, v1 = sign * cf1, v2 = sign * cf2;
+      const double jg = sqrt(v0 * v0 + v1 * v1 + v2 * v2);
+      const double ijg = 1.0 / jg;
+      const double nrm[3] = {v0 * ijg, v1 * ijg, v2 * ijg};
+      const PrimX pn = d_primx(g, un);
+      double fn[NS];
+      d_flux_contract_x(gm1, pf, pn, nrm[0], nrm[1], nrm[2], fn);
+      if (P.roe) {
+        double d[NS];
+        if (!d_roe_x(g, uf, un, pf, pn, nrm, d)) atomicOr(P.err, ERR_ROE);
+#pragma unroll
+        for (int s = 0; s < NS; ++s) fn[s] -= d[s];
+      }
+      const double cc = wt * jg;
+      if (side == 0) {
+#pragma unroll
+        for (int s = 0; s < NS; ++s) fout0[s] = fma(cc, fn[s], ff[s]);
+      } else {
+#pragma unroll
+        for (int s = 0; s < NS; ++s) fout1[s] = fma(cc, fn[s], ff[s]);
+      }
+    }
+  }
+  __syncthreads();
+
+  // ---- tail ----
+  const int nbs = nb * 5;
+  // prefetch the RK epilogue operands (same line mapping as the final pass)
+  double pre_un[Cfg::LPT][N], pre_acc[Cfg::LPT][N];
+#pragma unroll
+  for (int j = 0; j < Cfg::LPT; ++j) {
+    const int it = tid + j * nthr;
+#pragma unroll
+    for (int c = 0; c < N; ++c) pre_un[j][c] = pre_acc[j][c] = 0.0;
+    if (it < nbs * N2 && P.stage >= 1) {
+      const int bsi = it / N2, l = it - bsi * N2;
+      const size_t gb = (size_t)e0 * 5 * N3 + (size_t)bsi * N3 + l;  // zeta line: base = l
+#pragma unroll
+      for (int c = 0; c < N; ++c) {
+        pre_un[j][c] = P.un[gb + c * N2];
+        if (P.stage >= 2) pre_acc[j][c] = P.acc[gb + c * N2];
+      }
+    }
+  }
+  // vol = sum of the three direction accumulators (into ACCV[b][0])
+  for (int it = tid; it < nbs * N3; it += nthr) {
+    const int b = it / (5 * N3), r = it - b * 5 * N3;
+    double* a0 = ACCV + b * AS;
+    a0[r] = a0[r] + a0[5 * N3 + r] + a0[10 * N3 + r];
+  }
+  __syncthreads();
+  // face rows -> FACC[b][dir][s][side][N2] = ACCV[b][5N3 : 5N3 + 30N2]
+  double* FACC = ACCV + 5 * N3;
+  if (lb < nb) {
+    const int t1 = lrem % N, t2 = lrem / N, k = t1 + N * t2;
+#pragma unroll
+    for (int s = 0; s < NS; ++s) {
+      FACC[lb * AS + ldir * 10 * N2 + (s * 2 + 0) * N2 + k] = fout0[s];
+      FACC[lb * AS + ldir * 10 * N2 + (s * 2 + 1) * N2 + k] = fout1[s];
+    }
+  }
+  __syncthreads();
+  double* G = WORK + 10 * N3;  // [b][G1: 10N2 | G2: 10N2 | H2: 10N2]
+  if (!P.dS) {
+    // Pi~^T S9 in three fused passes; 1/(w J) in the last
+    tail_pass<N, 0, true, false>(O.M, O.bm, FACC, AS, ACCV, AS, WORK, WS, WJ, nbs, tid, nthr);
+    tail_face_pass<N, 0>(O.M, FACC + 10 * N2, AS, G, WS, nb, tid, nthr);
+    tail_face_pass<N, 0>(O.M, FACC + 20 * N2, AS, G + 10 * N2, WS, nb, tid, nthr);
+    __syncthreads();
+    tail_pass<N, 1, true, false>(O.M, O.bm, G, WS, WORK, WS, WORK + 5 * N3, WS, WJ, nbs, tid, nthr);
+    tail_face_pass<N, 1>(O.M, G + 10 * N2, WS, G + 20 * N2, WS, nb, tid, nthr);
+    __syncthreads();
+    tail_pass<N, 2, true, true>(O.M, O.bm, G + 20 * N2, WS, WORK + 5 * N3, WS, ACCV, AS, WJ, nbs,
+                                tid, nthr);
+    __syncthreads();
+  } else {
+    // entropy diagnostic: R = S9 explicitly (chi^T, bound_sol), -v_hat . R, then Pi~^T
+    tail_pass<N, 0, true, false>(O.it, O.bs, FACC, AS, ACCV, AS, WORK, WS, WJ, nbs, tid, nthr);
+    tail_face_pass<N, 0>(O.it, FACC + 10 * N2, AS, G, WS, nb, tid, nthr);
+    tail_face_pass<N, 0>(O.it, FACC + 20 * N2, AS, G + 10 * N2, WS, nb, tid, nthr);
+    __syncthreads();
+    tail_pass<N, 1, true, false>(O.it, O.bs, G, WS, WORK, WS, WORK + 5 * N3, WS, WJ, nbs, tid, nthr);
+    tail_face_pass<N, 1>(O.it, G + 10 * N2, WS, G + 20 * N2, WS, nb, tid, nthr);
+    __syncthreads();
+    tail_pass<N, 2, true, false>(O.it, O.bs, G + 20 * N2, WS, WORK + 5 * N3, WS, ACCV, AS, WJ, nbs,
+                                 tid, nthr);
+    __syncthreads();
+    for (int it = tid; it < nbs * N3; it += nthr) {
+      const int b = it / (5 * N3), r = it - b * 5 * N3;
+      WORK[b * WS + r] = P.vhat[(size_t)(e0 + b) * 5 * N3 + r] * ACCV[b * AS + r];
+    }
+    __syncthreads();
+    if (tid < nb) {
+      double s = 0.0;
+      for (int r = 0; r < 5 * N3; ++r) s += WORK[tid * WS + r];
+      P.dS[e0 + tid] = -s;
+    }
+    __syncthreads();
+    tail_pass<N, 0, false, false>(O.frt, O.bs, nullptr, 0, ACCV, AS, WORK, WS, WJ, nbs, tid, nthr);
+    __syncthreads();
+    tail_pass<N, 1, false, false>(O.frt, O.bs, nullptr, 0, WORK, WS, WORK + 5 * N3, WS, WJ, nbs, tid,
+                                  nthr);
+    __syncthreads();
+    tail_pass<N, 2, false, true>(O.frt, O.bs, nullptr, 0, WORK + 5 * N3, WS, ACCV, AS, WJ, nbs, tid,
+                                 nthr);
+    __syncthreads();
+  }
+  // second half of S10: Pi~ along xi, eta
+  tail_pass<N, 0, false, false>(O.fr, O.bs, nullptr, 0, ACCV, AS, WORK, WS, WJ, nbs, tid, nthr);
+  __syncthreads();
+  tail_pass<N, 1, false, false>(O.fr, O.bs, nullptr, 0, WORK, WS, WORK + 5 * N3, WS, WJ, nbs, tid,
+                                nthr);
+  __syncthreads();
+  // Pi~ along zeta, negate, RK stage epilogue (zeta lines: coalesced across the warp)
+  const double dt = P.stage ? *P.dt : 0.0;
+  const double hdt = 0.5 * dt, sdt = dt / 6.0;
+#pragma unroll
+  for (int j = 0; j < Cfg::LPT; ++j) {
+    const int it = tid + j * nthr;
+    if (it >= nbs * N2) break;
+    const int bsi = it / N2, l = it - bsi * N2;
+    const int b = bsi / 5, s = bsi - 5 * b;
+    const double* src = WORK + b * WS + 5 * N3 + s * N3 + l;
+    double x[N];
+#pragma unroll
+    for (int a = 0; a < N; ++a) x[a] = src[a * N2];
+    const size_t gb = (size_t)e0 * 5 * N3 + (size_t)bsi * N3 + l;
+#pragma unroll
+    for (int c = 0; c < N; ++c) {
+      double z = 0.0;
+#pragma unroll
+      for (int a = 0; a < N; ++a) z = fma(O.fr[c * N + a], x[a], z);
+      const double kv = -z;
+      const size_t gi = gb + c * N2;
+      switch (P.stage) {
+        case 0: P.out[gi] = kv; break;
+        case 1:
+          P.acc[gi] = kv;
+          P.us[gi] = fma(hdt, kv, pre_un[j][c]);
+          break;
+        case 2:
+          P.acc[gi] = fma(2.0, kv, pre_acc[j][c]);
+          P.us[gi] = fma(hdt, kv, pre_un[j][c]);
+          break;
+        case 3:
+          P.acc[gi] = fma(2.0, kv, pre_acc[j][c]);
+          P.us[gi] = fma(dt, kv, pre_un[j][c]);
+          break;
+        default: {
+          const double a4 = pre_acc[j][c] + kv;
+          P.un[gi] = fma(sdt, a4, pre_un[j][c]);
+        }
+      }
+    }
+  }
+}
+
+}  // namespace nsfr_b200

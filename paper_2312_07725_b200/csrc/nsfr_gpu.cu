@@ -20,6 +20,7 @@ struct nsfr_gpu_ctx {
   nsfr_gpu_setup s{};
   int N = 0, E = 0, m = 0, nz = 0, k0 = 0, k1 = 0;
   Tables1D tab;
+  DevTables htab{};  // host copy of the device tables (source of the kernel-parameter operators)
   DevTables* d_tab = nullptr;
   double *d_un = nullptr, *d_us = nullptr, *d_acc = nullptr, *d_rhs = nullptr;
   double *d_utv = nullptr, *d_tr = nullptr, *d_cof = nullptr, *d_jac = nullptr, *d_wj = nullptr;
@@ -92,11 +93,52 @@ void ev_end(nsfr_gpu_ctx* c) {
   cudaEventRecord(c->ev_pool.back(), c->st);
 }
 
+// 1D operators for the kernel-parameter bank, from the host table copy
+template <int N>
+ProjOps<N> proj_ops(const DevTables& t) {
+  ProjOps<N> o{};
+  for (int i = 0; i < N * N; ++i) {
+    o.interp[i] = t.interp[i];
+    o.proj[i] = t.proj[i];
+  }
+  for (int i = 0; i < 2 * N; ++i) o.bsol[i] = t.bsol[i];
+  return o;
+}
+
+template <int N>
+ResOps<N> res_ops(const DevTables& t) {
+  ResOps<N> o{};
+  for (int a = 0; a < N; ++a)
+    for (int i = 0; i < N; ++i) {
+      // M = Pi~^T chi^T: (Pi~^T)[a][r] = frproj[r][a], (chi^T)[r][i] = interp[i][r]
+      double s = 0.0;
+      for (int r = 0; r < N; ++r) s += t.frproj[r * N + a] * t.interp[i * N + r];
+      o.M[a * N + i] = s;
+    }
+  for (int side = 0; side < 2; ++side)
+    for (int a = 0; a < N; ++a) {
+      double s = 0.0;
+      for (int r = 0; r < N; ++r) s += t.frproj[r * N + a] * t.bsol[side * N + r];
+      o.bm[side * N + a] = s;
+    }
+  for (int i = 0; i < N * N; ++i) {
+    o.fr[i] = t.frproj[i];
+    o.frt[i] = t.frproj_t[i];
+    o.it[i] = t.interp_t[i];
+    o.q[i] = t.qskew[i];
+  }
+  for (int i = 0; i < 2 * N; ++i) {
+    o.bs[i] = t.bsol[i];
+    o.bflux[i] = t.bflux[i];
+  }
+  for (int i = 0; i < N; ++i) o.wq[i] = t.wq[i];
+  return o;
+}
+
 template <int N>
 int launch_project(nsfr_gpu_ctx* ctx, const double* u, bool want_lam) {
   if (int rc = set_attrs<N>(ctx)) return rc;
   ProjParams P{};
-  P.tab = ctx->d_tab;
   P.u = u;
   P.ut_vol = ctx->d_utv;
   P.traces = ctx->d_tr;
@@ -111,7 +153,7 @@ int launch_project(nsfr_gpu_ctx* ctx, const double* u, bool want_lam) {
   P.gamma = ctx->s.gamma;
   const int grid = (ctx->E + ProjCfg<N>::EPB - 1) / ProjCfg<N>::EPB;
   ev_begin(ctx, 1);
-  k_project<N><<<grid, ProjCfg<N>::THREADS, ProjCfg<N>::SMEM, ctx->st>>>(P);
+  k_project<N><<<grid, ProjCfg<N>::THREADS, ProjCfg<N>::SMEM, ctx->st>>>(P, proj_ops<N>(ctx->htab));
   ev_end(ctx);
   ++ctx->launches;
   CK(cudaGetLastError());
@@ -121,7 +163,6 @@ int launch_project(nsfr_gpu_ctx* ctx, const double* u, bool want_lam) {
 template <int N>
 int launch_residual(nsfr_gpu_ctx* ctx, int stage, bool entropy) {
   ResParams P{};
-  P.tab = ctx->d_tab;
   P.ut_vol = ctx->d_utv;
   P.traces = ctx->d_tr;
   P.halo_lo = ctx->nranks > 1 ? ctx->d_halo_lo : nullptr;
@@ -144,7 +185,7 @@ int launch_residual(nsfr_gpu_ctx* ctx, int stage, bool entropy) {
   P.roe = ctx->s.roe;
   const int grid = (ctx->E + ResCfg<N>::EPB - 1) / ResCfg<N>::EPB;
   ev_begin(ctx, 2);
-  k_residual<N><<<grid, ResCfg<N>::THREADS, ResCfg<N>::SMEM, ctx->st>>>(P);
+  k_residual<N><<<grid, ResCfg<N>::THREADS, ResCfg<N>::SMEM, ctx->st>>>(P, res_ops<N>(ctx->htab));
   ev_end(ctx);
   ++ctx->launches;
   CK(cudaGetLastError());
@@ -387,6 +428,7 @@ int nsfr_gpu_create(const nsfr_gpu_setup* setup, nsfr_gpu_ctx** out) {
   }
   DevTables dt;
   fill_dev_tables(ctx->tab, s.tables && s.tables->interp ? s.tables : nullptr, dt);
+  ctx->htab = dt;
   const size_t ns = state_count(ctx), n3 = static_cast<size_t>(ctx->E) * nsol(ctx);
   const size_t ntr = static_cast<size_t>(ctx->E) * 6 * NS * ctx->N * ctx->N;
   auto alloc = [&](double** p, size_t n) { return cudaMalloc(p, sizeof(double) * std::max<size_t>(n, 1)); };

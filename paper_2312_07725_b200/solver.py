@@ -20,7 +20,7 @@ from dataclasses import dataclass, field
 import numpy as np
 
 HERE = os.path.dirname(os.path.abspath(__file__))
-LIB_PATH = os.path.join(HERE, "libnsfr_b200.so")
+LIB_PATH = os.environ.get("NSFR_B200_LIB") or os.path.join(HERE, "libnsfr_b200.so")
 
 CASES = {"vortex": 0, "tgv": 1, "free_stream": 2}
 C_PLUS = {2: 0.5 * 0.206, 3: 0.5 * 3.80e-3, 4: 0.5 * 4.67e-5, 5: 0.5 * 4.28e-7}
