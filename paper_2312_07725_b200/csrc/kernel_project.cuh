@@ -18,7 +18,7 @@ namespace nsfr_b200 {
 
 struct ProjParams {
   const double* u;       // [E][5][N^3] stage input
-  double* ut_vol;        // [E][5][N^3] entropy-projected conservative (volume)
+  double* ut_vol;        // [E][6][N^3] rho,u,v,w,p,rho/p of the entropy-projected volume state
   double* traces;        // [E][6][5][N^2]
   double* vhat;          // [E][5][N^3] or nullptr
   double* send_lo;       // [m*m][5][N^2] face 4 of plane 0, or nullptr
@@ -107,10 +107,9 @@ __device__ __forceinline__ void face_pass(const double (&op)[N * N], const doubl
 }
 
 template <int N>
-__global__ void __launch_bounds__(ProjCfg<N>::THREADS) k_project(ProjParams P, ProjOps<N> O) {
+__device__ __forceinline__ void proj_batch(const ProjParams& P, const ProjOps<N>& O, int e0, double* sm) {
   using Cfg = ProjCfg<N>;
   constexpr int N2 = Cfg::N2, N3 = Cfg::N3, EPB = Cfg::EPB;
-  extern __shared__ double sm[];
   double* A = sm;
   double* B = A + EPB * 5 * N3;
   double* V = B + EPB * 5 * N3;
@@ -122,7 +121,6 @@ __global__ void __launch_bounds__(ProjCfg<N>::THREADS) k_project(ProjParams P, P
   double* F1 = F2 + EPB * 10 * N2;  // [EPB*5][2][N2]  dir-1 faces: chi_zeta T1
   double* F0 = F1 + EPB * 10 * N2;  // [EPB*5][2][N2]  dir-0 faces: chi_zeta T0b
   const int tid = threadIdx.x, nthr = blockDim.x;
-  const int e0 = blockIdx.x * EPB;
   const int nb = min(EPB, P.E - e0);
   const double g = P.gamma;
   {
@@ -195,9 +193,16 @@ __global__ void __launch_bounds__(ProjCfg<N>::THREADS) k_project(ProjParams P, P
 #pragma unroll
     for (int s = 0; s < NS; ++s) vv[s] = C4[(b * 5 + s) * N3 + q];
     if (!d_entropy_to_cons(g, vv, uu)) atomicOr(P.err, ERR_STATE);
-    double* dst = P.ut_vol + (size_t)(e0 + b) * 5 * N3 + q;
-#pragma unroll
-    for (int s = 0; s < NS; ++s) dst[s * N3] = uu[s];
+    // K2 consumes the per-node primitive bundle (prim(), euler.cpp:109-115,
+    // plus rho/p and the two reciprocals its log means use)
+    const PrimX pr = d_primx(g, uu);
+    double* dst = P.ut_vol + (size_t)(e0 + b) * 6 * N3 + q;
+    dst[0 * N3] = pr.rho;
+    dst[1 * N3] = pr.u;
+    dst[2 * N3] = pr.v;
+    dst[3 * N3] = pr.w;
+    dst[4 * N3] = pr.p;
+    dst[5 * N3] = pr.rp;
   }
   for (int it = tid; it < nb * 6 * N2; it += nthr) {
     const int b = it / (6 * N2), r = it - b * 6 * N2, f = r / N2, k = r - f * N2;
@@ -222,6 +227,21 @@ __global__ void __launch_bounds__(ProjCfg<N>::THREADS) k_project(ProjParams P, P
       for (int s = 0; s < NS; ++s) P.send_hi[((size_t)plane * 5 + s) * N2 + k] = uu[s];
     }
   }
+}
+
+// One batch per CTA; L2 prefetch of the input block of the CTA `ahead`
+// (= #resident CTAs) later (see k_residual).
+template <int N>
+__global__ void __launch_bounds__(ProjCfg<N>::THREADS) k_project(ProjParams P, ProjOps<N> O, int ahead) {
+  extern __shared__ double sm[];
+  constexpr int EPB = ProjCfg<N>::EPB, N3 = N * N * N;
+  const int nbatch = (P.E + EPB - 1) / EPB;
+  const long long pb = static_cast<long long>(blockIdx.x) + ahead;
+  if (threadIdx.x == 0 && pb < nbatch) {
+    const int e0 = pb * EPB, nb = min(EPB, P.E - e0);
+    l2_prefetch(P.u + (size_t)e0 * 5 * N3, (size_t)nb * 5 * N3 * sizeof(double));
+  }
+  proj_batch<N>(P, O, blockIdx.x * EPB, sm);
 }
 
 }  // namespace nsfr_b200

@@ -26,11 +26,11 @@
 namespace nsfr_b200 {
 
 struct ResParams {
-  const double* ut_vol;   // [E][5][N^3]
+  const double* ut_vol;   // [E][6][N^3] rho,u,v,w,p,rho/p of u~ (K1)
   const double* traces;   // [E][6][5][N^2]
   const double* halo_lo;  // [m*m][5][N^2] face 5 of plane k0-1 (nullptr: wrap locally)
   const double* halo_hi;  // [m*m][5][N^2] face 4 of plane k1
-  const double* cof;      // [E][9][N^3]
+  const double* cof;      // [E][9][N^3] = 0.5 C
   const double* wj;       // [E][N^3]
   const double* vhat;     // [E][5][N^3] or nullptr
   double* dS;             // [E] or nullptr
@@ -66,7 +66,7 @@ struct ResCfg {
   static constexpr int THREADS = ((EPB * LINES + 31) / 32) * 32;
   // WORK: line phase = 8 N3 node primitives + 9 N3 half cofactors;
   //       tail = 10 N3 pass buffers + 30 N2 face-lift buffers
-  static constexpr int WORK = (17 * N3 > 10 * N3 + 30 * N2) ? 17 * N3 : 10 * N3 + 30 * N2;
+  static constexpr int WORK = (15 * N3 > 10 * N3 + 30 * N2) ? 15 * N3 : 10 * N3 + 30 * N2;
   static constexpr int PER_EL = 15 * N3 + WORK + N3;  // ACCV (3 x 5 N3) + WORK + w J
   static constexpr int SMEM = EPB * PER_EL * 8;
 #ifdef NSFR_RES_MINB
@@ -141,46 +141,65 @@ __device__ __forceinline__ void tail_face_pass(const double (&op)[N * N], const 
   }
 }
 
+// L2 prefetch of everything batch `e0` will read (issued one batch ahead).
 template <int N>
-__global__ void __launch_bounds__(ResCfg<N>::THREADS, ResCfg<N>::MINB)
-    k_residual(ResParams P, ResOps<N> O) {
+__device__ __forceinline__ void res_prefetch(const ResParams& P, int e0, int tid) {
+  using Cfg = ResCfg<N>;
+  constexpr int N2 = Cfg::N2, N3 = Cfg::N3, EPB = Cfg::EPB;
+  if (e0 >= P.E || tid >= 32) return;
+  const int nb = min(EPB, P.E - e0);
+  const size_t b8 = sizeof(double);
+  switch (tid) {
+    case 0: l2_prefetch(P.ut_vol + (size_t)e0 * 6 * N3, nb * 6 * N3 * b8); break;
+    case 1: l2_prefetch(P.cof + (size_t)e0 * 9 * N3, nb * 9 * N3 * b8); break;
+    case 2: l2_prefetch(P.wj + (size_t)e0 * N3, nb * N3 * b8); break;
+    case 3: l2_prefetch(P.traces + (size_t)e0 * 30 * N2, nb * 30 * N2 * b8); break;
+    case 4: if (P.stage >= 1) l2_prefetch(P.un + (size_t)e0 * 5 * N3, nb * 5 * N3 * b8); break;
+    case 5: if (P.stage >= 2) l2_prefetch(P.acc + (size_t)e0 * 5 * N3, nb * 5 * N3 * b8); break;
+    default: {  // neighbour face blocks (geometry.hpp:24-29), lanes 6.. : (element, face)
+      const int j = tid - 6;
+      if (j >= 6 * nb) break;
+      const int e = e0 + j / 6, f = j % 6, dir = f / 2, step = (f & 1) ? 1 : -1;
+      const int mm = P.m;
+      int i = e % mm, jj = (e / mm) % mm, kl = e / (mm * mm);
+      if (dir == 0) i = (i + step + mm) % mm;
+      if (dir == 1) jj = (jj + step + mm) % mm;
+      if (dir == 2) {
+        kl += step;
+        if (kl < 0 || kl >= P.nz) {
+          const double* halo = kl < 0 ? P.halo_lo : P.halo_hi;
+          if (halo) {
+            l2_prefetch(halo + (size_t)(i + mm * jj) * 5 * N2, 5 * N2 * b8);
+            break;
+          }
+          kl = (kl + P.nz) % P.nz;
+        }
+      }
+      l2_prefetch(P.traces + ((size_t)(i + mm * (jj + mm * kl)) * 6 + (f ^ 1)) * 5 * N2, 5 * N2 * b8);
+    }
+  }
+}
+
+template <int N>
+__device__ __forceinline__ void res_batch(const ResParams& P, const ResOps<N>& O, int e0, double* sm) {
   using Cfg = ResCfg<N>;
   constexpr int N2 = Cfg::N2, N3 = Cfg::N3, EPB = Cfg::EPB, LINES = Cfg::LINES;
   constexpr int AS = 15 * N3;     // element stride of ACCV
   constexpr int WS = Cfg::WORK;   // element stride of WORK
-  extern __shared__ double sm[];
   double* ACCV = sm;                    // [EPB][3][5][N3]
   double* WORK = ACCV + EPB * AS;       // [EPB][WS]
   double* WJ = WORK + EPB * WS;         // [EPB][N3]
   const int tid = threadIdx.x, nthr = blockDim.x;
-  const int e0 = blockIdx.x * EPB;
   const int nb = min(EPB, P.E - e0);
   const double g = P.gamma, gm1 = g - 1.0;
-  // stage element data: node primitives (+ reciprocals) of u~, 0.5*C and w J
-  for (int it = tid; it < nb * N3; it += nthr) {
-    const int b = it / N3, q = it - b * N3;
-    const double* src = P.ut_vol + (size_t)(e0 + b) * 5 * N3 + q;
-    double uc[NS];
-#pragma unroll
-    for (int s = 0; s < NS; ++s) uc[s] = src[s * N3];
-    const PrimX pr = d_primx(g, uc);
-    double* Pd = WORK + b * WS;
-    Pd[0 * N3 + q] = pr.rho;
-    Pd[1 * N3 + q] = pr.u;
-    Pd[2 * N3 + q] = pr.v;
-    Pd[3 * N3 + q] = pr.w;
-    Pd[4 * N3 + q] = pr.p;
-    Pd[5 * N3 + q] = pr.rp;
-    Pd[6 * N3 + q] = pr.ir;
-    Pd[7 * N3 + q] = pr.irp;
-    const double wjq = P.wj[(size_t)(e0 + b) * N3 + q];
-    if (!(wjq > 0.0)) atomicOr(P.err, ERR_MESH);
-    WJ[b * N3 + q] = wjq;
+  // stage element data (pure copies): node primitives of u~ (written by K1),
+  // 0.5 C (stored pre-halved) and w J
+  for (int it = tid; it < nb * 15 * N3; it += nthr) {
+    const int b = it / (15 * N3), r = it - b * 15 * N3;
+    WORK[b * WS + r] = r < 6 * N3 ? P.ut_vol[(size_t)(e0 + b) * 6 * N3 + r]
+                                  : P.cof[(size_t)(e0 + b) * 9 * N3 + (r - 6 * N3)];
   }
-  for (int it = tid; it < nb * 9 * N3; it += nthr) {
-    const int b = it / (9 * N3), r = it - b * 9 * N3;
-    WORK[b * WS + 8 * N3 + r] = 0.5 * P.cof[(size_t)(e0 + b) * 9 * N3 + r];
-  }
+  for (int it = tid; it < nb * N3; it += nthr) WJ[it] = P.wj[(size_t)e0 * N3 + it];
   __syncthreads();
 
   // ---- line phase: one thread owns one 1D line (dir, t1, t2) ----
@@ -193,7 +212,7 @@ __global__ void __launch_bounds__(ResCfg<N>::THREADS, ResCfg<N>::MINB)
     const int stride = dir == 0 ? 1 : (dir == 1 ? N : N2);
     const int lbase = dir == 0 ? N * (t1 + N * t2) : (dir == 1 ? t1 + N2 * t2 : t1 + N * t2);
     const double* Pd = WORK + b * WS;
-    const double* Ch = Pd + 8 * N3;
+    const double* Ch = Pd + 6 * N3;
     double* acc = ACCV + b * AS + dir * 5 * N3;
     const double wt = O.wq[t1] * O.wq[t2];
 #pragma unroll
@@ -205,7 +224,7 @@ __global__ void __launch_bounds__(ResCfg<N>::THREADS, ResCfg<N>::MINB)
     for (int a = 0; a < N - 1; ++a) {
       const int ia = lbase + a * stride;
       const PrimX pa{Pd[ia], Pd[N3 + ia], Pd[2 * N3 + ia], Pd[3 * N3 + ia],
-                     Pd[4 * N3 + ia], Pd[5 * N3 + ia], Pd[6 * N3 + ia], Pd[7 * N3 + ia]};
+                     Pd[4 * N3 + ia], Pd[5 * N3 + ia], 0.0};
       const double ca0 = Ch[(0 + dir) * N3 + ia], ca1 = Ch[(3 + dir) * N3 + ia],
                    ca2 = Ch[(6 + dir) * N3 + ia];
       double fa[NS] = {0.0, 0.0, 0.0, 0.0, 0.0};
@@ -213,7 +232,7 @@ __global__ void __launch_bounds__(ResCfg<N>::THREADS, ResCfg<N>::MINB)
       for (int bb = a + 1; bb < N; ++bb) {
         const int ib = lbase + bb * stride;
         const PrimX pb{Pd[ib], Pd[N3 + ib], Pd[2 * N3 + ib], Pd[3 * N3 + ib],
-                       Pd[4 * N3 + ib], Pd[5 * N3 + ib], Pd[6 * N3 + ib], Pd[7 * N3 + ib]};
+                       Pd[4 * N3 + ib], Pd[5 * N3 + ib], 0.0};
         double f[NS];
         d_flux_contract_x(gm1, pa, pb, ca0 + Ch[(0 + dir) * N3 + ib], ca1 + Ch[(3 + dir) * N3 + ib],
                           ca2 + Ch[(6 + dir) * N3 + ib], f);
@@ -273,7 +292,7 @@ __global__ void __launch_bounds__(ResCfg<N>::THREADS, ResCfg<N>::MINB)
       for (int a = 0; a < N; ++a) {
         const int ia = lbase + a * stride;
         const PrimX pa{Pd[ia], Pd[N3 + ia], Pd[2 * N3 + ia], Pd[3 * N3 + ia],
-                       Pd[4 * N3 + ia], Pd[5 * N3 + ia], Pd[6 * N3 + ia], Pd[7 * N3 + ia]};
+                       Pd[4 * N3 + ia], Pd[5 * N3 + ia], 0.0};
         double fl[NS];
         d_flux_contract_x(gm1, pa, pf, Ch[(0 + dir) * N3 + ia] + ch0, Ch[(3 + dir) * N3 + ia] + ch1,
                           Ch[(6 + dir) * N3 + ia] + ch2, fl);
@@ -440,6 +459,21 @@ __global__ void __launch_bounds__(ResCfg<N>::THREADS, ResCfg<N>::MINB)
       }
     }
   }
+}
+
+// One batch per CTA (CTAs retire at staggered times, so their staging, line
+// and tail phases overlap on each SM — a persistent grid that walks batches
+// in lockstep measured slower). Each CTA prefetches into L2 the batch of the
+// CTA `ahead` = #resident CTAs later, which the block scheduler starts about
+// when this one retires, so that CTA's staging loads hit L2.
+template <int N>
+__global__ void __launch_bounds__(ResCfg<N>::THREADS, ResCfg<N>::MINB)
+    k_residual(ResParams P, ResOps<N> O, int ahead) {
+  extern __shared__ double sm[];
+  constexpr int EPB = ResCfg<N>::EPB;
+  const long long pe = (static_cast<long long>(blockIdx.x) + ahead) * EPB;
+  if (pe < P.E) res_prefetch<N>(P, static_cast<int>(pe), threadIdx.x);
+  res_batch<N>(P, O, blockIdx.x * EPB, sm);
 }
 
 }  // namespace nsfr_b200

@@ -68,13 +68,25 @@ thread_local std::string g_create_error;
 size_t nsol(const nsfr_gpu_ctx* c) { return static_cast<size_t>(c->N) * c->N * c->N; }
 size_t state_count(const nsfr_gpu_ctx* c) { return static_cast<size_t>(c->E) * NS * nsol(c); }
 
+// Per-N launch configuration of the persistent kernels: resident CTAs on the device.
+template <int N>
+struct Resident {
+  static inline int proj = 0, res = 0;
+};
+
 template <int N>
 int set_attrs(nsfr_gpu_ctx* ctx) {
-  static bool done = false;
-  if (done) return NSFR_OK;
+  if (Resident<N>::res) return NSFR_OK;
   CK(cudaFuncSetAttribute(k_project<N>, cudaFuncAttributeMaxDynamicSharedMemorySize, ProjCfg<N>::SMEM));
   CK(cudaFuncSetAttribute(k_residual<N>, cudaFuncAttributeMaxDynamicSharedMemorySize, ResCfg<N>::SMEM));
-  done = true;
+  int sms = 0, bp = 0, br = 0;
+  CK(cudaDeviceGetAttribute(&sms, cudaDevAttrMultiProcessorCount, ctx->s.device));
+  CK(cudaOccupancyMaxActiveBlocksPerMultiprocessor(&bp, k_project<N>, ProjCfg<N>::THREADS, ProjCfg<N>::SMEM));
+  CK(cudaOccupancyMaxActiveBlocksPerMultiprocessor(&br, k_residual<N>, ResCfg<N>::THREADS, ResCfg<N>::SMEM));
+  // NSFR_NO_PREFETCH=1 disables the look-ahead L2 prefetch (A/B measurements)
+  const bool pf = std::getenv("NSFR_NO_PREFETCH") == nullptr;
+  Resident<N>::proj = pf ? sms * std::max(bp, 1) : (1 << 30);
+  Resident<N>::res = pf ? sms * std::max(br, 1) : (1 << 30);
   return NSFR_OK;
 }
 
@@ -153,7 +165,8 @@ int launch_project(nsfr_gpu_ctx* ctx, const double* u, bool want_lam) {
   P.gamma = ctx->s.gamma;
   const int grid = (ctx->E + ProjCfg<N>::EPB - 1) / ProjCfg<N>::EPB;
   ev_begin(ctx, 1);
-  k_project<N><<<grid, ProjCfg<N>::THREADS, ProjCfg<N>::SMEM, ctx->st>>>(P, proj_ops<N>(ctx->htab));
+  k_project<N><<<grid, ProjCfg<N>::THREADS, ProjCfg<N>::SMEM, ctx->st>>>(P, proj_ops<N>(ctx->htab),
+                                                                           Resident<N>::proj);
   ev_end(ctx);
   ++ctx->launches;
   CK(cudaGetLastError());
@@ -183,9 +196,11 @@ int launch_residual(nsfr_gpu_ctx* ctx, int stage, bool entropy) {
   P.nz = ctx->nz;
   P.gamma = ctx->s.gamma;
   P.roe = ctx->s.roe;
+  if (int rc = set_attrs<N>(ctx)) return rc;
   const int grid = (ctx->E + ResCfg<N>::EPB - 1) / ResCfg<N>::EPB;
   ev_begin(ctx, 2);
-  k_residual<N><<<grid, ResCfg<N>::THREADS, ResCfg<N>::SMEM, ctx->st>>>(P, res_ops<N>(ctx->htab));
+  k_residual<N><<<grid, ResCfg<N>::THREADS, ResCfg<N>::SMEM, ctx->st>>>(P, res_ops<N>(ctx->htab),
+                                                                         Resident<N>::res);
   ev_end(ctx);
   ++ctx->launches;
   CK(cudaGetLastError());
@@ -433,7 +448,7 @@ int nsfr_gpu_create(const nsfr_gpu_setup* setup, nsfr_gpu_ctx** out) {
   const size_t ntr = static_cast<size_t>(ctx->E) * 6 * NS * ctx->N * ctx->N;
   auto alloc = [&](double** p, size_t n) { return cudaMalloc(p, sizeof(double) * std::max<size_t>(n, 1)); };
   if (cudaMalloc(&ctx->d_tab, sizeof(DevTables)) || alloc(&ctx->d_un, ns) || alloc(&ctx->d_us, ns) ||
-      alloc(&ctx->d_acc, ns) || alloc(&ctx->d_rhs, ns) || alloc(&ctx->d_utv, ns) ||
+      alloc(&ctx->d_acc, ns) || alloc(&ctx->d_rhs, ns) || alloc(&ctx->d_utv, 6 * n3) ||
       alloc(&ctx->d_tr, ntr) || alloc(&ctx->d_cof, 9 * n3) || alloc(&ctx->d_jac, n3) ||
       alloc(&ctx->d_wj, n3) || alloc(&ctx->d_dS, ctx->E) || alloc(&ctx->d_part, 2 * (size_t)ctx->E) ||
       alloc(&ctx->d_red, 4) || cudaMalloc(&ctx->d_step, sizeof(StepState)) ||
@@ -482,7 +497,7 @@ int nsfr_gpu_create(const nsfr_gpu_setup* setup, nsfr_gpu_ctx** out) {
     return fail(NSFR_E_CUDA);
   }
   if (setup->jac_vol && setup->cof_vol) {
-    // caller-built metrics (ElementMetrics layout [e][q][9]) -> [e][9][q], wj = w J
+    // caller-built metrics (ElementMetrics layout [e][q][9]) -> 0.5 C as [e][9][q], wj = w J
     const int N3 = static_cast<int>(nsol(ctx));
     std::vector<double> cof(9 * n3), wj(n3);
     const auto& wq = (s.tables && s.tables->wq) ? std::vector<double>(s.tables->wq, s.tables->wq + ctx->N)
@@ -490,7 +505,8 @@ int nsfr_gpu_create(const nsfr_gpu_setup* setup, nsfr_gpu_ctx** out) {
     for (int e = 0; e < ctx->E; ++e)
       for (int q = 0; q < N3; ++q) {
         for (int c = 0; c < 9; ++c)
-          cof[(static_cast<size_t>(e) * 9 + c) * N3 + q] = setup->cof_vol[(static_cast<size_t>(e) * N3 + q) * 9 + c];
+          cof[(static_cast<size_t>(e) * 9 + c) * N3 + q] =
+              0.5 * setup->cof_vol[(static_cast<size_t>(e) * N3 + q) * 9 + c];
         const int i = q % ctx->N, j = (q / ctx->N) % ctx->N, k = q / (ctx->N * ctx->N);
         double w = wq[i];
         w *= wq[j];
@@ -571,7 +587,7 @@ int nsfr_gpu_get_metrics(nsfr_gpu_ctx* ctx, double* jac, double* cof) {
     for (int e = 0; e < ctx->E; ++e)
       for (int q = 0; q < N3; ++q)
         for (int k = 0; k < 9; ++k)
-          cof[(static_cast<size_t>(e) * N3 + q) * 9 + k] = c[(static_cast<size_t>(e) * 9 + k) * N3 + q];
+          cof[(static_cast<size_t>(e) * N3 + q) * 9 + k] = 2.0 * c[(static_cast<size_t>(e) * 9 + k) * N3 + q];
   }
   return NSFR_OK;
 }

@@ -5,7 +5,8 @@
 //   k_l2        L2 error partials; k_reduce deterministic sums
 //   k_step_*    adaptive-dt bookkeeping
 // Layout in HBM (element-contiguous blocks, xi fastest):
-//   state/us/acc/ut_vol [E][5][N^3]; traces [E][6][5][N^2]; cof [E][9][N^3]
+//   state/us/acc [E][5][N^3]; ut_vol [E][8][N^3] node primitives; traces [E][6][5][N^2];
+//   cof [E][9][N^3] = 0.5 C
 //   (component 3*n_phys + i_ref major); wj [E][N^3] = w_i w_j w_k J.
 #pragma once
 #include <cuda_runtime.h>
@@ -197,7 +198,8 @@ __global__ void k_metrics(MetricParams P) {
       tp_pass_rt(T.quad_diff, nq, k, aq + (3 * n + j) * N3, nq, nq, nq, d1, tid, nthr);
       tp_pass_rt(T.quad_diff, nq, j, aq + (3 * n + k) * N3, nq, nq, nq, d2, tid, nthr);
       __syncthreads();
-      for (int q = tid; q < N3; q += nthr) C[(3 * n + i) * N3 + q] = d1[q] - d2[q];
+      // stored pre-halved: K2 uses 0.5 (C_i + C_j) = Ch_i + Ch_j exactly
+      for (int q = tid; q < N3; q += nthr) C[(3 * n + i) * N3 + q] = 0.5 * (d1[q] - d2[q]);
     }
   __syncthreads();
   // face normals must be nondegenerate (geometry.cpp:227-233)
@@ -210,7 +212,7 @@ __global__ void k_metrics(MetricParams P) {
       for (int a = 0; a < nq; ++a) {
         const int q = dir == 0 ? a + nq * (t1i + nq * t2i)
                                : (dir == 1 ? t1i + nq * (a + nq * t2i) : t1i + nq * (t2i + nq * a));
-        cf = fma(T.bflux[side * nq + a], C[(3 * n + dir) * N3 + q], cf);
+        cf = fma(T.bflux[side * nq + a], 2.0 * C[(3 * n + dir) * N3 + q], cf);
       }
       v2 += cf * cf;
     }
