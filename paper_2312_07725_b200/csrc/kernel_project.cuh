@@ -34,7 +34,13 @@ struct ProjOps {
   double interp[N * N];  // chi   (nq x np)
   double proj[N * N];    // Pi    (np x nq)
   double bsol[2 * N];    // bound_sol rows at xi = -1, +1
+  double c35;            // gm1^(1/gm1) when gamma/(gamma-1) == 7/2 (closed-form u(v)), else 0
 };
+
+template <int N>
+__device__ __forceinline__ bool u_of_v(const ProjOps<N>& O, double g, const double* v, double* u) {
+  return O.c35 > 0.0 ? d_entropy_to_cons_35(g, O.c35, v, u) : d_entropy_to_cons(g, v, u);
+}
 
 template <int N>
 struct ProjCfg {
@@ -192,7 +198,7 @@ __device__ __forceinline__ void proj_batch(const ProjParams& P, const ProjOps<N>
     double vv[NS], uu[NS];
 #pragma unroll
     for (int s = 0; s < NS; ++s) vv[s] = C4[(b * 5 + s) * N3 + q];
-    if (!d_entropy_to_cons(g, vv, uu)) atomicOr(P.err, ERR_STATE);
+    if (!u_of_v<N>(O, g, vv, uu)) atomicOr(P.err, ERR_STATE);
     // K2 consumes the per-node primitive bundle (prim(), euler.cpp:109-115,
     // plus rho/p and the two reciprocals its log means use)
     const PrimX pr = d_primx(g, uu);
@@ -211,7 +217,7 @@ __device__ __forceinline__ void proj_batch(const ProjParams& P, const ProjOps<N>
     double vv[NS], uu[NS];
 #pragma unroll
     for (int s = 0; s < NS; ++s) vv[s] = Fd[((b * 5 + s) * 2 + side) * N2 + k];
-    if (!d_entropy_to_cons(g, vv, uu)) atomicOr(P.err, ERR_STATE);
+    if (!u_of_v<N>(O, g, vv, uu)) atomicOr(P.err, ERR_STATE);
     const int e = e0 + b;
     double* dst = P.traces + ((size_t)e * 6 + f) * 5 * N2 + k;
 #pragma unroll

@@ -114,6 +114,7 @@ ProjOps<N> proj_ops(const DevTables& t) {
     o.proj[i] = t.proj[i];
   }
   for (int i = 0; i < 2 * N; ++i) o.bsol[i] = t.bsol[i];
+  o.c35 = 0.0;
   return o;
 }
 
@@ -164,9 +165,14 @@ int launch_project(nsfr_gpu_ctx* ctx, const double* u, bool want_lam) {
   P.nz = ctx->nz;
   P.gamma = ctx->s.gamma;
   const int grid = (ctx->E + ProjCfg<N>::EPB - 1) / ProjCfg<N>::EPB;
+  ProjOps<N> ops = proj_ops<N>(ctx->htab);
+  {  // closed-form u(v) when gamma/(gamma-1) == 7/2 in exact arithmetic (gamma = 1.4)
+    const double g = ctx->s.gamma, gm1 = g - 1.0;
+    if (std::fabs(g / gm1 - 3.5) < 1e-12 && std::getenv("NSFR_POW_U_OF_V") == nullptr)
+      ops.c35 = std::pow(gm1, 1.0 / gm1);
+  }
   ev_begin(ctx, 1);
-  k_project<N><<<grid, ProjCfg<N>::THREADS, ProjCfg<N>::SMEM, ctx->st>>>(P, proj_ops<N>(ctx->htab),
-                                                                           Resident<N>::proj);
+  k_project<N><<<grid, ProjCfg<N>::THREADS, ProjCfg<N>::SMEM, ctx->st>>>(P, ops, Resident<N>::proj);
   ev_end(ctx);
   ++ctx->launches;
   CK(cudaGetLastError());

@@ -298,8 +298,10 @@ class GpuSolver:
         assert u.shape == self.state_shape, (u.shape, self.state_shape)
         self._check(self.lib.nsfr_gpu_set_state(self.ctx, _ptr(u)))
 
-    def get_state(self) -> np.ndarray:
-        u = np.zeros(self.state_shape)
+    def get_state(self, out: np.ndarray | None = None) -> np.ndarray:
+        """Download the state; `out` (e.g. a pinned host buffer) is filled in place."""
+        u = np.zeros(self.state_shape) if out is None else out
+        assert u.shape == self.state_shape and u.dtype == np.float64 and u.flags.c_contiguous
         self._check(self.lib.nsfr_gpu_get_state(self.ctx, _ptr(u)))
         return u
 
