@@ -131,7 +131,8 @@ __device__ __forceinline__ void proj_batch(const ProjParams& P, const ProjOps<N>
   const double g = P.gamma;
   {
     const double* src = P.u + (size_t)e0 * 5 * N3;
-    for (int i = tid; i < nb * 5 * N3; i += nthr) A[i] = src[i];
+    for (int i = tid; i < nb * 5 * N3; i += nthr) cp_async8(&A[i], src + i);
+    cp_async_wait_all();
   }
   __syncthreads();
   const int nbs = nb * 5;

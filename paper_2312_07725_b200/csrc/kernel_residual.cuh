@@ -25,6 +25,24 @@
 
 namespace nsfr_b200 {
 
+// Development instrumentation (-DNSFR_PHASE_PROF): per-CTA clock64 deltas of
+// the K2 phases (staging, line, lift+project, WA+epilogue) summed over CTAs.
+#ifdef NSFR_PHASE_PROF
+__device__ unsigned long long g_phase_cycles[4];
+#define PHASE_START() long long t_prev_ = clock64()
+#define PHASE_MARK(i)                                                        \
+  do {                                                                       \
+    if (threadIdx.x == 0) {                                                  \
+      const long long t_ = clock64();                                        \
+      atomicAdd(&g_phase_cycles[i], static_cast<unsigned long long>(t_ - t_prev_)); \
+      t_prev_ = t_;                                                          \
+    }                                                                        \
+  } while (0)
+#else
+#define PHASE_START()
+#define PHASE_MARK(i)
+#endif
+
 struct ResParams {
   const double* ut_vol;   // [E][6][N^3] rho,u,v,w,p,rho/p of u~ (K1)
   const double* traces;   // [E][6][5][N^2]
@@ -192,15 +210,18 @@ __device__ __forceinline__ void res_batch(const ResParams& P, const ResOps<N>& O
   const int tid = threadIdx.x, nthr = blockDim.x;
   const int nb = min(EPB, P.E - e0);
   const double g = P.gamma, gm1 = g - 1.0;
+  PHASE_START();
   // stage element data (pure copies): node primitives of u~ (written by K1),
   // 0.5 C (stored pre-halved) and w J
   for (int it = tid; it < nb * 15 * N3; it += nthr) {
     const int b = it / (15 * N3), r = it - b * 15 * N3;
-    WORK[b * WS + r] = r < 6 * N3 ? P.ut_vol[(size_t)(e0 + b) * 6 * N3 + r]
-                                  : P.cof[(size_t)(e0 + b) * 9 * N3 + (r - 6 * N3)];
+    cp_async8(&WORK[b * WS + r], r < 6 * N3 ? P.ut_vol + (size_t)(e0 + b) * 6 * N3 + r
+                                            : P.cof + (size_t)(e0 + b) * 9 * N3 + (r - 6 * N3));
   }
-  for (int it = tid; it < nb * N3; it += nthr) WJ[it] = P.wj[(size_t)e0 * N3 + it];
+  for (int it = tid; it < nb * N3; it += nthr) cp_async8(&WJ[it], P.wj + (size_t)e0 * N3 + it);
+  cp_async_wait_all();
   __syncthreads();
+  PHASE_MARK(0);
 
   // ---- line phase: one thread owns one 1D line (dir, t1, t2) ----
   double fout0[NS], fout1[NS];  // face rows of the two faces this line pierces (registers)
@@ -228,8 +249,33 @@ __device__ __forceinline__ void res_batch(const ResParams& P, const ResOps<N>& O
       const double ca0 = Ch[(0 + dir) * N3 + ia], ca1 = Ch[(3 + dir) * N3 + ia],
                    ca2 = Ch[(6 + dir) * N3 + ia];
       double fa[NS] = {0.0, 0.0, 0.0, 0.0, 0.0};
+      int bb0 = a + 1;
+#ifdef NSFR_PAIR2
+      // two independent pair fluxes per iteration (ILP for the FP64 pipe)
 #pragma unroll 1
-      for (int bb = a + 1; bb < N; ++bb) {
+      for (; bb0 + 1 < N; bb0 += 2) {
+        const int ib = lbase + bb0 * stride, ic = ib + stride;
+        const PrimX pb{Pd[ib], Pd[N3 + ib], Pd[2 * N3 + ib], Pd[3 * N3 + ib],
+                       Pd[4 * N3 + ib], Pd[5 * N3 + ib], 0.0};
+        const PrimX pc{Pd[ic], Pd[N3 + ic], Pd[2 * N3 + ic], Pd[3 * N3 + ic],
+                       Pd[4 * N3 + ic], Pd[5 * N3 + ic], 0.0};
+        double f[NS], h[NS];
+        d_flux_contract_x(gm1, pa, pb, ca0 + Ch[(0 + dir) * N3 + ib], ca1 + Ch[(3 + dir) * N3 + ib],
+                          ca2 + Ch[(6 + dir) * N3 + ib], f);
+        d_flux_contract_x(gm1, pa, pc, ca0 + Ch[(0 + dir) * N3 + ic], ca1 + Ch[(3 + dir) * N3 + ic],
+                          ca2 + Ch[(6 + dir) * N3 + ic], h);
+        const double c = wt * O.q[a * N + bb0], d = wt * O.q[a * N + bb0 + 1];
+#pragma unroll
+        for (int s = 0; s < NS; ++s) {
+          fa[s] = fma(c, f[s], fa[s]);
+          acc[s * N3 + ib] = fma(-c, f[s], acc[s * N3 + ib]);
+          fa[s] = fma(d, h[s], fa[s]);
+          acc[s * N3 + ic] = fma(-d, h[s], acc[s * N3 + ic]);
+        }
+      }
+#endif
+#pragma unroll 1
+      for (int bb = bb0; bb < N; ++bb) {
         const int ib = lbase + bb * stride;
         const PrimX pb{Pd[ib], Pd[N3 + ib], Pd[2 * N3 + ib], Pd[3 * N3 + ib],
                        Pd[4 * N3 + ib], Pd[5 * N3 + ib], 0.0};
@@ -328,6 +374,7 @@ __device__ __forceinline__ void res_batch(const ResParams& P, const ResOps<N>& O
     }
   }
   __syncthreads();
+  PHASE_MARK(1);
 
   // ---- tail ----
   const int nbs = nb * 5;
@@ -411,6 +458,7 @@ __device__ __forceinline__ void res_batch(const ResParams& P, const ResOps<N>& O
                                  nthr);
     __syncthreads();
   }
+  PHASE_MARK(2);
   // second half of S10: Pi~ along xi, eta
   tail_pass<N, 0, false, false>(O.fr, O.bs, nullptr, 0, ACCV, AS, WORK, WS, WJ, nbs, tid, nthr);
   __syncthreads();
@@ -459,6 +507,7 @@ __device__ __forceinline__ void res_batch(const ResParams& P, const ResOps<N>& O
       }
     }
   }
+  PHASE_MARK(3);
 }
 
 // One batch per CTA (CTAs retire at staggered times, so their staging, line

@@ -867,3 +867,15 @@ extern "C" int nsfr_gpu_measure_fp64_peak(int device, double* tflops) {
   *tflops = 2.0 * 8 * 16 * (double)iters * threads * blocks / (best * 1e-3) / 1e12;
   return NSFR_OK;
 }
+
+#ifdef NSFR_PHASE_PROF
+// Development only: read and reset the K2 phase cycle counters.
+extern "C" int nsfr_gpu_phase_counters(double* out4) {
+  unsigned long long h[4];
+  if (cudaMemcpyFromSymbol(h, g_phase_cycles, sizeof h) != cudaSuccess) return NSFR_E_CUDA;
+  for (int i = 0; i < 4; ++i) out4[i] = static_cast<double>(h[i]);
+  const unsigned long long z[4] = {0, 0, 0, 0};
+  cudaMemcpyToSymbol(g_phase_cycles, z, sizeof z);
+  return NSFR_OK;
+}
+#endif
