@@ -213,12 +213,20 @@ __device__ __forceinline__ void res_batch(const ResParams& P, const ResOps<N>& O
   PHASE_START();
   // stage element data (pure copies): node primitives of u~ (written by K1),
   // 0.5 C (stored pre-halved) and w J
-  for (int it = tid; it < nb * 15 * N3; it += nthr) {
-    const int b = it / (15 * N3), r = it - b * 15 * N3;
-    cp_async8(&WORK[b * WS + r], r < 6 * N3 ? P.ut_vol + (size_t)(e0 + b) * 6 * N3 + r
-                                            : P.cof + (size_t)(e0 + b) * 9 * N3 + (r - 6 * N3));
+#pragma unroll
+  for (int b = 0; b < EPB; ++b) {
+    if (b < nb) {
+      const double* pu = P.ut_vol + (size_t)(e0 + b) * 6 * N3;
+      const double* pc = P.cof + (size_t)(e0 + b) * 9 * N3;
+      double* w = WORK + b * WS;
+      for (int i = tid; i < 6 * N3; i += nthr) cp_async8(w + i, pu + i);
+      for (int i = tid; i < 9 * N3; i += nthr) cp_async8(w + 6 * N3 + i, pc + i);
+    }
   }
-  for (int it = tid; it < nb * N3; it += nthr) cp_async8(&WJ[it], P.wj + (size_t)e0 * N3 + it);
+  {
+    const double* pw = P.wj + (size_t)e0 * N3;
+    for (int i = tid; i < nb * N3; i += nthr) cp_async8(WJ + i, pw + i);
+  }
   cp_async_wait_all();
   __syncthreads();
   PHASE_MARK(0);
