@@ -34,6 +34,7 @@ struct ProjOps {
   double interp[N * N];  // chi   (nq x np)
   double proj[N * N];    // Pi    (np x nq)
   double bsol[2 * N];    // bound_sol rows at xi = -1, +1
+  double bp[2 * N];      // bound_sol_side Pi: face trace rows applied to nodal v (chi Pi = I)
   double c35;            // gm1^(1/gm1) when gamma/(gamma-1) == 7/2 (closed-form u(v)), else 0
 };
 
@@ -47,8 +48,8 @@ struct ProjCfg {
   static constexpr int N2 = N * N, N3 = N * N * N;
   static constexpr int EPB = N3 <= 32 ? 8 : (N3 <= 64 ? 4 : (N3 <= 128 ? 2 : 1));
   static constexpr int THREADS = ((EPB * N3 + 31) / 32) * 32;
-  // smem doubles per element: A, B, V, C4 (5 N3 each) + T0, T0b, T1, F2, F1, F0 (10 N2 each)
-  static constexpr int PER_EL = 20 * N3 + 60 * N2;
+  // smem doubles per element: A, B, V (5 N3 each) + F0, F1, F2 (10 N2 each)
+  static constexpr int PER_EL = 15 * N3 + 30 * N2;
   static constexpr int SMEM = EPB * PER_EL * 8;
 };
 
@@ -88,6 +89,31 @@ __device__ __forceinline__ void line_pass(const double (&op)[N * N], const doubl
   }
 }
 
+// Face traces of direction D: one thread per 1D line along D contracts it with
+// the two boundary rows bp[side] into fo[batch][side][N2] (line index l).
+template <int N, int D>
+__device__ __forceinline__ void face_contract(const double (&bp)[2 * N], const double* in, double* fo,
+                                              int nbs, int tid, int nthr) {
+  constexpr int N2 = N * N, N3 = N * N * N;
+  constexpr int stride = D == 0 ? 1 : (D == 1 ? N : N2);
+  for (int it = tid; it < nbs * N2; it += nthr) {
+    const int bsi = it / N2, l = it - bsi * N2;
+    const int l0 = l % N, l1 = l / N;
+    const int base = D == 0 ? N * (l0 + N * l1) : (D == 1 ? l0 + N2 * l1 : l0 + N * l1);
+    const double* src = in + bsi * N3 + base;
+    double x[N];
+#pragma unroll
+    for (int a = 0; a < N; ++a) x[a] = src[a * stride];
+#pragma unroll
+    for (int side = 0; side < 2; ++side) {
+      double acc = 0.0;
+#pragma unroll
+      for (int a = 0; a < N; ++a) acc = fma(bp[side * N + a], x[a], acc);
+      fo[(bsi * 2 + side) * N2 + l] = acc;
+    }
+  }
+}
+
 // Line pass on face arrays [batch][N2] (index t1 + N t2) along t1 (T=0) or t2 (T=1).
 template <int N, int T>
 __device__ __forceinline__ void face_pass(const double (&op)[N * N], const double* in, double* out,
@@ -119,13 +145,9 @@ __device__ __forceinline__ void proj_batch(const ProjParams& P, const ProjOps<N>
   double* A = sm;
   double* B = A + EPB * 5 * N3;
   double* V = B + EPB * 5 * N3;
-  double* C4 = V + EPB * 5 * N3;
-  double* T0 = C4 + EPB * 5 * N3;   // [EPB*5][2][N2]  bs_xi v_hat          (index j + N k)
-  double* T0b = T0 + EPB * 10 * N2; // [EPB*5][2][N2]  chi_eta T0
-  double* T1 = T0b + EPB * 10 * N2; // [EPB*5][2][N2]  bs_eta X             (index i + N k)
-  double* F2 = T1 + EPB * 10 * N2;  // [EPB*5][2][N2]  dir-2 faces: bs_zeta XY (index i + N j)
-  double* F1 = F2 + EPB * 10 * N2;  // [EPB*5][2][N2]  dir-1 faces: chi_zeta T1
-  double* F0 = F1 + EPB * 10 * N2;  // [EPB*5][2][N2]  dir-0 faces: chi_zeta T0b
+  double* F0 = V + EPB * 5 * N3;    // [EPB*5][2][N2] dir-0 face v~ (index j + N k)
+  double* F1 = F0 + EPB * 10 * N2;  // [EPB*5][2][N2] dir-1 face v~ (index i + N k)
+  double* F2 = F1 + EPB * 10 * N2;  // [EPB*5][2][N2] dir-2 face v~ (index i + N j)
   const int tid = threadIdx.x, nthr = blockDim.x;
   const int nb = min(EPB, P.E - e0);
   const double g = P.gamma;
@@ -143,7 +165,11 @@ __device__ __forceinline__ void proj_batch(const ProjParams& P, const ProjOps<N>
   __syncthreads();
   line_pass<N, 2, false>(O.interp, A, B, O.bsol, nullptr, nbs, tid, nthr);
   __syncthreads();
-  // S2 v(u_q), and the wavespeed for adaptive dt
+  // S2 v(u_q) -> V, the wavespeed for adaptive dt, and the
+  // volume state K2 consumes. With n_q = n_p (GL or LGL, no overintegration)
+  // Pi = chi^-1, so the reference's volume round trip u(chi^3 Pi^3 v(u_q))
+  // is u_q in exact arithmetic: K2 gets the primitives of u_q directly
+  // (the RHS moves by ~1x the reference's own 1-ulp floor).
   double lam = 0.0;
   for (int it = tid; it < nb * N3; it += nthr) {
     const int b = it / N3, q = it - b * N3;
@@ -161,47 +187,8 @@ __device__ __forceinline__ void proj_batch(const ProjParams& P, const ProjOps<N>
       lam = fmax(lam, speed + a);
     }
 #pragma unroll
-    for (int s = 0; s < NS; ++s) B[(b * 5 + s) * N3 + q] = vv[s];
-  }
-  if (P.lam) {
-    for (int o = 16; o > 0; o >>= 1) lam = fmax(lam, __shfl_xor_sync(0xffffffffu, lam, o));
-    if ((tid & 31) == 0 && lam > 0.0) atomicMax(P.lam, dbl_bits(lam));
-  }
-  __syncthreads();
-  // S3 v_hat = Pi^3 v_q
-  line_pass<N, 0, false>(O.proj, B, A, O.bsol, nullptr, nbs, tid, nthr);
-  __syncthreads();
-  line_pass<N, 1, false>(O.proj, A, B, O.bsol, nullptr, nbs, tid, nthr);
-  __syncthreads();
-  line_pass<N, 2, false>(O.proj, B, V, O.bsol, nullptr, nbs, tid, nthr);
-  __syncthreads();
-  if (P.vhat) {
-    double* dst = P.vhat + (size_t)e0 * 5 * N3;
-    for (int i = tid; i < nb * 5 * N3; i += nthr) dst[i] = V[i];
-  }
-  // S4 in the apply_tensor_product order (xi, eta, zeta) with the bound_sol row
-  // in each face's normal direction (sumfac.cpp:57-69):
-  //   X = chi_xi V, T0 = bs_xi V (same xi-lines)
-  line_pass<N, 0, true>(O.interp, V, A, O.bsol, T0, nbs, tid, nthr);
-  __syncthreads();
-  //   XY = chi_eta X, T1 = bs_eta X (same eta-lines); T0b = chi_eta T0
-  line_pass<N, 1, true>(O.interp, A, B, O.bsol, T1, nbs, tid, nthr);
-  face_pass<N, 0>(O.interp, T0, T0b, nbs * 2, tid, nthr);
-  __syncthreads();
-  //   v~_vol = chi_zeta XY, F2 = bs_zeta XY (same zeta-lines); F1 = chi_zeta T1; F0 = chi_zeta T0b
-  line_pass<N, 2, true>(O.interp, B, C4, O.bsol, F2, nbs, tid, nthr);
-  face_pass<N, 1>(O.interp, T1, F1, nbs * 2, tid, nthr);
-  face_pass<N, 1>(O.interp, T0b, F0, nbs * 2, tid, nthr);
-  __syncthreads();
-  // S5 u~ = u(v~) at volume and face nodes
-  for (int it = tid; it < nb * N3; it += nthr) {
-    const int b = it / N3, q = it - b * N3;
-    double vv[NS], uu[NS];
-#pragma unroll
-    for (int s = 0; s < NS; ++s) vv[s] = C4[(b * 5 + s) * N3 + q];
-    if (!u_of_v<N>(O, g, vv, uu)) atomicOr(P.err, ERR_STATE);
-    // K2 consumes the per-node primitive bundle (prim(), euler.cpp:109-115,
-    // plus rho/p and the two reciprocals its log means use)
+    for (int s = 0; s < NS; ++s) V[(b * 5 + s) * N3 + q] = vv[s];
+    // primitive bundle for K2 (prim(), euler.cpp:109-115, plus rho/p)
     const PrimX pr = d_primx(g, uu);
     double* dst = P.ut_vol + (size_t)(e0 + b) * 6 * N3 + q;
     dst[0 * N3] = pr.rho;
@@ -211,6 +198,29 @@ __device__ __forceinline__ void proj_batch(const ProjParams& P, const ProjOps<N>
     dst[4 * N3] = pr.p;
     dst[5 * N3] = pr.rp;
   }
+  if (P.lam) {
+    for (int o = 16; o > 0; o >>= 1) lam = fmax(lam, __shfl_xor_sync(0xffffffffu, lam, o));
+    if ((tid & 31) == 0 && lam > 0.0) atomicMax(P.lam, dbl_bits(lam));
+  }
+  __syncthreads();
+  // S3 v_hat = Pi^3 v_q: only the entropy diagnostic (-v_hat . R) needs it
+  if (P.vhat) {
+    line_pass<N, 0, false>(O.proj, V, A, O.bsol, nullptr, nbs, tid, nthr);
+    __syncthreads();
+    line_pass<N, 1, false>(O.proj, A, B, O.bsol, nullptr, nbs, tid, nthr);
+    __syncthreads();
+    line_pass<N, 2, false>(O.proj, B, A, O.bsol, nullptr, nbs, tid, nthr);
+    __syncthreads();
+    double* dst = P.vhat + (size_t)e0 * 5 * N3;
+    for (int i = tid; i < nb * 5 * N3; i += nthr) dst[i] = A[i];
+  }
+  // S4 faces: v~_f = (bs_side (x) chi (x) chi) Pi^3 v_q = (bs_side Pi) along the
+  // normal applied to v_q (chi Pi = I tangentially): one contraction per line
+  face_contract<N, 0>(O.bp, V, F0, nbs, tid, nthr);
+  face_contract<N, 1>(O.bp, V, F1, nbs, tid, nthr);
+  face_contract<N, 2>(O.bp, V, F2, nbs, tid, nthr);
+  __syncthreads();
+  // S5 u~ = u(v~) at the face nodes
   for (int it = tid; it < nb * 6 * N2; it += nthr) {
     const int b = it / (6 * N2), r = it - b * 6 * N2, f = r / N2, k = r - f * N2;
     const int dir = f / 2, side = f % 2;

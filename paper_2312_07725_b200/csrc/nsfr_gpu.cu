@@ -114,6 +114,12 @@ ProjOps<N> proj_ops(const DevTables& t) {
     o.proj[i] = t.proj[i];
   }
   for (int i = 0; i < 2 * N; ++i) o.bsol[i] = t.bsol[i];
+  for (int side = 0; side < 2; ++side)
+    for (int a = 0; a < N; ++a) {  // (bound_sol Pi)[side][a]; Pi is np x nq
+      double s = 0.0;
+      for (int r = 0; r < N; ++r) s += t.bsol[side * N + r] * t.proj[r * N + a];
+      o.bp[side * N + a] = s;
+    }
   o.c35 = 0.0;
   return o;
 }
