@@ -129,7 +129,7 @@ __device__ __forceinline__ void tail_pass(const double (&op)[N * N], const doubl
         acc = fma(bvec[r], f0, acc);
         acc = fma(bvec[N + r], f1, acc);
       }
-      if (DIV) acc = acc / wj[b * N3 + base + r * stride];
+      if (DIV) acc = acc * wj[b * N3 + base + r * stride];  // wj holds 1/(w J)
       dst[r * stride] = acc;
     }
   }

@@ -528,7 +528,7 @@ int nsfr_gpu_create(const nsfr_gpu_setup* setup, nsfr_gpu_ctx** out) {
           ctx->msg = "nsfr_gpu_create: nonpositive J in caller metrics";
           return fail(NSFR_E_MESH);
         }
-        wj[static_cast<size_t>(e) * N3 + q] = w * J;
+        wj[static_cast<size_t>(e) * N3 + q] = 1.0 / (w * J);  // K2 multiplies by 1/(w J)
       }
     if (cudaMemcpy(ctx->d_cof, cof.data(), sizeof(double) * cof.size(), cudaMemcpyHostToDevice) ||
         cudaMemcpy(ctx->d_jac, setup->jac_vol, sizeof(double) * n3, cudaMemcpyHostToDevice) ||

@@ -7,7 +7,7 @@
 // Layout in HBM (element-contiguous blocks, xi fastest):
 //   state/us/acc [E][5][N^3]; ut_vol [E][8][N^3] node primitives; traces [E][6][5][N^2];
 //   cof [E][9][N^3] = 0.5 C
-//   (component 3*n_phys + i_ref major); wj [E][N^3] = w_i w_j w_k J.
+//   (component 3*n_phys + i_ref major); wj [E][N^3] = 1/(w_i w_j w_k J).
 #pragma once
 #include <cuda_runtime.h>
 
@@ -176,7 +176,7 @@ __global__ void k_metrics(MetricParams P) {
     double w = T.wq[i];
     w *= T.wq[j];
     w *= T.wq[k];
-    P.wj[(size_t)e * N3 + q] = w * J;
+    P.wj[(size_t)e * N3 + q] = 1.0 / (w * J);  // the WA inverse multiplies by 1/(w J)
   }
   // conservative curl (geometry.cpp:174-199)
   for (int n = 0; n < 3; ++n) {
