@@ -188,15 +188,15 @@ __device__ __forceinline__ void proj_batch(const ProjParams& P, const ProjOps<N>
     }
 #pragma unroll
     for (int s = 0; s < NS; ++s) V[(b * 5 + s) * N3 + q] = vv[s];
-    // primitive bundle for K2 (prim(), euler.cpp:109-115, plus rho/p)
-    const PrimX pr = d_primx(g, uu);
+    // half-scaled primitive bundle for K2's pair fluxes (prim(), euler.cpp:109-115)
+    const PrimH ph = to_half(g - 1.0, d_primx(g, uu));
     double* dst = P.ut_vol + (size_t)(e0 + b) * 6 * N3 + q;
-    dst[0 * N3] = pr.rho;
-    dst[1 * N3] = pr.u;
-    dst[2 * N3] = pr.v;
-    dst[3 * N3] = pr.w;
-    dst[4 * N3] = pr.p;
-    dst[5 * N3] = pr.rp;
+    dst[0 * N3] = ph.hr;
+    dst[1 * N3] = ph.hu;
+    dst[2 * N3] = ph.hv;
+    dst[3 * N3] = ph.hw;
+    dst[4 * N3] = ph.hp;
+    dst[5 * N3] = ph.grp;
   }
   if (P.lam) {
     for (int o = 16; o > 0; o >>= 1) lam = fmax(lam, __shfl_xor_sync(0xffffffffu, lam, o));

@@ -252,8 +252,8 @@ __device__ __forceinline__ void res_batch(const ResParams& P, const ResOps<N>& O
 #pragma unroll 1
     for (int a = 0; a < N - 1; ++a) {
       const int ia = lbase + a * stride;
-      const PrimX pa{Pd[ia], Pd[N3 + ia], Pd[2 * N3 + ia], Pd[3 * N3 + ia],
-                     Pd[4 * N3 + ia], Pd[5 * N3 + ia], 0.0};
+      const PrimH pa{Pd[ia], Pd[N3 + ia], Pd[2 * N3 + ia], Pd[3 * N3 + ia],
+                     Pd[4 * N3 + ia], Pd[5 * N3 + ia]};
       const double ca0 = Ch[(0 + dir) * N3 + ia], ca1 = Ch[(3 + dir) * N3 + ia],
                    ca2 = Ch[(6 + dir) * N3 + ia];
       double fa[NS] = {0.0, 0.0, 0.0, 0.0, 0.0};
@@ -263,14 +263,14 @@ __device__ __forceinline__ void res_batch(const ResParams& P, const ResOps<N>& O
 #pragma unroll 1
       for (; bb0 + 1 < N; bb0 += 2) {
         const int ib = lbase + bb0 * stride, ic = ib + stride;
-        const PrimX pb{Pd[ib], Pd[N3 + ib], Pd[2 * N3 + ib], Pd[3 * N3 + ib],
-                       Pd[4 * N3 + ib], Pd[5 * N3 + ib], 0.0};
-        const PrimX pc{Pd[ic], Pd[N3 + ic], Pd[2 * N3 + ic], Pd[3 * N3 + ic],
-                       Pd[4 * N3 + ic], Pd[5 * N3 + ic], 0.0};
+        const PrimH pb{Pd[ib], Pd[N3 + ib], Pd[2 * N3 + ib], Pd[3 * N3 + ib],
+                       Pd[4 * N3 + ib], Pd[5 * N3 + ib]};
+        const PrimH pc{Pd[ic], Pd[N3 + ic], Pd[2 * N3 + ic], Pd[3 * N3 + ic],
+                       Pd[4 * N3 + ic], Pd[5 * N3 + ic]};
         double f[NS], h[NS];
-        d_flux_contract_x(gm1, pa, pb, ca0 + Ch[(0 + dir) * N3 + ib], ca1 + Ch[(3 + dir) * N3 + ib],
+        d_flux_h(pa, pb,ca0 + Ch[(0 + dir) * N3 + ib], ca1 + Ch[(3 + dir) * N3 + ib],
                           ca2 + Ch[(6 + dir) * N3 + ib], f);
-        d_flux_contract_x(gm1, pa, pc, ca0 + Ch[(0 + dir) * N3 + ic], ca1 + Ch[(3 + dir) * N3 + ic],
+        d_flux_h(pa, pc,ca0 + Ch[(0 + dir) * N3 + ic], ca1 + Ch[(3 + dir) * N3 + ic],
                           ca2 + Ch[(6 + dir) * N3 + ic], h);
         const double c = wt * O.q[a * N + bb0], d = wt * O.q[a * N + bb0 + 1];
 #pragma unroll
@@ -285,10 +285,10 @@ __device__ __forceinline__ void res_batch(const ResParams& P, const ResOps<N>& O
 #pragma unroll 1
       for (int bb = bb0; bb < N; ++bb) {
         const int ib = lbase + bb * stride;
-        const PrimX pb{Pd[ib], Pd[N3 + ib], Pd[2 * N3 + ib], Pd[3 * N3 + ib],
-                       Pd[4 * N3 + ib], Pd[5 * N3 + ib], 0.0};
+        const PrimH pb{Pd[ib], Pd[N3 + ib], Pd[2 * N3 + ib], Pd[3 * N3 + ib],
+                       Pd[4 * N3 + ib], Pd[5 * N3 + ib]};
         double f[NS];
-        d_flux_contract_x(gm1, pa, pb, ca0 + Ch[(0 + dir) * N3 + ib], ca1 + Ch[(3 + dir) * N3 + ib],
+        d_flux_h(pa, pb,ca0 + Ch[(0 + dir) * N3 + ib], ca1 + Ch[(3 + dir) * N3 + ib],
                           ca2 + Ch[(6 + dir) * N3 + ib], f);
         const double c = wt * O.q[a * N + bb];
 #pragma unroll
@@ -330,6 +330,7 @@ __device__ __forceinline__ void res_batch(const ResParams& P, const ResOps<N>& O
         for (int s = 0; s < NS; ++s) un[s] = nt[s * N2];
       }
       const PrimX pf = d_primx(g, uf);
+      const PrimH pfh = to_half(gm1, pf);
       // own face cofactor column C_f[:,dir] = sum_a bound_flux(side,a) C_a (geometry.cpp:218-226)
       double cf0 = 0.0, cf1 = 0.0, cf2 = 0.0;
 #pragma unroll
@@ -345,10 +346,10 @@ __device__ __forceinline__ void res_batch(const ResParams& P, const ResOps<N>& O
 #pragma unroll 1
       for (int a = 0; a < N; ++a) {
         const int ia = lbase + a * stride;
-        const PrimX pa{Pd[ia], Pd[N3 + ia], Pd[2 * N3 + ia], Pd[3 * N3 + ia],
-                       Pd[4 * N3 + ia], Pd[5 * N3 + ia], 0.0};
+        const PrimH pa{Pd[ia], Pd[N3 + ia], Pd[2 * N3 + ia], Pd[3 * N3 + ia],
+                       Pd[4 * N3 + ia], Pd[5 * N3 + ia]};
         double fl[NS];
-        d_flux_contract_x(gm1, pa, pf, Ch[(0 + dir) * N3 + ia] + ch0, Ch[(3 + dir) * N3 + ia] + ch1,
+        d_flux_h(pa, pfh,Ch[(0 + dir) * N3 + ia] + ch0, Ch[(3 + dir) * N3 + ia] + ch1,
                           Ch[(6 + dir) * N3 + ia] + ch2, fl);
         const double c = sign * O.bflux[side * N + a] * wt;
 #pragma unroll
@@ -364,7 +365,7 @@ __device__ __forceinline__ void res_batch(const ResParams& P, const ResOps<N>& O
       const double nrm[3] = {v0 * ijg, v1 * ijg, v2 * ijg};
       const PrimX pn = d_primx(g, un);
       double fn[NS];
-      d_flux_contract_x(gm1, pf, pn, nrm[0], nrm[1], nrm[2], fn);
+      d_flux_h(pfh, to_half(gm1, pn), nrm[0], nrm[1], nrm[2], fn);
       if (P.roe) {
         double d[NS];
         if (!d_roe_x(g, uf, un, pf, pn, nrm, d)) atomicOr(P.err, ERR_ROE);
