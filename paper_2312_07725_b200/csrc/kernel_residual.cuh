@@ -384,6 +384,12 @@ __device__ __forceinline__ void res_batch(const ResParams& P, const ResOps<N>& O
   }
   __syncthreads();
   PHASE_MARK(1);
+#ifdef NSFR_SKIP_TAIL  // timing diagnostic only: stage states stay u_n (results are wrong)
+  if (tid == 0) P.out[e0] = ACCV[0] + fout0[0] + fout1[0];
+  if (P.stage >= 1 && P.stage <= 3)
+    for (int i = tid; i < nb * 5 * N3; i += nthr) P.us[(size_t)e0 * 5 * N3 + i] = P.un[(size_t)e0 * 5 * N3 + i];
+  return;
+#endif
 
   // ---- tail ----
   const int nbs = nb * 5;

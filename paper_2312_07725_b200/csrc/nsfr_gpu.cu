@@ -728,12 +728,18 @@ int nsfr_gpu_advance(nsfr_gpu_ctx* ctx, int nsteps, double cfl, double t_final, 
     ctx->launches = l0;  // counted on replay
   }
   const long long per_step = 4 * 2 + 3;
+  // with a final time, poll t every 16 steps (steps past t_final have dt = 0)
+  const int chunk = t_final > 0.0 ? 16 : nsteps;
   for (int i = 0; i < nsteps; ++i) {
     if (ctx->timing) {
       if (int rc = enqueue_step(ctx, false)) return rc;
     } else {
       CK(cudaGraphLaunch(ctx->graph, ctx->st));
       ctx->launches += per_step;
+    }
+    if (chunk < nsteps && (i + 1) % chunk == 0) {
+      if (int rc = sync_check(ctx)) return rc;
+      if (ctx->h_step->t >= t_final) break;
     }
   }
   if (int rc = sync_check(ctx)) return rc;

@@ -153,6 +153,20 @@ def test_config1_twenty_steps(meta):
     np.testing.assert_allclose(g.l2_error(), meta["config1_l2_t20"], rtol=1e-10)
 
 
+@pytest.mark.parametrize("name,c1d", [("c_dg", 0.0), ("c_plus", OC_PLUS[3])])
+def test_config2_to_final_time(name, c1d):
+    """BASELINE configs[1]: 16^3 vortex, p=3, EC+Roe, RK4 at CFL 0.1 to t_f = 2
+    (~305 steps); final L2(rho), L2(p) within 1e-10 relative of the reference
+    build (tests/golden/config2.json, tests/golden/make_golden_config2.py)."""
+    with open(os.path.join(GOLD, "config2.json")) as f:
+        gold = json.load(f)[name]
+    g = P().GpuSolver(gpu_cfg(p=3, m=16, c1d=c1d))
+    g.init_case()
+    t = g.advance(2000, cfl=0.1, t_final=2.0)  # the driver stops within 16 steps of t_f
+    assert t == pytest.approx(gold["t_final"], abs=1e-12)
+    np.testing.assert_allclose(g.l2_error(), gold["l2"], rtol=1e-10)
+
+
 def test_advance_graph_equals_stepwise():
     cfg = gpu_cfg(p=3, m=4)
     a = P().GpuSolver(cfg)
