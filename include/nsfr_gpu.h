@@ -143,8 +143,9 @@ int nsfr_gpu_l2_error(nsfr_gpu_ctx* ctx, int case_kind, double out2[2]);
 int nsfr_gpu_entropy_change(nsfr_gpu_ctx* ctx, double* out);
 
 /* Bench helper: time nsteps RK4 steps (t_final unbounded) with CUDA events on
- * the context stream; inputs stay resident in HBM. kernel_ms (optional, [2])
- * receives the summed durations of the K1 (projection) and K2 (residual)
+ * the context stream; inputs stay resident in HBM. kernel_ms (optional, [3])
+ * receives the summed durations of the K1 (projection prologue), K2 (pair
+ * and face fluxes) and K3 (lift, mass inverse, RK update, next projection)
  * launches, each bracketed by its own events (disables the step graph). */
 int nsfr_gpu_time_steps(nsfr_gpu_ctx* ctx, int nsteps, double cfl, double* step_ms, double* kernel_ms);
 

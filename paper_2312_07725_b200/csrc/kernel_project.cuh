@@ -138,25 +138,19 @@ __device__ __forceinline__ void face_pass(const double (&op)[N * N], const doubl
   }
 }
 
+// S1-S5 for the nb elements whose state u_hat sits in shared memory A
+// ([EPB*5][N3], synchronised by the caller). B, V: [EPB*5][N3] scratch;
+// F: [3][EPB*5][2][N2] face scratch. Shared by K1 and the fused K3 (kernel_update.cuh).
 template <int N>
-__device__ __forceinline__ void proj_batch(const ProjParams& P, const ProjOps<N>& O, int e0, double* sm) {
+__device__ __forceinline__ void proj_core(const ProjParams& P, const ProjOps<N>& O, int e0, int nb,
+                                          double* A, double* B, double* V, double* F) {
   using Cfg = ProjCfg<N>;
   constexpr int N2 = Cfg::N2, N3 = Cfg::N3, EPB = Cfg::EPB;
-  double* A = sm;
-  double* B = A + EPB * 5 * N3;
-  double* V = B + EPB * 5 * N3;
-  double* F0 = V + EPB * 5 * N3;    // [EPB*5][2][N2] dir-0 face v~ (index j + N k)
+  double* F0 = F;                   // [EPB*5][2][N2] dir-0 face v~ (index j + N k)
   double* F1 = F0 + EPB * 10 * N2;  // [EPB*5][2][N2] dir-1 face v~ (index i + N k)
   double* F2 = F1 + EPB * 10 * N2;  // [EPB*5][2][N2] dir-2 face v~ (index i + N j)
   const int tid = threadIdx.x, nthr = blockDim.x;
-  const int nb = min(EPB, P.E - e0);
   const double g = P.gamma;
-  {
-    const double* src = P.u + (size_t)e0 * 5 * N3;
-    for (int i = tid; i < nb * 5 * N3; i += nthr) cp_async8(&A[i], src + i);
-    cp_async_wait_all();
-  }
-  __syncthreads();
   const int nbs = nb * 5;
   // S1 u_q = chi^3 u_hat (xi, eta, zeta passes: apply_tensor_product order)
   line_pass<N, 0, false>(O.interp, A, B, O.bsol, nullptr, nbs, tid, nthr);
@@ -244,6 +238,24 @@ __device__ __forceinline__ void proj_batch(const ProjParams& P, const ProjOps<N>
       for (int s = 0; s < NS; ++s) P.send_hi[((size_t)plane * 5 + s) * N2 + k] = uu[s];
     }
   }
+}
+
+template <int N>
+__device__ __forceinline__ void proj_batch(const ProjParams& P, const ProjOps<N>& O, int e0, double* sm) {
+  using Cfg = ProjCfg<N>;
+  constexpr int N3 = Cfg::N3, EPB = Cfg::EPB;
+  double* A = sm;
+  double* B = A + EPB * 5 * N3;
+  double* V = B + EPB * 5 * N3;
+  const int tid = threadIdx.x, nthr = blockDim.x;
+  const int nb = min(EPB, P.E - e0);
+  {
+    const double* src = P.u + (size_t)e0 * 5 * N3;
+    for (int i = tid; i < nb * 5 * N3; i += nthr) cp_async8(&A[i], src + i);
+    cp_async_wait_all();
+  }
+  __syncthreads();
+  proj_core<N>(P, O, e0, nb, A, B, V, V + EPB * 5 * N3);
 }
 
 // One batch per CTA; L2 prefetch of the input block of the CTA `ahead`

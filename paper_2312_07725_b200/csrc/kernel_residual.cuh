@@ -1,32 +1,24 @@
-// K2: residual S6-S10 for one RK stage, fused:
+// K2: residual rows S6-S8 for one RK stage:
 //   S6  volume Hadamard flux differencing   (sumfac.hpp:48-94, 0.5*skew -> skew(a,b), D2)
 //   S7  hybrid surface-volume Hadamard      (sumfac.hpp:110-157, own face cofactor, D1)
 //   S8  EC + Roe face flux vs the neighbour's trace (euler.cpp:142-162, 229-301; D3)
-//   S9  chi^T lifting of volume and face rows
-//   S10 weight-adjusted inverse -Pi~ (W J)^-1 Pi~^T R (fr_operators.cpp:280-309, D6)
-//   + the classical RK4 stage update (D4).
+// Output: the volume rows vol = sum over directions [E][5][N^3] and the face
+// rows facc [E][3 dir][5][2 side][N^2]; S9 lifting, S10 and the RK update run
+// in K3 (kernel_update.cuh), fused with the next stage's entropy projection.
 //
-// Thread mapping. Line phase: one thread per 1D line (dir, t1, t2) of an
-// element does every two-point evaluation touching that line: the n(n-1)/2
-// volume pairs, the 2n hybrid pairs with the two faces it pierces and the two
-// face fluxes. Each node belongs to exactly one line per direction, so the
-// per-direction accumulators need no atomics (deterministic).
-//
-// Tail. S9 and the first half of S10 are both tensor products, so
-//   Pi~^T^3 R = M^3 vol + sum_f (b_f (x) M (x) M) facc_f,  M = Pi~^T chi^T, b_f = Pi~^T bs_f
-// runs as three LINE passes with the face lifts injected into the pass of
-// their normal direction, the 1/(w J) scaling fused into the last one, then
-// three Pi~ passes with the RK update fused into the last. (The entropy
-// diagnostic needs R itself: that path lifts with chi^T first.)
+// Thread mapping. One thread per 1D line (dir, t1, t2) of an element does
+// every two-point evaluation touching that line: the n(n-1)/2 volume pairs,
+// the 2n hybrid pairs with the two faces it pierces and the two face fluxes.
+// Each node belongs to exactly one line per direction, so the per-direction
+// accumulators need no atomics (deterministic).
 // All 1D operators travel in the kernel parameter (constant) bank.
 #pragma once
-#include "kernel_project.cuh"
 #include "physics.cuh"
 
 namespace nsfr_b200 {
 
 // Development instrumentation (-DNSFR_PHASE_PROF): per-CTA clock64 deltas of
-// the K2 phases (staging, line, lift+project, WA+epilogue) summed over CTAs.
+// the K2 phases (staging, line, output) summed over CTAs.
 #ifdef NSFR_PHASE_PROF
 __device__ unsigned long long g_phase_cycles[4];
 #define PHASE_START() long long t_prev_ = clock64()
@@ -44,33 +36,21 @@ __device__ unsigned long long g_phase_cycles[4];
 #endif
 
 struct ResParams {
-  const double* ut_vol;   // [E][6][N^3] rho,u,v,w,p,rho/p of u~ (K1)
+  const double* ut_vol;   // [E][6][N^3] half-scaled primitives of u~ (K1 / K3)
   const double* traces;   // [E][6][5][N^2]
   const double* halo_lo;  // [m*m][5][N^2] face 5 of plane k0-1 (nullptr: wrap locally)
   const double* halo_hi;  // [m*m][5][N^2] face 4 of plane k1
   const double* cof;      // [E][9][N^3] = 0.5 C
-  const double* wj;       // [E][N^3]
-  const double* vhat;     // [E][5][N^3] or nullptr
-  double* dS;             // [E] or nullptr
-  double* un;             // RK base state (stage 4 writes it)
-  double* us;             // next stage state
-  double* acc;            // RK accumulator
-  double* out;            // stage 0: dU/dt
-  const double* dt;       // device scalar
+  double* vol;            // [E][5][N^3] volume rows
+  double* facc;           // [E][3][5][2][N^2] face rows
   unsigned* err;
-  int stage, E, m, nz;
+  int E, m, nz;
   double gamma;
   int roe;
 };
 
 template <int N>
 struct ResOps {
-  double M[N * N];       // Pi~^T chi^T          (lift + project, hot path)
-  double bm[2 * N];      // Pi~^T bound_sol_side
-  double fr[N * N];      // Pi~                  (np x nq)
-  double frt[N * N];     // Pi~^T                (entropy-diagnostic path)
-  double it[N * N];      // chi^T                (entropy-diagnostic path)
-  double bs[2 * N];      // bound_sol            (entropy-diagnostic path)
   double q[N * N];       // skew(a,b) = q(a,b) - q(b,a), q = 0.5 skew
   double bflux[2 * N];   // flux basis at -1, +1
   double wq[N];          // quadrature weights
@@ -82,82 +62,15 @@ struct ResCfg {
   static constexpr int LINES = 3 * N2;
   static constexpr int EPB = LINES <= 32 ? 6 : (LINES <= 64 ? 4 : 2);
   static constexpr int THREADS = ((EPB * LINES + 31) / 32) * 32;
-  // WORK: line phase = 8 N3 node primitives + 9 N3 half cofactors;
-  //       tail = 10 N3 pass buffers + 30 N2 face-lift buffers
-  static constexpr int WORK = (15 * N3 > 10 * N3 + 30 * N2) ? 15 * N3 : 10 * N3 + 30 * N2;
-  static constexpr int PER_EL = 15 * N3 + WORK + N3;  // ACCV (3 x 5 N3) + WORK + w J
+  // ACCV (3 directions x 5 N3) + node primitives (6 N3) + half cofactors (9 N3)
+  static constexpr int PER_EL = 30 * N3;
   static constexpr int SMEM = EPB * PER_EL * 8;
 #ifdef NSFR_RES_MINB
   static constexpr int MINB = NSFR_RES_MINB;
 #else
   static constexpr int MINB = SMEM <= 56 * 1024 ? 4 : (SMEM <= 75 * 1024 ? 3 : (SMEM <= 112 * 1024 ? 2 : 1));
 #endif
-  static constexpr int LPT = (EPB * 5 * N2 + THREADS - 1) / THREADS;  // epilogue lines per thread
 };
-
-// Line pass along D over nb*5 tensors [N^3] with element strides; optional
-// injection of a face array (two sides, [s][side][N2] per element) through the
-// boundary vectors bvec[side][r], and optional division by w J (smem).
-template <int N, int D, bool INJ, bool DIV>
-__device__ __forceinline__ void tail_pass(const double (&op)[N * N], const double (&bvec)[2 * N],
-                                          const double* inj, int inj_es, const double* in, int in_es,
-                                          double* out, int out_es, const double* wj, int nbs,
-                                          int tid, int nthr) {
-  constexpr int N2 = N * N, N3 = N * N * N;
-  constexpr int stride = D == 0 ? 1 : (D == 1 ? N : N2);
-  for (int it = tid; it < nbs * N2; it += nthr) {
-    const int bsi = it / N2, l = it - bsi * N2;
-    const int b = bsi / 5, s = bsi - 5 * b;
-    const int l0 = l % N, l1 = l / N;
-    const int base = D == 0 ? N * (l0 + N * l1) : (D == 1 ? l0 + N2 * l1 : l0 + N * l1);
-    const double* src = in + b * in_es + s * N3 + base;
-    double x[N];
-#pragma unroll
-    for (int a = 0; a < N; ++a) x[a] = src[a * stride];
-    double f0 = 0.0, f1 = 0.0;
-    if (INJ) {
-      f0 = inj[b * inj_es + (s * 2 + 0) * N2 + l];
-      f1 = inj[b * inj_es + (s * 2 + 1) * N2 + l];
-    }
-    double* dst = out + b * out_es + s * N3 + base;
-#pragma unroll
-    for (int r = 0; r < N; ++r) {
-      double acc = 0.0;
-#pragma unroll
-      for (int a = 0; a < N; ++a) acc = fma(op[r * N + a], x[a], acc);
-      if (INJ) {
-        acc = fma(bvec[r], f0, acc);
-        acc = fma(bvec[N + r], f1, acc);
-      }
-      if (DIV) acc = acc * wj[b * N3 + base + r * stride];  // wj holds 1/(w J)
-      dst[r * stride] = acc;
-    }
-  }
-}
-
-// Face-array pass (10 arrays [s][side] of N2 per element) along t1 (T=0) or t2 (T=1).
-template <int N, int T>
-__device__ __forceinline__ void tail_face_pass(const double (&op)[N * N], const double* in, int in_es,
-                                               double* out, int out_es, int nb, int tid, int nthr) {
-  constexpr int N2 = N * N;
-  constexpr int stride = T == 0 ? 1 : N;
-  for (int it = tid; it < nb * 10 * N; it += nthr) {
-    const int b = it / (10 * N), r = it - b * 10 * N, bi = r / N, l = r - bi * N;
-    const int base = T == 0 ? N * l : l;
-    const double* src = in + b * in_es + bi * N2 + base;
-    double x[N];
-#pragma unroll
-    for (int a = 0; a < N; ++a) x[a] = src[a * stride];
-    double* dst = out + b * out_es + bi * N2 + base;
-#pragma unroll
-    for (int rr = 0; rr < N; ++rr) {
-      double acc = 0.0;
-#pragma unroll
-      for (int a = 0; a < N; ++a) acc = fma(op[rr * N + a], x[a], acc);
-      dst[rr * stride] = acc;
-    }
-  }
-}
 
 // L2 prefetch of everything batch `e0` will read (issued one batch ahead).
 template <int N>
@@ -170,12 +83,9 @@ __device__ __forceinline__ void res_prefetch(const ResParams& P, int e0, int tid
   switch (tid) {
     case 0: l2_prefetch(P.ut_vol + (size_t)e0 * 6 * N3, nb * 6 * N3 * b8); break;
     case 1: l2_prefetch(P.cof + (size_t)e0 * 9 * N3, nb * 9 * N3 * b8); break;
-    case 2: l2_prefetch(P.wj + (size_t)e0 * N3, nb * N3 * b8); break;
-    case 3: l2_prefetch(P.traces + (size_t)e0 * 30 * N2, nb * 30 * N2 * b8); break;
-    case 4: if (P.stage >= 1) l2_prefetch(P.un + (size_t)e0 * 5 * N3, nb * 5 * N3 * b8); break;
-    case 5: if (P.stage >= 2) l2_prefetch(P.acc + (size_t)e0 * 5 * N3, nb * 5 * N3 * b8); break;
-    default: {  // neighbour face blocks (geometry.hpp:24-29), lanes 6.. : (element, face)
-      const int j = tid - 6;
+    case 2: l2_prefetch(P.traces + (size_t)e0 * 30 * N2, nb * 30 * N2 * b8); break;
+    default: {  // neighbour face blocks (geometry.hpp:24-29), lanes 3.. : (element, face)
+      const int j = tid - 3;
       if (j >= 6 * nb) break;
       const int e = e0 + j / 6, f = j % 6, dir = f / 2, step = (f & 1) ? 1 : -1;
       const int mm = P.m;
@@ -203,16 +113,14 @@ __device__ __forceinline__ void res_batch(const ResParams& P, const ResOps<N>& O
   using Cfg = ResCfg<N>;
   constexpr int N2 = Cfg::N2, N3 = Cfg::N3, EPB = Cfg::EPB, LINES = Cfg::LINES;
   constexpr int AS = 15 * N3;     // element stride of ACCV
-  constexpr int WS = Cfg::WORK;   // element stride of WORK
+  constexpr int WS = 15 * N3;     // element stride of WORK
   double* ACCV = sm;                    // [EPB][3][5][N3]
   double* WORK = ACCV + EPB * AS;       // [EPB][WS]
-  double* WJ = WORK + EPB * WS;         // [EPB][N3]
   const int tid = threadIdx.x, nthr = blockDim.x;
   const int nb = min(EPB, P.E - e0);
   const double g = P.gamma, gm1 = g - 1.0;
   PHASE_START();
-  // stage element data (pure copies): node primitives of u~ (written by K1),
-  // 0.5 C (stored pre-halved) and w J
+  // stage element data (pure copies): node primitives of u~ and 0.5 C (stored pre-halved)
 #pragma unroll
   for (int b = 0; b < EPB; ++b) {
     if (b < nb) {
@@ -222,10 +130,6 @@ __device__ __forceinline__ void res_batch(const ResParams& P, const ResOps<N>& O
       for (int i = tid; i < 6 * N3; i += nthr) cp_async8(w + i, pu + i);
       for (int i = tid; i < 9 * N3; i += nthr) cp_async8(w + 6 * N3 + i, pc + i);
     }
-  }
-  {
-    const double* pw = P.wj + (size_t)e0 * N3;
-    for (int i = tid; i < nb * N3; i += nthr) cp_async8(WJ + i, pw + i);
   }
   cp_async_wait_all();
   __syncthreads();
@@ -257,38 +161,13 @@ __device__ __forceinline__ void res_batch(const ResParams& P, const ResOps<N>& O
       const double ca0 = Ch[(0 + dir) * N3 + ia], ca1 = Ch[(3 + dir) * N3 + ia],
                    ca2 = Ch[(6 + dir) * N3 + ia];
       double fa[NS] = {0.0, 0.0, 0.0, 0.0, 0.0};
-      int bb0 = a + 1;
-#ifdef NSFR_PAIR2
-      // two independent pair fluxes per iteration (ILP for the FP64 pipe)
 #pragma unroll 1
-      for (; bb0 + 1 < N; bb0 += 2) {
-        const int ib = lbase + bb0 * stride, ic = ib + stride;
-        const PrimH pb{Pd[ib], Pd[N3 + ib], Pd[2 * N3 + ib], Pd[3 * N3 + ib],
-                       Pd[4 * N3 + ib], Pd[5 * N3 + ib]};
-        const PrimH pc{Pd[ic], Pd[N3 + ic], Pd[2 * N3 + ic], Pd[3 * N3 + ic],
-                       Pd[4 * N3 + ic], Pd[5 * N3 + ic]};
-        double f[NS], h[NS];
-        d_flux_h(pa, pb,ca0 + Ch[(0 + dir) * N3 + ib], ca1 + Ch[(3 + dir) * N3 + ib],
-                          ca2 + Ch[(6 + dir) * N3 + ib], f);
-        d_flux_h(pa, pc,ca0 + Ch[(0 + dir) * N3 + ic], ca1 + Ch[(3 + dir) * N3 + ic],
-                          ca2 + Ch[(6 + dir) * N3 + ic], h);
-        const double c = wt * O.q[a * N + bb0], d = wt * O.q[a * N + bb0 + 1];
-#pragma unroll
-        for (int s = 0; s < NS; ++s) {
-          fa[s] = fma(c, f[s], fa[s]);
-          acc[s * N3 + ib] = fma(-c, f[s], acc[s * N3 + ib]);
-          fa[s] = fma(d, h[s], fa[s]);
-          acc[s * N3 + ic] = fma(-d, h[s], acc[s * N3 + ic]);
-        }
-      }
-#endif
-#pragma unroll 1
-      for (int bb = bb0; bb < N; ++bb) {
+      for (int bb = a + 1; bb < N; ++bb) {
         const int ib = lbase + bb * stride;
         const PrimH pb{Pd[ib], Pd[N3 + ib], Pd[2 * N3 + ib], Pd[3 * N3 + ib],
                        Pd[4 * N3 + ib], Pd[5 * N3 + ib]};
         double f[NS];
-        d_flux_h(pa, pb,ca0 + Ch[(0 + dir) * N3 + ib], ca1 + Ch[(3 + dir) * N3 + ib],
+        d_flux_h(pa, pb, ca0 + Ch[(0 + dir) * N3 + ib], ca1 + Ch[(3 + dir) * N3 + ib],
                           ca2 + Ch[(6 + dir) * N3 + ib], f);
         const double c = wt * O.q[a * N + bb];
 #pragma unroll
@@ -349,7 +228,7 @@ __device__ __forceinline__ void res_batch(const ResParams& P, const ResOps<N>& O
         const PrimH pa{Pd[ia], Pd[N3 + ia], Pd[2 * N3 + ia], Pd[3 * N3 + ia],
                        Pd[4 * N3 + ia], Pd[5 * N3 + ia]};
         double fl[NS];
-        d_flux_h(pa, pfh,Ch[(0 + dir) * N3 + ia] + ch0, Ch[(3 + dir) * N3 + ia] + ch1,
+        d_flux_h(pa, pfh, Ch[(0 + dir) * N3 + ia] + ch0, Ch[(3 + dir) * N3 + ia] + ch1,
                           Ch[(6 + dir) * N3 + ia] + ch2, fl);
         const double c = sign * O.bflux[side * N + a] * wt;
 #pragma unroll
@@ -382,154 +261,32 @@ __device__ __forceinline__ void res_batch(const ResParams& P, const ResOps<N>& O
       }
     }
   }
-  __syncthreads();
-  PHASE_MARK(1);
-#ifdef NSFR_SKIP_TAIL  // timing diagnostic only: stage states stay u_n (results are wrong)
-  if (tid == 0) P.out[e0] = ACCV[0] + fout0[0] + fout1[0];
-  if (P.stage >= 1 && P.stage <= 3)
-    for (int i = tid; i < nb * 5 * N3; i += nthr) P.us[(size_t)e0 * 5 * N3 + i] = P.un[(size_t)e0 * 5 * N3 + i];
-  return;
-#endif
-
-  // ---- tail ----
-  const int nbs = nb * 5;
-  // prefetch the RK epilogue operands (same line mapping as the final pass)
-  double pre_un[Cfg::LPT][N], pre_acc[Cfg::LPT][N];
-#pragma unroll
-  for (int j = 0; j < Cfg::LPT; ++j) {
-    const int it = tid + j * nthr;
-#pragma unroll
-    for (int c = 0; c < N; ++c) pre_un[j][c] = pre_acc[j][c] = 0.0;
-    if (it < nbs * N2 && P.stage >= 1) {
-      const int bsi = it / N2, l = it - bsi * N2;
-      const size_t gb = (size_t)e0 * 5 * N3 + (size_t)bsi * N3 + l;  // zeta line: base = l
-#pragma unroll
-      for (int c = 0; c < N; ++c) {
-        pre_un[j][c] = P.un[gb + c * N2];
-        if (P.stage >= 2) pre_acc[j][c] = P.acc[gb + c * N2];
-      }
-    }
-  }
-  // vol = sum of the three direction accumulators (into ACCV[b][0])
-  for (int it = tid; it < nbs * N3; it += nthr) {
-    const int b = it / (5 * N3), r = it - b * 5 * N3;
-    double* a0 = ACCV + b * AS;
-    a0[r] = a0[r] + a0[5 * N3 + r] + a0[10 * N3 + r];
-  }
-  __syncthreads();
-  // face rows -> FACC[b][dir][s][side][N2] = ACCV[b][5N3 : 5N3 + 30N2]
-  double* FACC = ACCV + 5 * N3;
+  // face rows straight from registers: facc[e][dir][s][side][k]
   if (lb < nb) {
-    const int t1 = lrem % N, t2 = lrem / N, k = t1 + N * t2;
+    const int k = (lrem % N) + N * (lrem / N);
+    double* fa = P.facc + ((size_t)(e0 + lb) * 3 + ldir) * 10 * N2 + k;
 #pragma unroll
     for (int s = 0; s < NS; ++s) {
-      FACC[lb * AS + ldir * 10 * N2 + (s * 2 + 0) * N2 + k] = fout0[s];
-      FACC[lb * AS + ldir * 10 * N2 + (s * 2 + 1) * N2 + k] = fout1[s];
+      fa[(s * 2 + 0) * N2] = fout0[s];
+      fa[(s * 2 + 1) * N2] = fout1[s];
     }
   }
   __syncthreads();
-  double* G = WORK + 10 * N3;  // [b][G1: 10N2 | G2: 10N2 | H2: 10N2]
-  if (!P.dS) {
-    // Pi~^T S9 in three fused passes; 1/(w J) in the last
-    tail_pass<N, 0, true, false>(O.M, O.bm, FACC, AS, ACCV, AS, WORK, WS, WJ, nbs, tid, nthr);
-    tail_face_pass<N, 0>(O.M, FACC + 10 * N2, AS, G, WS, nb, tid, nthr);
-    tail_face_pass<N, 0>(O.M, FACC + 20 * N2, AS, G + 10 * N2, WS, nb, tid, nthr);
-    __syncthreads();
-    tail_pass<N, 1, true, false>(O.M, O.bm, G, WS, WORK, WS, WORK + 5 * N3, WS, WJ, nbs, tid, nthr);
-    tail_face_pass<N, 1>(O.M, G + 10 * N2, WS, G + 20 * N2, WS, nb, tid, nthr);
-    __syncthreads();
-    tail_pass<N, 2, true, true>(O.M, O.bm, G + 20 * N2, WS, WORK + 5 * N3, WS, ACCV, AS, WJ, nbs,
-                                tid, nthr);
-    __syncthreads();
-  } else {
-    // entropy diagnostic: R = S9 explicitly (chi^T, bound_sol), -v_hat . R, then Pi~^T
-    tail_pass<N, 0, true, false>(O.it, O.bs, FACC, AS, ACCV, AS, WORK, WS, WJ, nbs, tid, nthr);
-    tail_face_pass<N, 0>(O.it, FACC + 10 * N2, AS, G, WS, nb, tid, nthr);
-    tail_face_pass<N, 0>(O.it, FACC + 20 * N2, AS, G + 10 * N2, WS, nb, tid, nthr);
-    __syncthreads();
-    tail_pass<N, 1, true, false>(O.it, O.bs, G, WS, WORK, WS, WORK + 5 * N3, WS, WJ, nbs, tid, nthr);
-    tail_face_pass<N, 1>(O.it, G + 10 * N2, WS, G + 20 * N2, WS, nb, tid, nthr);
-    __syncthreads();
-    tail_pass<N, 2, true, false>(O.it, O.bs, G + 20 * N2, WS, WORK + 5 * N3, WS, ACCV, AS, WJ, nbs,
-                                 tid, nthr);
-    __syncthreads();
-    for (int it = tid; it < nbs * N3; it += nthr) {
-      const int b = it / (5 * N3), r = it - b * 5 * N3;
-      WORK[b * WS + r] = P.vhat[(size_t)(e0 + b) * 5 * N3 + r] * ACCV[b * AS + r];
-    }
-    __syncthreads();
-    if (tid < nb) {
-      double s = 0.0;
-      for (int r = 0; r < 5 * N3; ++r) s += WORK[tid * WS + r];
-      P.dS[e0 + tid] = -s;
-    }
-    __syncthreads();
-    tail_pass<N, 0, false, false>(O.frt, O.bs, nullptr, 0, ACCV, AS, WORK, WS, WJ, nbs, tid, nthr);
-    __syncthreads();
-    tail_pass<N, 1, false, false>(O.frt, O.bs, nullptr, 0, WORK, WS, WORK + 5 * N3, WS, WJ, nbs, tid,
-                                  nthr);
-    __syncthreads();
-    tail_pass<N, 2, false, true>(O.frt, O.bs, nullptr, 0, WORK + 5 * N3, WS, ACCV, AS, WJ, nbs, tid,
-                                 nthr);
-    __syncthreads();
+  PHASE_MARK(1);
+  // volume rows: sum of the three direction accumulators
+  for (int it = tid; it < nb * 5 * N3; it += nthr) {
+    const int b = it / (5 * N3), r = it - b * 5 * N3;
+    const double* a0 = ACCV + b * AS;
+    P.vol[(size_t)e0 * 5 * N3 + it] = a0[r] + a0[5 * N3 + r] + a0[10 * N3 + r];
   }
   PHASE_MARK(2);
-  // second half of S10: Pi~ along xi, eta
-  tail_pass<N, 0, false, false>(O.fr, O.bs, nullptr, 0, ACCV, AS, WORK, WS, WJ, nbs, tid, nthr);
-  __syncthreads();
-  tail_pass<N, 1, false, false>(O.fr, O.bs, nullptr, 0, WORK, WS, WORK + 5 * N3, WS, WJ, nbs, tid,
-                                nthr);
-  __syncthreads();
-  // Pi~ along zeta, negate, RK stage epilogue (zeta lines: coalesced across the warp)
-  const double dt = P.stage ? *P.dt : 0.0;
-  const double hdt = 0.5 * dt, sdt = dt / 6.0;
-#pragma unroll
-  for (int j = 0; j < Cfg::LPT; ++j) {
-    const int it = tid + j * nthr;
-    if (it >= nbs * N2) break;
-    const int bsi = it / N2, l = it - bsi * N2;
-    const int b = bsi / 5, s = bsi - 5 * b;
-    const double* src = WORK + b * WS + 5 * N3 + s * N3 + l;
-    double x[N];
-#pragma unroll
-    for (int a = 0; a < N; ++a) x[a] = src[a * N2];
-    const size_t gb = (size_t)e0 * 5 * N3 + (size_t)bsi * N3 + l;
-#pragma unroll
-    for (int c = 0; c < N; ++c) {
-      double z = 0.0;
-#pragma unroll
-      for (int a = 0; a < N; ++a) z = fma(O.fr[c * N + a], x[a], z);
-      const double kv = -z;
-      const size_t gi = gb + c * N2;
-      switch (P.stage) {
-        case 0: P.out[gi] = kv; break;
-        case 1:
-          P.acc[gi] = kv;
-          P.us[gi] = fma(hdt, kv, pre_un[j][c]);
-          break;
-        case 2:
-          P.acc[gi] = fma(2.0, kv, pre_acc[j][c]);
-          P.us[gi] = fma(hdt, kv, pre_un[j][c]);
-          break;
-        case 3:
-          P.acc[gi] = fma(2.0, kv, pre_acc[j][c]);
-          P.us[gi] = fma(dt, kv, pre_un[j][c]);
-          break;
-        default: {
-          const double a4 = pre_acc[j][c] + kv;
-          P.un[gi] = fma(sdt, a4, pre_un[j][c]);
-        }
-      }
-    }
-  }
-  PHASE_MARK(3);
 }
 
-// One batch per CTA (CTAs retire at staggered times, so their staging, line
-// and tail phases overlap on each SM — a persistent grid that walks batches
-// in lockstep measured slower). Each CTA prefetches into L2 the batch of the
-// CTA `ahead` = #resident CTAs later, which the block scheduler starts about
-// when this one retires, so that CTA's staging loads hit L2.
+// One batch per CTA (CTAs retire at staggered times, so their staging and
+// line phases overlap on each SM — a persistent grid that walks batches in
+// lockstep measured slower). Each CTA prefetches into L2 the batch of the CTA
+// `ahead` = #resident CTAs later, which the block scheduler starts about when
+// this one retires, so that CTA's staging loads hit L2.
 template <int N>
 __global__ void __launch_bounds__(ResCfg<N>::THREADS, ResCfg<N>::MINB)
     k_residual(ResParams P, ResOps<N> O, int ahead) {

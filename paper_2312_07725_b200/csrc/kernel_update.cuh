@@ -1,0 +1,298 @@
+// K3: the rest of the residual, the RK4 stage update and the NEXT stage's
+// entropy projection, fused:
+//   S9  chi^T lifting of the volume rows (K2's vol) and face rows (K2's facc)
+//   S10 weight-adjusted inverse -Pi~ (W J)^-1 Pi~^T R (fr_operators.cpp:280-309, D6)
+//   RK  classical RK4 stage update (D4)
+//   S1-S5 of u_{s+1} (kernel_project.cuh::proj_core) straight from shared memory,
+//       so the stage state never round-trips through HBM; lambda_max of the
+//       new u_n after the last stage (adaptive dt of the next step).
+//
+// S9 and the first half of S10 are both tensor products, so
+//   Pi~^T^3 R = M^3 vol + sum_f (b_f (x) M (x) M) facc_f,  M = Pi~^T chi^T, b_f = Pi~^T bs_f
+// runs as three LINE passes with the face lifts injected into the pass of
+// their normal direction, the 1/(w J) scaling fused into the last one, then
+// three Pi~ passes with the RK update fused into the last. (The entropy
+// diagnostic needs R itself: that path lifts with chi^T first.)
+//
+// Stage 0 is a plain residual (dU/dt into `out`, optional -v_hat . R); stages
+// 1-3 accumulate acc and project u_{s+1}; stage 4 writes u_{n+1} and projects it.
+#pragma once
+#include "kernel_project.cuh"
+#include "physics.cuh"
+
+namespace nsfr_b200 {
+
+struct UpdParams {
+  const double* vol;   // [E][5][N^3] volume rows (K2)
+  const double* facc;  // [E][3][5][2][N^2] face rows (K2)
+  const double* wj;    // [E][N^3] 1/(w J)
+  const double* vhat;  // [E][5][N^3] or nullptr (entropy diagnostic, stage 0)
+  double* dS;          // [E] or nullptr
+  double* un;          // RK base state (stage 4 writes it)
+  double* acc;         // RK accumulator
+  double* out;         // stage 0: dU/dt
+  const double* dt;    // device scalar
+  int stage;
+  ProjParams pj;       // projection of u_{s+1} (pj.u unused); pj.err, pj.E shared
+};
+
+template <int N>
+struct TailOps {
+  double M[N * N];       // Pi~^T chi^T          (lift + project, hot path)
+  double bm[2 * N];      // Pi~^T bound_sol_side
+  double fr[N * N];      // Pi~                  (np x nq)
+  double frt[N * N];     // Pi~^T                (entropy-diagnostic path)
+  double it[N * N];      // chi^T                (entropy-diagnostic path)
+  double bs[2 * N];      // bound_sol            (entropy-diagnostic path)
+};
+
+template <int N>
+struct UpdOps {
+  TailOps<N> t;
+  ProjOps<N> p;
+};
+
+template <int N>
+struct UpdCfg {
+  static constexpr int N2 = N * N, N3 = N * N * N;
+  static constexpr int EPB = ProjCfg<N>::EPB;  // proj_core's batch layout
+  static constexpr int THREADS = ProjCfg<N>::THREADS;
+  // R0 vol/u_{s+1}, R1, R2 pass buffers (5 N3 each), R3 facc / face scratch,
+  // R4 face-lift buffers (30 N2 each), R5 1/(w J) (N3)
+  static constexpr int PER_EL = 16 * N3 + 60 * N2;
+  static constexpr int SMEM = EPB * PER_EL * 8;
+  // CTAs per SM: what shared memory allows, but keep >= RMIN registers per thread
+  static constexpr int RMIN = N <= 5 ? 64 : 80;
+  static constexpr int FIT_S = (228 * 1024) / (SMEM + 1024), FIT_R = 65536 / (THREADS * RMIN);
+  static constexpr int FIT = FIT_S < FIT_R ? FIT_S : FIT_R;
+  static constexpr int MINB = FIT < 1 ? 1 : (FIT > 8 ? 8 : FIT);
+  static constexpr int LPT = (EPB * 5 * N2 + THREADS - 1) / THREADS;  // epilogue lines per thread
+};
+
+// Line pass along D over nbs = nb*5 tensors [N^3] with element strides; optional
+// injection of a face array (two sides, [s][side][N2] per element) through the
+// boundary vectors bvec[side][r], and optional scaling by 1/(w J) (smem).
+template <int N, int D, bool INJ, bool DIV>
+__device__ __forceinline__ void tail_pass(const double (&op)[N * N], const double (&bvec)[2 * N],
+                                          const double* inj, int inj_es, const double* in, int in_es,
+                                          double* out, int out_es, const double* wj, int nbs,
+                                          int tid, int nthr) {
+  constexpr int N2 = N * N, N3 = N * N * N;
+  constexpr int stride = D == 0 ? 1 : (D == 1 ? N : N2);
+  for (int it = tid; it < nbs * N2; it += nthr) {
+    const int bsi = it / N2, l = it - bsi * N2;
+    const int b = bsi / 5, s = bsi - 5 * b;
+    const int l0 = l % N, l1 = l / N;
+    const int base = D == 0 ? N * (l0 + N * l1) : (D == 1 ? l0 + N2 * l1 : l0 + N * l1);
+    const double* src = in + b * in_es + s * N3 + base;
+    double x[N];
+#pragma unroll
+    for (int a = 0; a < N; ++a) x[a] = src[a * stride];
+    double f0 = 0.0, f1 = 0.0;
+    if (INJ) {
+      f0 = inj[b * inj_es + (s * 2 + 0) * N2 + l];
+      f1 = inj[b * inj_es + (s * 2 + 1) * N2 + l];
+    }
+    double* dst = out + b * out_es + s * N3 + base;
+#pragma unroll
+    for (int r = 0; r < N; ++r) {
+      double acc = 0.0;
+#pragma unroll
+      for (int a = 0; a < N; ++a) acc = fma(op[r * N + a], x[a], acc);
+      if (INJ) {
+        acc = fma(bvec[r], f0, acc);
+        acc = fma(bvec[N + r], f1, acc);
+      }
+      if (DIV) acc = acc * wj[b * N3 + base + r * stride];  // wj holds 1/(w J)
+      dst[r * stride] = acc;
+    }
+  }
+}
+
+// Face-array pass (10 arrays [s][side] of N2 per element) along t1 (T=0) or t2 (T=1).
+template <int N, int T>
+__device__ __forceinline__ void tail_face_pass(const double (&op)[N * N], const double* in, int in_es,
+                                               double* out, int out_es, int nb, int tid, int nthr) {
+  constexpr int N2 = N * N;
+  constexpr int stride = T == 0 ? 1 : N;
+  for (int it = tid; it < nb * 10 * N; it += nthr) {
+    const int b = it / (10 * N), r = it - b * 10 * N, bi = r / N, l = r - bi * N;
+    const int base = T == 0 ? N * l : l;
+    const double* src = in + b * in_es + bi * N2 + base;
+    double x[N];
+#pragma unroll
+    for (int a = 0; a < N; ++a) x[a] = src[a * stride];
+    double* dst = out + b * out_es + bi * N2 + base;
+#pragma unroll
+    for (int rr = 0; rr < N; ++rr) {
+      double acc = 0.0;
+#pragma unroll
+      for (int a = 0; a < N; ++a) acc = fma(op[rr * N + a], x[a], acc);
+      dst[rr * stride] = acc;
+    }
+  }
+}
+
+template <int N>
+__device__ __forceinline__ void upd_prefetch(const UpdParams& P, int e0, int tid) {
+  using Cfg = UpdCfg<N>;
+  constexpr int N2 = Cfg::N2, N3 = Cfg::N3, EPB = Cfg::EPB;
+  if (e0 >= P.pj.E || tid >= 6) return;
+  const size_t nb = min(EPB, P.pj.E - e0), b8 = sizeof(double);
+  switch (tid) {
+    case 0: l2_prefetch(P.vol + (size_t)e0 * 5 * N3, nb * 5 * N3 * b8); break;
+    case 1: l2_prefetch(P.facc + (size_t)e0 * 30 * N2, nb * 30 * N2 * b8); break;
+    case 2: l2_prefetch(P.wj + (size_t)e0 * N3, nb * N3 * b8); break;
+    case 3: if (P.stage >= 1) l2_prefetch(P.un + (size_t)e0 * 5 * N3, nb * 5 * N3 * b8); break;
+    case 4: if (P.stage >= 2) l2_prefetch(P.acc + (size_t)e0 * 5 * N3, nb * 5 * N3 * b8); break;
+    default: if (P.vhat) l2_prefetch(P.vhat + (size_t)e0 * 5 * N3, nb * 5 * N3 * b8);
+  }
+}
+
+template <int N>
+__device__ __forceinline__ void upd_batch(const UpdParams& P, const UpdOps<N>& O, int e0, double* sm) {
+  using Cfg = UpdCfg<N>;
+  constexpr int N2 = Cfg::N2, N3 = Cfg::N3, EPB = Cfg::EPB;
+  constexpr int VS = 5 * N3, FS = 30 * N2;  // element strides of the volume / face regions
+  double* R0 = sm;                 // vol, then Pi~^T R, then u_{s+1}
+  double* R1 = R0 + EPB * VS;
+  double* R2 = R1 + EPB * VS;
+  double* R3 = R2 + EPB * VS;      // facc [b][dir][s][side][N2], later proj_core face scratch
+  double* R4 = R3 + EPB * FS;      // [b][G1 | G2 | H2] (10 N2 each)
+  double* WJ = R4 + EPB * FS;
+  const TailOps<N>& T = O.t;
+  const int tid = threadIdx.x, nthr = blockDim.x;
+  const int nb = min(EPB, P.pj.E - e0);
+  const int nbs = nb * 5;
+  {
+    const double* pv = P.vol + (size_t)e0 * VS;
+    const double* pf = P.facc + (size_t)e0 * FS;
+    const double* pw = P.wj + (size_t)e0 * N3;
+    for (int i = tid; i < nb * VS; i += nthr) cp_async8(R0 + i, pv + i);
+    for (int i = tid; i < nb * FS; i += nthr) cp_async8(R3 + i, pf + i);
+    for (int i = tid; i < nb * N3; i += nthr) cp_async8(WJ + i, pw + i);
+  }
+  // RK operands of the final pass (zeta lines, same mapping), in flight meanwhile
+  double pre_un[Cfg::LPT][N], pre_acc[Cfg::LPT][N];
+#pragma unroll
+  for (int j = 0; j < Cfg::LPT; ++j) {
+    const int it = tid + j * nthr;
+#pragma unroll
+    for (int c = 0; c < N; ++c) pre_un[j][c] = pre_acc[j][c] = 0.0;
+    if (it < nbs * N2 && P.stage >= 1) {
+      const int bsi = it / N2, l = it - bsi * N2;
+      const size_t gb = (size_t)e0 * VS + (size_t)bsi * N3 + l;
+#pragma unroll
+      for (int c = 0; c < N; ++c) {
+        pre_un[j][c] = P.un[gb + c * N2];
+        if (P.stage >= 2) pre_acc[j][c] = P.acc[gb + c * N2];
+      }
+    }
+  }
+  cp_async_wait_all();
+  __syncthreads();
+
+  if (!P.dS) {
+    // Pi~^T S9 in three fused passes; 1/(w J) in the last
+    tail_pass<N, 0, true, false>(T.M, T.bm, R3, FS, R0, VS, R1, VS, WJ, nbs, tid, nthr);
+    tail_face_pass<N, 0>(T.M, R3 + 10 * N2, FS, R4, FS, nb, tid, nthr);
+    tail_face_pass<N, 0>(T.M, R3 + 20 * N2, FS, R4 + 10 * N2, FS, nb, tid, nthr);
+    __syncthreads();
+    tail_pass<N, 1, true, false>(T.M, T.bm, R4, FS, R1, VS, R2, VS, WJ, nbs, tid, nthr);
+    tail_face_pass<N, 1>(T.M, R4 + 10 * N2, FS, R4 + 20 * N2, FS, nb, tid, nthr);
+    __syncthreads();
+    tail_pass<N, 2, true, true>(T.M, T.bm, R4 + 20 * N2, FS, R2, VS, R0, VS, WJ, nbs, tid, nthr);
+    __syncthreads();
+  } else {
+    // entropy diagnostic: R = S9 explicitly (chi^T, bound_sol), -v_hat . R, then Pi~^T
+    tail_pass<N, 0, true, false>(T.it, T.bs, R3, FS, R0, VS, R1, VS, WJ, nbs, tid, nthr);
+    tail_face_pass<N, 0>(T.it, R3 + 10 * N2, FS, R4, FS, nb, tid, nthr);
+    tail_face_pass<N, 0>(T.it, R3 + 20 * N2, FS, R4 + 10 * N2, FS, nb, tid, nthr);
+    __syncthreads();
+    tail_pass<N, 1, true, false>(T.it, T.bs, R4, FS, R1, VS, R2, VS, WJ, nbs, tid, nthr);
+    tail_face_pass<N, 1>(T.it, R4 + 10 * N2, FS, R4 + 20 * N2, FS, nb, tid, nthr);
+    __syncthreads();
+    tail_pass<N, 2, true, false>(T.it, T.bs, R4 + 20 * N2, FS, R2, VS, R0, VS, WJ, nbs, tid, nthr);
+    __syncthreads();
+    for (int it = tid; it < nbs * N3; it += nthr) R1[it] = P.vhat[(size_t)e0 * VS + it] * R0[it];
+    __syncthreads();
+    if (tid < nb) {
+      double s = 0.0;
+      for (int r = 0; r < VS; ++r) s += R1[tid * VS + r];
+      P.dS[e0 + tid] = -s;
+    }
+    __syncthreads();
+    tail_pass<N, 0, false, false>(T.frt, T.bs, nullptr, 0, R0, VS, R1, VS, WJ, nbs, tid, nthr);
+    __syncthreads();
+    tail_pass<N, 1, false, false>(T.frt, T.bs, nullptr, 0, R1, VS, R2, VS, WJ, nbs, tid, nthr);
+    __syncthreads();
+    tail_pass<N, 2, false, true>(T.frt, T.bs, nullptr, 0, R2, VS, R0, VS, WJ, nbs, tid, nthr);
+    __syncthreads();
+  }
+  // second half of S10: Pi~ along xi, eta
+  tail_pass<N, 0, false, false>(T.fr, T.bs, nullptr, 0, R0, VS, R1, VS, WJ, nbs, tid, nthr);
+  __syncthreads();
+  tail_pass<N, 1, false, false>(T.fr, T.bs, nullptr, 0, R1, VS, R2, VS, WJ, nbs, tid, nthr);
+  __syncthreads();
+  // Pi~ along zeta, negate, RK stage epilogue (zeta lines: coalesced across the
+  // warp); u_{s+1} also lands in R0 for the projection below
+  const double dt = P.stage ? *P.dt : 0.0;
+  const double hdt = 0.5 * dt, sdt = dt / 6.0;
+#pragma unroll
+  for (int j = 0; j < Cfg::LPT; ++j) {
+    const int it = tid + j * nthr;
+    if (it >= nbs * N2) break;
+    const int bsi = it / N2, l = it - bsi * N2;
+    const double* src = R2 + bsi * N3 + l;
+    double x[N];
+#pragma unroll
+    for (int a = 0; a < N; ++a) x[a] = src[a * N2];
+    const size_t gb = (size_t)e0 * VS + (size_t)bsi * N3 + l;
+    double* nxt = R0 + bsi * N3 + l;
+#pragma unroll
+    for (int c = 0; c < N; ++c) {
+      double z = 0.0;
+#pragma unroll
+      for (int a = 0; a < N; ++a) z = fma(T.fr[c * N + a], x[a], z);
+      const double kv = -z;
+      const size_t gi = gb + c * N2;
+      switch (P.stage) {
+        case 0: P.out[gi] = kv; break;
+        case 1:
+          P.acc[gi] = kv;
+          nxt[c * N2] = fma(hdt, kv, pre_un[j][c]);
+          break;
+        case 2:
+          P.acc[gi] = fma(2.0, kv, pre_acc[j][c]);
+          nxt[c * N2] = fma(hdt, kv, pre_un[j][c]);
+          break;
+        case 3:
+          P.acc[gi] = fma(2.0, kv, pre_acc[j][c]);
+          nxt[c * N2] = fma(dt, kv, pre_un[j][c]);
+          break;
+        default: {
+          const double a4 = pre_acc[j][c] + kv;
+          const double u1 = fma(sdt, a4, pre_un[j][c]);
+          P.un[gi] = u1;
+          nxt[c * N2] = u1;
+        }
+      }
+    }
+  }
+  if (P.stage == 0) return;
+  __syncthreads();
+  proj_core<N>(P.pj, O.p, e0, nb, R0, R1, R2, R3);
+}
+
+// One batch per CTA with look-ahead L2 prefetch (see k_residual).
+template <int N>
+__global__ void __launch_bounds__(UpdCfg<N>::THREADS, UpdCfg<N>::MINB)
+    k_update(UpdParams P, UpdOps<N> O, int ahead) {
+  extern __shared__ double sm[];
+  constexpr int EPB = UpdCfg<N>::EPB;
+  const long long pe = (static_cast<long long>(blockIdx.x) + ahead) * EPB;
+  if (pe < P.pj.E) upd_prefetch<N>(P, static_cast<int>(pe), threadIdx.x);
+  upd_batch<N>(P, O, blockIdx.x * EPB, sm);
+}
+
+}  // namespace nsfr_b200

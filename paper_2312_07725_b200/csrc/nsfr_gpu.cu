@@ -22,7 +22,8 @@ struct nsfr_gpu_ctx {
   Tables1D tab;
   DevTables htab{};  // host copy of the device tables (source of the kernel-parameter operators)
   DevTables* d_tab = nullptr;
-  double *d_un = nullptr, *d_us = nullptr, *d_acc = nullptr, *d_rhs = nullptr;
+  double *d_un = nullptr, *d_acc = nullptr, *d_rhs = nullptr;
+  double *d_vol = nullptr, *d_facc = nullptr;  // K2 -> K3 volume / face rows
   double *d_utv = nullptr, *d_tr = nullptr, *d_cof = nullptr, *d_jac = nullptr, *d_wj = nullptr;
   double *d_vhat = nullptr, *d_dS = nullptr, *d_part = nullptr, *d_red = nullptr;
   double *d_send_lo = nullptr, *d_send_hi = nullptr, *d_halo_lo = nullptr, *d_halo_hi = nullptr;
@@ -35,6 +36,9 @@ struct nsfr_gpu_ctx {
   int rank = 0, nranks = 1, peer_lo = 0, peer_hi = 0;
   long long halo_count = 0;
   cudaGraphExec_t graph = nullptr;
+  // ut_vol/traces hold the projection of d_un and lam_bits its lambda_max
+  // (K3 re-projects after every stage); cleared when d_un changes from outside
+  bool proj_valid = false;
   long long launches = 0;
   // per-launch event timing (bench roofline)
   bool timing = false;
@@ -71,7 +75,7 @@ size_t state_count(const nsfr_gpu_ctx* c) { return static_cast<size_t>(c->E) * N
 // Per-N launch configuration of the persistent kernels: resident CTAs on the device.
 template <int N>
 struct Resident {
-  static inline int proj = 0, res = 0;
+  static inline int proj = 0, res = 0, upd = 0;
 };
 
 template <int N>
@@ -79,14 +83,17 @@ int set_attrs(nsfr_gpu_ctx* ctx) {
   if (Resident<N>::res) return NSFR_OK;
   CK(cudaFuncSetAttribute(k_project<N>, cudaFuncAttributeMaxDynamicSharedMemorySize, ProjCfg<N>::SMEM));
   CK(cudaFuncSetAttribute(k_residual<N>, cudaFuncAttributeMaxDynamicSharedMemorySize, ResCfg<N>::SMEM));
-  int sms = 0, bp = 0, br = 0;
+  CK(cudaFuncSetAttribute(k_update<N>, cudaFuncAttributeMaxDynamicSharedMemorySize, UpdCfg<N>::SMEM));
+  int sms = 0, bp = 0, br = 0, bu = 0;
   CK(cudaDeviceGetAttribute(&sms, cudaDevAttrMultiProcessorCount, ctx->s.device));
   CK(cudaOccupancyMaxActiveBlocksPerMultiprocessor(&bp, k_project<N>, ProjCfg<N>::THREADS, ProjCfg<N>::SMEM));
   CK(cudaOccupancyMaxActiveBlocksPerMultiprocessor(&br, k_residual<N>, ResCfg<N>::THREADS, ResCfg<N>::SMEM));
+  CK(cudaOccupancyMaxActiveBlocksPerMultiprocessor(&bu, k_update<N>, UpdCfg<N>::THREADS, UpdCfg<N>::SMEM));
   // NSFR_NO_PREFETCH=1 disables the look-ahead L2 prefetch (A/B measurements)
   const bool pf = std::getenv("NSFR_NO_PREFETCH") == nullptr;
   Resident<N>::proj = pf ? sms * std::max(bp, 1) : (1 << 30);
   Resident<N>::res = pf ? sms * std::max(br, 1) : (1 << 30);
+  Resident<N>::upd = pf ? sms * std::max(bu, 1) : (1 << 30);
   return NSFR_OK;
 }
 
@@ -107,7 +114,8 @@ void ev_end(nsfr_gpu_ctx* c) {
 
 // 1D operators for the kernel-parameter bank, from the host table copy
 template <int N>
-ProjOps<N> proj_ops(const DevTables& t) {
+ProjOps<N> proj_ops(const nsfr_gpu_ctx* ctx) {
+  const DevTables& t = ctx->htab;
   ProjOps<N> o{};
   for (int i = 0; i < N * N; ++i) {
     o.interp[i] = t.interp[i];
@@ -121,12 +129,28 @@ ProjOps<N> proj_ops(const DevTables& t) {
       o.bp[side * N + a] = s;
     }
   o.c35 = 0.0;
+  {  // closed-form u(v) when gamma/(gamma-1) == 7/2 in exact arithmetic (gamma = 1.4)
+    const double g = ctx->s.gamma, gm1 = g - 1.0;
+    if (std::fabs(g / gm1 - 3.5) < 1e-12 && std::getenv("NSFR_POW_U_OF_V") == nullptr)
+      o.c35 = std::pow(gm1, 1.0 / gm1);
+  }
   return o;
 }
 
 template <int N>
 ResOps<N> res_ops(const DevTables& t) {
   ResOps<N> o{};
+  for (int i = 0; i < N * N; ++i) o.q[i] = t.qskew[i];
+  for (int i = 0; i < 2 * N; ++i) o.bflux[i] = t.bflux[i];
+  for (int i = 0; i < N; ++i) o.wq[i] = t.wq[i];
+  return o;
+}
+
+template <int N>
+UpdOps<N> upd_ops(const nsfr_gpu_ctx* ctx) {
+  const DevTables& t = ctx->htab;
+  UpdOps<N> u{};
+  TailOps<N>& o = u.t;
   for (int a = 0; a < N; ++a)
     for (int i = 0; i < N; ++i) {
       // M = Pi~^T chi^T: (Pi~^T)[a][r] = frproj[r][a], (chi^T)[r][i] = interp[i][r]
@@ -144,19 +168,14 @@ ResOps<N> res_ops(const DevTables& t) {
     o.fr[i] = t.frproj[i];
     o.frt[i] = t.frproj_t[i];
     o.it[i] = t.interp_t[i];
-    o.q[i] = t.qskew[i];
   }
-  for (int i = 0; i < 2 * N; ++i) {
-    o.bs[i] = t.bsol[i];
-    o.bflux[i] = t.bflux[i];
-  }
-  for (int i = 0; i < N; ++i) o.wq[i] = t.wq[i];
-  return o;
+  for (int i = 0; i < 2 * N; ++i) o.bs[i] = t.bsol[i];
+  u.p = proj_ops<N>(ctx);
+  return u;
 }
 
-template <int N>
-int launch_project(nsfr_gpu_ctx* ctx, const double* u, bool want_lam) {
-  if (int rc = set_attrs<N>(ctx)) return rc;
+// projection parameters writing ut_vol / traces / halo send buffers
+ProjParams proj_params(nsfr_gpu_ctx* ctx, const double* u, bool want_lam) {
   ProjParams P{};
   P.u = u;
   P.ut_vol = ctx->d_utv;
@@ -170,15 +189,17 @@ int launch_project(nsfr_gpu_ctx* ctx, const double* u, bool want_lam) {
   P.m = ctx->m;
   P.nz = ctx->nz;
   P.gamma = ctx->s.gamma;
+  return P;
+}
+
+template <int N>
+int launch_project(nsfr_gpu_ctx* ctx, const double* u, bool want_lam) {
+  if (int rc = set_attrs<N>(ctx)) return rc;
+  const ProjParams P = proj_params(ctx, u, want_lam);
   const int grid = (ctx->E + ProjCfg<N>::EPB - 1) / ProjCfg<N>::EPB;
-  ProjOps<N> ops = proj_ops<N>(ctx->htab);
-  {  // closed-form u(v) when gamma/(gamma-1) == 7/2 in exact arithmetic (gamma = 1.4)
-    const double g = ctx->s.gamma, gm1 = g - 1.0;
-    if (std::fabs(g / gm1 - 3.5) < 1e-12 && std::getenv("NSFR_POW_U_OF_V") == nullptr)
-      ops.c35 = std::pow(gm1, 1.0 / gm1);
-  }
   ev_begin(ctx, 1);
-  k_project<N><<<grid, ProjCfg<N>::THREADS, ProjCfg<N>::SMEM, ctx->st>>>(P, ops, Resident<N>::proj);
+  k_project<N><<<grid, ProjCfg<N>::THREADS, ProjCfg<N>::SMEM, ctx->st>>>(P, proj_ops<N>(ctx),
+                                                                         Resident<N>::proj);
   ev_end(ctx);
   ++ctx->launches;
   CK(cudaGetLastError());
@@ -186,23 +207,16 @@ int launch_project(nsfr_gpu_ctx* ctx, const double* u, bool want_lam) {
 }
 
 template <int N>
-int launch_residual(nsfr_gpu_ctx* ctx, int stage, bool entropy) {
+int launch_residual(nsfr_gpu_ctx* ctx) {
   ResParams P{};
   P.ut_vol = ctx->d_utv;
   P.traces = ctx->d_tr;
   P.halo_lo = ctx->nranks > 1 ? ctx->d_halo_lo : nullptr;
   P.halo_hi = ctx->nranks > 1 ? ctx->d_halo_hi : nullptr;
   P.cof = ctx->d_cof;
-  P.wj = ctx->d_wj;
-  P.vhat = entropy ? ctx->d_vhat : nullptr;
-  P.dS = entropy ? ctx->d_dS : nullptr;
-  P.un = ctx->d_un;
-  P.us = ctx->d_us;
-  P.acc = ctx->d_acc;
-  P.out = ctx->d_rhs;
-  P.dt = &ctx->d_step->dt;
+  P.vol = ctx->d_vol;
+  P.facc = ctx->d_facc;
   P.err = ctx->d_err;
-  P.stage = stage;
   P.E = ctx->E;
   P.m = ctx->m;
   P.nz = ctx->nz;
@@ -219,29 +233,48 @@ int launch_residual(nsfr_gpu_ctx* ctx, int stage, bool entropy) {
   return NSFR_OK;
 }
 
-int project(nsfr_gpu_ctx* ctx, const double* u, bool lam) {
-  switch (ctx->N) {
-    case 3: return launch_project<3>(ctx, u, lam);
-    case 4: return launch_project<4>(ctx, u, lam);
-    case 5: return launch_project<5>(ctx, u, lam);
-    case 6: return launch_project<6>(ctx, u, lam);
-    case 7: return launch_project<7>(ctx, u, lam);
-  }
-  ctx->msg = "unsupported p";
-  return NSFR_E_DIM;
+// stage 0: dU/dt (+ entropy change); stages 1-4: RK update and projection of
+// the next stage state (lambda_max after stage 4)
+template <int N>
+int launch_update(nsfr_gpu_ctx* ctx, int stage, bool entropy) {
+  UpdParams P{};
+  P.vol = ctx->d_vol;
+  P.facc = ctx->d_facc;
+  P.wj = ctx->d_wj;
+  P.vhat = entropy ? ctx->d_vhat : nullptr;
+  P.dS = entropy ? ctx->d_dS : nullptr;
+  P.un = ctx->d_un;
+  P.acc = ctx->d_acc;
+  P.out = ctx->d_rhs;
+  P.dt = &ctx->d_step->dt;
+  P.stage = stage;
+  P.pj = proj_params(ctx, nullptr, stage == 4);
+  P.pj.vhat = nullptr;
+  if (int rc = set_attrs<N>(ctx)) return rc;
+  const int grid = (ctx->E + UpdCfg<N>::EPB - 1) / UpdCfg<N>::EPB;
+  ev_begin(ctx, 3);
+  k_update<N><<<grid, UpdCfg<N>::THREADS, UpdCfg<N>::SMEM, ctx->st>>>(P, upd_ops<N>(ctx),
+                                                                      Resident<N>::upd);
+  ev_end(ctx);
+  ++ctx->launches;
+  CK(cudaGetLastError());
+  return NSFR_OK;
 }
 
-int residual(nsfr_gpu_ctx* ctx, int stage, bool entropy) {
-  switch (ctx->N) {
-    case 3: return launch_residual<3>(ctx, stage, entropy);
-    case 4: return launch_residual<4>(ctx, stage, entropy);
-    case 5: return launch_residual<5>(ctx, stage, entropy);
-    case 6: return launch_residual<6>(ctx, stage, entropy);
-    case 7: return launch_residual<7>(ctx, stage, entropy);
-  }
-  ctx->msg = "unsupported p";
-  return NSFR_E_DIM;
-}
+#define NSFR_DISPATCH(fn, args)                \
+  switch (ctx->N) {                            \
+    case 3: return fn<3> args;                 \
+    case 4: return fn<4> args;                 \
+    case 5: return fn<5> args;                 \
+    case 6: return fn<6> args;                 \
+    case 7: return fn<7> args;                 \
+  }                                            \
+  ctx->msg = "unsupported p";                  \
+  return NSFR_E_DIM
+
+int project(nsfr_gpu_ctx* ctx, const double* u, bool lam) { NSFR_DISPATCH(launch_project, (ctx, u, lam)); }
+int residual(nsfr_gpu_ctx* ctx) { NSFR_DISPATCH(launch_residual, (ctx)); }
+int update(nsfr_gpu_ctx* ctx, int stage, bool entropy) { NSFR_DISPATCH(launch_update, (ctx, stage, entropy)); }
 
 // z-face halo exchange with the two slab neighbours
 int exchange(nsfr_gpu_ctx* ctx) {
@@ -262,33 +295,43 @@ int allreduce_sum(nsfr_gpu_ctx* ctx, double* d, int n) {
   return NSFR_OK;
 }
 
-// one full residual of `u` into d_rhs (stage 0)
-int rhs_of(nsfr_gpu_ctx* ctx, const double* u, bool entropy) {
-  if (int rc = project(ctx, u, false)) return rc;
-  if (int rc = exchange(ctx)) return rc;
-  return residual(ctx, 0, entropy);
+// K1 of d_un with lambda_max (the step pipeline's prologue)
+int project_state(nsfr_gpu_ctx* ctx) {
+  k_step_begin<<<1, 1, 0, ctx->st>>>(ctx->d_step);
+  ++ctx->launches;
+  if (int rc = project(ctx, ctx->d_un, true)) return rc;
+  ctx->proj_valid = true;
+  return NSFR_OK;
 }
 
-// enqueue one RK4 step (no host sync). fixed_dt: dt already in d_step.
+int ensure_projected(nsfr_gpu_ctx* ctx) { return ctx->proj_valid ? NSFR_OK : project_state(ctx); }
+
+// one full residual of d_un into d_rhs (stage 0)
+int rhs_of_state(nsfr_gpu_ctx* ctx, bool entropy) {
+  if (int rc = project_state(ctx)) return rc;
+  if (int rc = exchange(ctx)) return rc;
+  if (int rc = residual(ctx)) return rc;
+  return update(ctx, 0, entropy);
+}
+
+// Enqueue one RK4 step (no host sync), graph-capturable: needs the projection
+// of d_un in place (ensure_projected) and leaves the projection of u_{n+1}.
+// fixed_dt: dt already in d_step.
+constexpr long long kLaunchesPerStep = 1 + 4 * 2 + 1;
 int enqueue_step(nsfr_gpu_ctx* ctx, bool fixed_dt) {
-  if (!fixed_dt) {
-    k_step_begin<<<1, 1, 0, ctx->st>>>(ctx->d_step);
-    ++ctx->launches;
-  }
-  if (int rc = project(ctx, ctx->d_un, !fixed_dt)) return rc;
   if (!fixed_dt) {
     if (ctx->nranks > 1)
       NK(ncclAllReduce(&ctx->d_step->lam_bits, &ctx->d_step->lam_bits, 1, ncclUint64, ncclMax,
                        ctx->comm, ctx->st));
-    k_step_dt<<<1, 1, 0, ctx->st>>>(ctx->d_step);
-    ++ctx->launches;
+    k_step_dt<<<1, 1, 0, ctx->st>>>(ctx->d_step);  // reads and clears lambda
+  } else {
+    k_step_begin<<<1, 1, 0, ctx->st>>>(ctx->d_step);  // clears lambda
   }
-  if (int rc = exchange(ctx)) return rc;
-  if (int rc = residual(ctx, 1, false)) return rc;
-  for (int stage = 2; stage <= 4; ++stage) {
-    if (int rc = project(ctx, ctx->d_us, false)) return rc;
+  ++ctx->launches;
+  for (int stage = 1; stage <= 4; ++stage) {
     if (int rc = exchange(ctx)) return rc;
-    if (int rc = residual(ctx, stage, false)) return rc;
+    if (int rc = residual(ctx)) return rc;
+    if (int rc = update(ctx, stage, false)) return rc;
   }
   k_step_end<<<1, 1, 0, ctx->st>>>(ctx->d_step);
   ++ctx->launches;
@@ -459,9 +502,9 @@ int nsfr_gpu_create(const nsfr_gpu_setup* setup, nsfr_gpu_ctx** out) {
   const size_t ns = state_count(ctx), n3 = static_cast<size_t>(ctx->E) * nsol(ctx);
   const size_t ntr = static_cast<size_t>(ctx->E) * 6 * NS * ctx->N * ctx->N;
   auto alloc = [&](double** p, size_t n) { return cudaMalloc(p, sizeof(double) * std::max<size_t>(n, 1)); };
-  if (cudaMalloc(&ctx->d_tab, sizeof(DevTables)) || alloc(&ctx->d_un, ns) || alloc(&ctx->d_us, ns) ||
+  if (cudaMalloc(&ctx->d_tab, sizeof(DevTables)) || alloc(&ctx->d_un, ns) || alloc(&ctx->d_vol, ns) ||
       alloc(&ctx->d_acc, ns) || alloc(&ctx->d_rhs, ns) || alloc(&ctx->d_utv, 6 * n3) ||
-      alloc(&ctx->d_tr, ntr) || alloc(&ctx->d_cof, 9 * n3) || alloc(&ctx->d_jac, n3) ||
+      alloc(&ctx->d_tr, ntr) || alloc(&ctx->d_facc, ntr) || alloc(&ctx->d_cof, 9 * n3) || alloc(&ctx->d_jac, n3) ||
       alloc(&ctx->d_wj, n3) || alloc(&ctx->d_dS, ctx->E) || alloc(&ctx->d_part, 2 * (size_t)ctx->E) ||
       alloc(&ctx->d_red, 4) || cudaMalloc(&ctx->d_step, sizeof(StepState)) ||
       cudaMalloc(&ctx->d_err, sizeof(unsigned)) ||
@@ -549,7 +592,7 @@ int nsfr_gpu_destroy(nsfr_gpu_ctx* ctx) {
   if (ctx->graph) cudaGraphExecDestroy(ctx->graph);
   for (auto e : ctx->ev_pool) cudaEventDestroy(e);
   if (ctx->comm) ncclCommDestroy(ctx->comm);
-  double* bufs[] = {ctx->d_un,  ctx->d_us,   ctx->d_acc,  ctx->d_rhs,     ctx->d_utv,     ctx->d_tr,
+  double* bufs[] = {ctx->d_un,  ctx->d_vol,  ctx->d_facc, ctx->d_acc,  ctx->d_rhs,     ctx->d_utv,     ctx->d_tr,
                     ctx->d_cof, ctx->d_jac,  ctx->d_wj,   ctx->d_vhat,    ctx->d_dS,      ctx->d_part,
                     ctx->d_red, ctx->d_send_lo, ctx->d_send_hi, ctx->d_halo_lo, ctx->d_halo_hi};
   for (double* b : bufs)
@@ -605,6 +648,7 @@ int nsfr_gpu_get_metrics(nsfr_gpu_ctx* ctx, double* jac, double* cof) {
 }
 
 int nsfr_gpu_set_state(nsfr_gpu_ctx* ctx, const double* u) {
+  ctx->proj_valid = false;
   CK(cudaMemcpyAsync(ctx->d_un, u, sizeof(double) * state_count(ctx), cudaMemcpyHostToDevice, ctx->st));
   CK(cudaStreamSynchronize(ctx->st));
   return NSFR_OK;
@@ -633,6 +677,7 @@ int nsfr_gpu_init_case(nsfr_gpu_ctx* ctx, int kind) {
   P.beta = ctx->s.beta;
   P.l = length_scale(ctx->s);
   P.gamma = ctx->s.gamma;
+  ctx->proj_valid = false;
   k_init<<<ctx->E, 128, smem, ctx->st>>>(P);
   ++ctx->launches;
   CK(cudaGetLastError());
@@ -657,7 +702,7 @@ int nsfr_gpu_rhs(nsfr_gpu_ctx* ctx, double* dudt, double* entropy_change) {
     ctx->msg = "entropy change needs setup.entropy_diag = 1";
     return NSFR_E_CONFIG;
   }
-  if (int rc = rhs_of(ctx, ctx->d_un, ent)) return rc;
+  if (int rc = rhs_of_state(ctx, ent)) return rc;
   if (ent) {
     k_reduce<<<1, 1024, 0, ctx->st>>>(ctx->d_dS, ctx->E, 1, ctx->d_red);
     ++ctx->launches;
@@ -679,9 +724,7 @@ int nsfr_gpu_get_traces(nsfr_gpu_ctx* ctx, double* traces) {
 }
 
 int nsfr_gpu_max_wavespeed(nsfr_gpu_ctx* ctx, double* lam) {
-  k_step_begin<<<1, 1, 0, ctx->st>>>(ctx->d_step);
-  ++ctx->launches;
-  if (int rc = project(ctx, ctx->d_un, true)) return rc;
+  if (int rc = project_state(ctx)) return rc;
   if (ctx->nranks > 1)
     NK(ncclAllReduce(&ctx->d_step->lam_bits, &ctx->d_step->lam_bits, 1, ncclUint64, ncclMax, ctx->comm, ctx->st));
   if (int rc = sync_check(ctx)) return rc;
@@ -692,6 +735,7 @@ int nsfr_gpu_max_wavespeed(nsfr_gpu_ctx* ctx, double* lam) {
 
 int nsfr_gpu_rk4_step_dt(nsfr_gpu_ctx* ctx, double dt) {
   CK(cudaMemcpyAsync(&ctx->d_step->dt, &dt, sizeof dt, cudaMemcpyHostToDevice, ctx->st));
+  if (int rc = ensure_projected(ctx)) return rc;
   if (int rc = enqueue_step(ctx, true)) return rc;
   return sync_check(ctx);
 }
@@ -708,6 +752,7 @@ static int set_step_params(nsfr_gpu_ctx* ctx, double cfl, double t_final) {
 
 int nsfr_gpu_rk4_step(nsfr_gpu_ctx* ctx, double cfl, double t_final, double* dt_used) {
   if (int rc = set_step_params(ctx, cfl, t_final)) return rc;
+  if (int rc = ensure_projected(ctx)) return rc;
   if (int rc = enqueue_step(ctx, false)) return rc;
   if (int rc = sync_check(ctx)) return rc;
   if (dt_used) *dt_used = ctx->h_step->dt;
@@ -716,6 +761,7 @@ int nsfr_gpu_rk4_step(nsfr_gpu_ctx* ctx, double cfl, double t_final, double* dt_
 
 int nsfr_gpu_advance(nsfr_gpu_ctx* ctx, int nsteps, double cfl, double t_final, double* t_out) {
   if (int rc = set_step_params(ctx, cfl, t_final)) return rc;
+  if (int rc = ensure_projected(ctx)) return rc;
   if (!ctx->graph && !ctx->timing) {
     cudaGraph_t g;
     CK(cudaStreamBeginCapture(ctx->st, cudaStreamCaptureModeThreadLocal));
@@ -727,7 +773,6 @@ int nsfr_gpu_advance(nsfr_gpu_ctx* ctx, int nsteps, double cfl, double t_final, 
     cudaGraphDestroy(g);
     ctx->launches = l0;  // counted on replay
   }
-  const long long per_step = 4 * 2 + 3;
   // with a final time, poll t every 16 steps (steps past t_final have dt = 0)
   const int chunk = t_final > 0.0 ? 16 : nsteps;
   for (int i = 0; i < nsteps; ++i) {
@@ -735,7 +780,7 @@ int nsfr_gpu_advance(nsfr_gpu_ctx* ctx, int nsteps, double cfl, double t_final, 
       if (int rc = enqueue_step(ctx, false)) return rc;
     } else {
       CK(cudaGraphLaunch(ctx->graph, ctx->st));
-      ctx->launches += per_step;
+      ctx->launches += kLaunchesPerStep;
     }
     if (chunk < nsteps && (i + 1) % chunk == 0) {
       if (int rc = sync_check(ctx)) return rc;
@@ -787,13 +832,14 @@ long long nsfr_gpu_launch_count(const nsfr_gpu_ctx* ctx) { return ctx->launches;
 
 // Bench helper: time `nsteps` RK4 steps with CUDA events on the context
 // stream. With kernel_ms != NULL each K1/K2 launch is bracketed by events and
-// kernel_ms[0]/[1] receive the summed K1/K2 durations (ms).
+// kernel_ms[0]/[1]/[2] receive the summed K1/K2/K3 durations (ms).
 int nsfr_gpu_time_steps(nsfr_gpu_ctx* ctx, int nsteps, double cfl, double* step_ms,
                         double* kernel_ms) {
   if (int rc = set_step_params(ctx, cfl, 0.0)) return rc;
   if (!kernel_ms && !ctx->graph) {
     if (int rc = nsfr_gpu_advance(ctx, 0, cfl, 0.0, nullptr)) return rc;  // capture the step graph
   }
+  if (int rc = ensure_projected(ctx)) return rc;
   ctx->timing = kernel_ms != nullptr;
   ctx->ev_marks.clear();
   cudaEvent_t a, b;
@@ -806,7 +852,7 @@ int nsfr_gpu_time_steps(nsfr_gpu_ctx* ctx, int nsteps, double cfl, double* step_
       rc = enqueue_step(ctx, false);
     } else {
       CK(cudaGraphLaunch(ctx->graph, ctx->st));
-      ctx->launches += 4 * 2 + 3;
+      ctx->launches += kLaunchesPerStep;
     }
   }
   CK(cudaEventRecord(b, ctx->st));
@@ -815,7 +861,7 @@ int nsfr_gpu_time_steps(nsfr_gpu_ctx* ctx, int nsteps, double cfl, double* step_
   CK(cudaEventElapsedTime(&ms, a, b));
   *step_ms = ms;
   if (kernel_ms) {
-    kernel_ms[0] = kernel_ms[1] = 0.0;
+    kernel_ms[0] = kernel_ms[1] = kernel_ms[2] = 0.0;
     for (auto& mk : ctx->ev_marks) {
       float x = 0.f;
       cudaEventElapsedTime(&x, ctx->ev_pool[mk.second], ctx->ev_pool[mk.second + 1]);

@@ -368,6 +368,7 @@ __global__ void k_step_dt(StepState* S) {
       dt = fmin(dt, S->t_final - S->t);
   }
   S->dt = dt;
+  S->lam_bits = 0ull;  // K3 of the last stage accumulates the next step's lambda
 }
 
 __global__ void k_step_end(StepState* S) { S->t += S->dt; }

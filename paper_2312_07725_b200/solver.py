@@ -360,6 +360,6 @@ class GpuSolver:
 
     def time_steps(self, nsteps: int, cfl: float = 0.1, per_kernel: bool = False):
         ms = np.zeros(1)
-        kms = np.zeros(2) if per_kernel else None
+        kms = np.zeros(3) if per_kernel else None
         self._check(self.lib.nsfr_gpu_time_steps(self.ctx, nsteps, cfl, _ptr(ms), _ptr(kms)))
         return (float(ms[0]), kms.copy()) if per_kernel else float(ms[0])

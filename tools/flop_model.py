@@ -48,7 +48,7 @@ def per_element(p: int) -> dict:
     _add(c, dict(fl=2 * 6 * 5 * 3 * n3))         # S4 faces
     _add(c, ENTROPY_TO_CONS, n3 + 6 * n2)         # S5
     k1 = dict(c)
-    # K2 residual
+    # K2 pair and face fluxes
     pv, ps = 3 * n2 * n * (n - 1) // 2, 6 * n3
     pair = {}
     _add(pair, FLUX_EC)
@@ -63,17 +63,20 @@ def per_element(p: int) -> dict:
     _add(face, ROE)
     _add(face, ENTROPY_VARS, 2)                   # Roe's entropy-variable jump
     _add(c, face, 6 * n2)
+    k2 = {key: c.get(key, 0) - k1.get(key, 0) for key in c}
     _add(c, dict(fl=2 * 15 * n4))                # S9 chi^T^3 volume
     _add(c, dict(fl=2 * 6 * 5 * 3 * n3))         # S9 faces
     _add(c, dict(fl=2 * 2 * 15 * n4, div=5 * n3))  # S10 Pi~^T^3, /wJ, Pi~^3
     _add(c, dict(fl=5 * n3 * 2))                 # RK stage update (2 FMA-equivalents)
-    k2 = {key: c.get(key, 0) - k1.get(key, 0) for key in c}
+    # K3 = S9, S10, RK update (+ the next stage's projection, K1's work)
+    k3 = {key: c.get(key, 0) - k2.get(key, 0) for key in c}
     special = sum(c.get(s, 0) for s in ("div", "log", "exp", "pow", "sqrt"))
     return {
         "n": n,
         "flops_total": c["fl"] + special,
         "flops_k1": k1["fl"] + sum(k1.get(s, 0) for s in ("div", "log", "exp", "pow", "sqrt")),
         "flops_k2": k2["fl"] + sum(k2.get(s, 0) for s in ("div", "log", "exp", "pow", "sqrt")),
+        "flops_k3": k3["fl"] + sum(k3.get(s, 0) for s in ("div", "log", "exp", "pow", "sqrt")),
         "special": {s: c.get(s, 0) for s in ("div", "log", "exp", "pow", "sqrt")},
         "pairs": pv + ps,
         "face_fluxes": 6 * n2,

@@ -16,6 +16,6 @@ for p, m in sizes:
     dof = m ** 3 * (p + 1) ** 3 * 5
     print(json.dumps({"lib": os.environ.get("NSFR_B200_LIB", "default"), "p": p, "m": m,
                       "ms_per_step": ms / 4, "dof_updates_per_s": 4 * dof * 4 / (ms / 1e3),
-                      "k1_ms": kms[0] / 12, "k2_ms": kms[1] / 12,
+                      "k2_ms": kms[1] / 12, "k3_ms": kms[2] / 12,
                       "ns_per_elem_rhs": (ms / 4 / 4) * 1e6 / m ** 3}), flush=True)
     g.close()
