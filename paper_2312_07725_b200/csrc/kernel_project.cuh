@@ -247,13 +247,14 @@ __device__ __forceinline__ void proj_batch(const ProjParams& P, const ProjOps<N>
   double* A = sm;
   double* B = A + EPB * 5 * N3;
   double* V = B + EPB * 5 * N3;
-  const int tid = threadIdx.x, nthr = blockDim.x;
   const int nb = min(EPB, P.E - e0);
+  __shared__ unsigned long long bar;
   {
-    const double* src = P.u + (size_t)e0 * 5 * N3;
-    for (int i = tid; i < nb * 5 * N3; i += nthr) cp_async8(&A[i], src + i);
-    cp_async_wait_all();
+    const StageBlock blk[1] = {{A, P.u + (size_t)e0 * 5 * N3, nb * 5 * N3}};
+    stage_issue<1>(blk, &bar);
   }
+  __syncthreads();
+  stage_wait(&bar);
   __syncthreads();
   proj_core<N>(P, O, e0, nb, A, B, V, V + EPB * 5 * N3);
 }
@@ -262,7 +263,7 @@ __device__ __forceinline__ void proj_batch(const ProjParams& P, const ProjOps<N>
 // (= #resident CTAs) later (see k_residual).
 template <int N>
 __global__ void __launch_bounds__(ProjCfg<N>::THREADS) k_project(ProjParams P, ProjOps<N> O, int ahead) {
-  extern __shared__ double sm[];
+  extern __shared__ __align__(128) double sm[];
   constexpr int EPB = ProjCfg<N>::EPB, N3 = N * N * N;
   const int nbatch = (P.E + EPB - 1) / EPB;
   const long long pb = static_cast<long long>(blockIdx.x) + ahead;

@@ -113,25 +113,22 @@ __device__ __forceinline__ void res_batch(const ResParams& P, const ResOps<N>& O
   using Cfg = ResCfg<N>;
   constexpr int N2 = Cfg::N2, N3 = Cfg::N3, EPB = Cfg::EPB, LINES = Cfg::LINES;
   constexpr int AS = 15 * N3;     // element stride of ACCV
-  constexpr int WS = 15 * N3;     // element stride of WORK
   double* ACCV = sm;                    // [EPB][3][5][N3]
-  double* WORK = ACCV + EPB * AS;       // [EPB][WS]
+  double* PRIM = ACCV + EPB * AS;       // [EPB][6][N3] half-scaled primitives
+  double* COF = PRIM + EPB * 6 * N3;    // [EPB][9][N3] 0.5 C
   const int tid = threadIdx.x, nthr = blockDim.x;
   const int nb = min(EPB, P.E - e0);
   const double g = P.gamma, gm1 = g - 1.0;
   PHASE_START();
-  // stage element data (pure copies): node primitives of u~ and 0.5 C (stored pre-halved)
-#pragma unroll
-  for (int b = 0; b < EPB; ++b) {
-    if (b < nb) {
-      const double* pu = P.ut_vol + (size_t)(e0 + b) * 6 * N3;
-      const double* pc = P.cof + (size_t)(e0 + b) * 9 * N3;
-      double* w = WORK + b * WS;
-      for (int i = tid; i < 6 * N3; i += nthr) cp_async8(w + i, pu + i);
-      for (int i = tid; i < 9 * N3; i += nthr) cp_async8(w + 6 * N3 + i, pc + i);
-    }
+  // stage element data (pure copies, TMA bulk): node primitives of u~ and 0.5 C
+  __shared__ unsigned long long bar;
+  {
+    const StageBlock blk[2] = {{PRIM, P.ut_vol + (size_t)e0 * 6 * N3, nb * 6 * N3},
+                               {COF, P.cof + (size_t)e0 * 9 * N3, nb * 9 * N3}};
+    stage_issue<2>(blk, &bar);
   }
-  cp_async_wait_all();
+  __syncthreads();
+  stage_wait(&bar);
   __syncthreads();
   PHASE_MARK(0);
 
@@ -144,8 +141,8 @@ __device__ __forceinline__ void res_batch(const ResParams& P, const ResOps<N>& O
     const int b = lb, e = e0 + b, dir = ldir, t1 = lrem % N, t2 = lrem / N;
     const int stride = dir == 0 ? 1 : (dir == 1 ? N : N2);
     const int lbase = dir == 0 ? N * (t1 + N * t2) : (dir == 1 ? t1 + N2 * t2 : t1 + N * t2);
-    const double* Pd = WORK + b * WS;
-    const double* Ch = Pd + 6 * N3;
+    const double* Pd = PRIM + b * 6 * N3;
+    const double* Ch = COF + b * 9 * N3;
     double* acc = ACCV + b * AS + dir * 5 * N3;
     const double wt = O.wq[t1] * O.wq[t2];
 #pragma unroll
@@ -290,7 +287,7 @@ __device__ __forceinline__ void res_batch(const ResParams& P, const ResOps<N>& O
 template <int N>
 __global__ void __launch_bounds__(ResCfg<N>::THREADS, ResCfg<N>::MINB)
     k_residual(ResParams P, ResOps<N> O, int ahead) {
-  extern __shared__ double sm[];
+  extern __shared__ __align__(128) double sm[];
   constexpr int EPB = ResCfg<N>::EPB;
   const long long pe = (static_cast<long long>(blockIdx.x) + ahead) * EPB;
   if (pe < P.E) res_prefetch<N>(P, static_cast<int>(pe), threadIdx.x);

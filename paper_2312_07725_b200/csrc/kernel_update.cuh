@@ -164,14 +164,14 @@ __device__ __forceinline__ void upd_batch(const UpdParams& P, const UpdOps<N>& O
   const int tid = threadIdx.x, nthr = blockDim.x;
   const int nb = min(EPB, P.pj.E - e0);
   const int nbs = nb * 5;
+  __shared__ unsigned long long bar;
   {
-    const double* pv = P.vol + (size_t)e0 * VS;
-    const double* pf = P.facc + (size_t)e0 * FS;
-    const double* pw = P.wj + (size_t)e0 * N3;
-    for (int i = tid; i < nb * VS; i += nthr) cp_async8(R0 + i, pv + i);
-    for (int i = tid; i < nb * FS; i += nthr) cp_async8(R3 + i, pf + i);
-    for (int i = tid; i < nb * N3; i += nthr) cp_async8(WJ + i, pw + i);
+    const StageBlock blk[3] = {{R0, P.vol + (size_t)e0 * VS, nb * VS},
+                               {R3, P.facc + (size_t)e0 * FS, nb * FS},
+                               {WJ, P.wj + (size_t)e0 * N3, nb * N3}};
+    stage_issue<3>(blk, &bar);
   }
+  __syncthreads();
   // RK operands of the final pass (zeta lines, same mapping), in flight meanwhile
   double pre_un[Cfg::LPT][N], pre_acc[Cfg::LPT][N];
 #pragma unroll
@@ -189,7 +189,7 @@ __device__ __forceinline__ void upd_batch(const UpdParams& P, const UpdOps<N>& O
       }
     }
   }
-  cp_async_wait_all();
+  stage_wait(&bar);
   __syncthreads();
 
   if (!P.dS) {
@@ -288,7 +288,7 @@ __device__ __forceinline__ void upd_batch(const UpdParams& P, const UpdOps<N>& O
 template <int N>
 __global__ void __launch_bounds__(UpdCfg<N>::THREADS, UpdCfg<N>::MINB)
     k_update(UpdParams P, UpdOps<N> O, int ahead) {
-  extern __shared__ double sm[];
+  extern __shared__ __align__(128) double sm[];
   constexpr int EPB = UpdCfg<N>::EPB;
   const long long pe = (static_cast<long long>(blockIdx.x) + ahead) * EPB;
   if (pe < P.pj.E) upd_prefetch<N>(P, static_cast<int>(pe), threadIdx.x);
