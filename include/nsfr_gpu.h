@@ -152,7 +152,11 @@ int nsfr_gpu_time_steps(nsfr_gpu_ctx* ctx, int nsteps, double cfl, double* step_
 /* FP64 pipe peak of `device` in TFLOP/s (DFMA loop; roofline denominator). */
 int nsfr_gpu_measure_fp64_peak(int device, double* tflops);
 
-/* Device pointers (for callers that keep inputs resident in HBM). */
+/* Device pointers (for callers that keep inputs resident in HBM). The device
+ * state holds u at the volume quadrature nodes, u_q = chi^3 u_hat ([e][5][n^3]);
+ * nsfr_gpu_set_state / nsfr_gpu_get_state convert from / to u_hat. A caller
+ * writing through this pointer must call nsfr_gpu_set_time (or set_state)
+ * before the next step so the cached projection is rebuilt. */
 double* nsfr_gpu_state_device_ptr(nsfr_gpu_ctx* ctx);
 size_t nsfr_gpu_state_count(const nsfr_gpu_ctx* ctx);
 /* Synchronise and report a pending device error (NSFR_E_INADMISSIBLE...). */

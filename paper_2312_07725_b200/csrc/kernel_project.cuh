@@ -1,6 +1,6 @@
 // K1: entropy projection S1-S5.
 //
-//   u_q = chi^3 u_hat;  v_q = v(u_q);  v_hat = Pi^3 v_q;
+//   u_q = chi^3 u_hat (the solver's state representation);  v_q = v(u_q);  v_hat = Pi^3 v_q;
 //   v~ = chi^3 v_hat at the volume, (bs_side (x) chi (x) chi) v_hat at each face;
 //   u~ = u(v~)                                   (euler.cpp:46-71)
 // plus lambda_max = max(|u| + a) over the volume nodes for adaptive dt.
@@ -17,7 +17,7 @@
 namespace nsfr_b200 {
 
 struct ProjParams {
-  const double* u;       // [E][5][N^3] stage input
+  const double* u;       // [E][5][N^3] stage input u_q at the volume quadrature nodes
   double* ut_vol;        // [E][6][N^3] rho,u,v,w,p,rho/p of the entropy-projected volume state
   double* traces;        // [E][6][5][N^2]
   double* vhat;          // [E][5][N^3] or nullptr
@@ -31,7 +31,6 @@ struct ProjParams {
 
 template <int N>
 struct ProjOps {
-  double interp[N * N];  // chi   (nq x np)
   double proj[N * N];    // Pi    (np x nq)
   double bsol[2 * N];    // bound_sol rows at xi = -1, +1
   double bp[2 * N];      // bound_sol_side Pi: face trace rows applied to nodal v (chi Pi = I)
@@ -138,8 +137,8 @@ __device__ __forceinline__ void face_pass(const double (&op)[N * N], const doubl
   }
 }
 
-// S1-S5 for the nb elements whose state u_hat sits in shared memory A
-// ([EPB*5][N3], synchronised by the caller). B, V: [EPB*5][N3] scratch;
+// S2-S5 for the nb elements whose state u_q (volume quadrature nodes) sits in
+// shared memory A ([EPB*5][N3], synchronised by the caller). B, V: [EPB*5][N3] scratch;
 // F: [3][EPB*5][2][N2] face scratch. Shared by K1 and the fused K3 (kernel_update.cuh).
 template <int N>
 __device__ __forceinline__ void proj_core(const ProjParams& P, const ProjOps<N>& O, int e0, int nb,
@@ -152,13 +151,8 @@ __device__ __forceinline__ void proj_core(const ProjParams& P, const ProjOps<N>&
   const int tid = threadIdx.x, nthr = blockDim.x;
   const double g = P.gamma;
   const int nbs = nb * 5;
-  // S1 u_q = chi^3 u_hat (xi, eta, zeta passes: apply_tensor_product order)
-  line_pass<N, 0, false>(O.interp, A, B, O.bsol, nullptr, nbs, tid, nthr);
-  __syncthreads();
-  line_pass<N, 1, false>(O.interp, B, A, O.bsol, nullptr, nbs, tid, nthr);
-  __syncthreads();
-  line_pass<N, 2, false>(O.interp, A, B, O.bsol, nullptr, nbs, tid, nthr);
-  __syncthreads();
+  // S1 u_q = chi^3 u_hat is where the state lives: the solver carries u_q
+  // (k_convert at the API boundary), so A already holds it.
   // S2 v(u_q) -> V, the wavespeed for adaptive dt, and the
   // volume state K2 consumes. With n_q = n_p (GL or LGL, no overintegration)
   // Pi = chi^-1, so the reference's volume round trip u(chi^3 Pi^3 v(u_q))
@@ -169,7 +163,7 @@ __device__ __forceinline__ void proj_core(const ProjParams& P, const ProjOps<N>&
     const int b = it / N3, q = it - b * N3;
     double uu[NS], vv[NS];
 #pragma unroll
-    for (int s = 0; s < NS; ++s) uu[s] = B[(b * 5 + s) * N3 + q];
+    for (int s = 0; s < NS; ++s) uu[s] = A[(b * 5 + s) * N3 + q];
     if (!d_entropy_vars(g, uu, vv)) {
       atomicOr(P.err, ERR_STATE);
 #pragma unroll

@@ -40,7 +40,7 @@ template <int N>
 struct TailOps {
   double M[N * N];       // Pi~^T chi^T          (lift + project, hot path)
   double bm[2 * N];      // Pi~^T bound_sol_side
-  double fr[N * N];      // Pi~                  (np x nq)
+  double fr[N * N];      // final passes: Pi~ (stage 0, u_hat space) or chi Pi~ (RK stages, u_q space)
   double frt[N * N];     // Pi~^T                (entropy-diagnostic path)
   double it[N * N];      // chi^T                (entropy-diagnostic path)
   double bs[2 * N];      // bound_sol            (entropy-diagnostic path)

@@ -117,10 +117,7 @@ template <int N>
 ProjOps<N> proj_ops(const nsfr_gpu_ctx* ctx) {
   const DevTables& t = ctx->htab;
   ProjOps<N> o{};
-  for (int i = 0; i < N * N; ++i) {
-    o.interp[i] = t.interp[i];
-    o.proj[i] = t.proj[i];
-  }
+  for (int i = 0; i < N * N; ++i) o.proj[i] = t.proj[i];
   for (int i = 0; i < 2 * N; ++i) o.bsol[i] = t.bsol[i];
   for (int side = 0; side < 2; ++side)
     for (int a = 0; a < N; ++a) {  // (bound_sol Pi)[side][a]; Pi is np x nq
@@ -146,8 +143,10 @@ ResOps<N> res_ops(const DevTables& t) {
   return o;
 }
 
+// stage 0 ends in u_hat space (Pi~^3: dU/dt of the coefficients); the RK
+// stages stay at the quadrature nodes, chi^3 Pi~^3 = (chi Pi~)^3
 template <int N>
-UpdOps<N> upd_ops(const nsfr_gpu_ctx* ctx) {
+UpdOps<N> upd_ops(const nsfr_gpu_ctx* ctx, int stage) {
   const DevTables& t = ctx->htab;
   UpdOps<N> u{};
   TailOps<N>& o = u.t;
@@ -164,8 +163,13 @@ UpdOps<N> upd_ops(const nsfr_gpu_ctx* ctx) {
       for (int r = 0; r < N; ++r) s += t.frproj[r * N + a] * t.bsol[side * N + r];
       o.bm[side * N + a] = s;
     }
+  for (int c = 0; c < N; ++c)
+    for (int a = 0; a < N; ++a) {
+      double s = 0.0;
+      for (int r = 0; r < N; ++r) s += t.interp[c * N + r] * t.frproj[r * N + a];
+      o.fr[c * N + a] = stage == 0 ? t.frproj[c * N + a] : s;
+    }
   for (int i = 0; i < N * N; ++i) {
-    o.fr[i] = t.frproj[i];
     o.frt[i] = t.frproj_t[i];
     o.it[i] = t.interp_t[i];
   }
@@ -253,7 +257,7 @@ int launch_update(nsfr_gpu_ctx* ctx, int stage, bool entropy) {
   if (int rc = set_attrs<N>(ctx)) return rc;
   const int grid = (ctx->E + UpdCfg<N>::EPB - 1) / UpdCfg<N>::EPB;
   ev_begin(ctx, 3);
-  k_update<N><<<grid, UpdCfg<N>::THREADS, UpdCfg<N>::SMEM, ctx->st>>>(P, upd_ops<N>(ctx),
+  k_update<N><<<grid, UpdCfg<N>::THREADS, UpdCfg<N>::SMEM, ctx->st>>>(P, upd_ops<N>(ctx, stage),
                                                                       Resident<N>::upd);
   ev_end(ctx);
   ++ctx->launches;
@@ -405,6 +409,15 @@ double length_scale(const nsfr_gpu_setup& s) {
 
 int setup_kernel_smem(nsfr_gpu_ctx* ctx, size_t bytes, const void* fn) {
   if (bytes > 48 * 1024) CK(cudaFuncSetAttribute(fn, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)bytes));
+  return NSFR_OK;
+}
+
+// u_hat <-> u_q (k_convert): to_quad applies chi^3, else Pi^3
+int convert_state(nsfr_gpu_ctx* ctx, const double* in, double* out, bool to_quad) {
+  const size_t smem = sizeof(double) * 4 * nsol(ctx);
+  k_convert<<<ctx->E, 128, smem, ctx->st>>>(ctx->d_tab, in, out, ctx->E, to_quad ? 1 : 0);
+  ++ctx->launches;
+  CK(cudaGetLastError());
   return NSFR_OK;
 }
 
@@ -649,13 +662,16 @@ int nsfr_gpu_get_metrics(nsfr_gpu_ctx* ctx, double* jac, double* cof) {
 
 int nsfr_gpu_set_state(nsfr_gpu_ctx* ctx, const double* u) {
   ctx->proj_valid = false;
-  CK(cudaMemcpyAsync(ctx->d_un, u, sizeof(double) * state_count(ctx), cudaMemcpyHostToDevice, ctx->st));
+  // u_hat -> scratch (d_vol is dead between steps) -> u_q = chi^3 u_hat
+  CK(cudaMemcpyAsync(ctx->d_vol, u, sizeof(double) * state_count(ctx), cudaMemcpyHostToDevice, ctx->st));
+  if (int rc = convert_state(ctx, ctx->d_vol, ctx->d_un, true)) return rc;
   CK(cudaStreamSynchronize(ctx->st));
   return NSFR_OK;
 }
 
 int nsfr_gpu_get_state(nsfr_gpu_ctx* ctx, double* u) {
-  CK(cudaMemcpyAsync(u, ctx->d_un, sizeof(double) * state_count(ctx), cudaMemcpyDeviceToHost, ctx->st));
+  if (int rc = convert_state(ctx, ctx->d_un, ctx->d_vol, false)) return rc;
+  CK(cudaMemcpyAsync(u, ctx->d_vol, sizeof(double) * state_count(ctx), cudaMemcpyDeviceToHost, ctx->st));
   CK(cudaStreamSynchronize(ctx->st));
   return NSFR_OK;
 }
@@ -667,7 +683,7 @@ int nsfr_gpu_init_case(nsfr_gpu_ctx* ctx, int kind) {
   if (int rc = setup_kernel_smem(ctx, smem, (const void*)k_init)) return rc;
   InitParams P{};
   P.tab = ctx->d_tab;
-  P.u = ctx->d_un;
+  P.u = ctx->d_vol;  // u_hat at the solution nodes, converted to u_q below
   P.E = ctx->E;
   P.m = ctx->m;
   P.k0 = ctx->k0;
@@ -681,10 +697,12 @@ int nsfr_gpu_init_case(nsfr_gpu_ctx* ctx, int kind) {
   k_init<<<ctx->E, 128, smem, ctx->st>>>(P);
   ++ctx->launches;
   CK(cudaGetLastError());
+  if (int rc = convert_state(ctx, ctx->d_vol, ctx->d_un, true)) return rc;
   return nsfr_gpu_set_time(ctx, 0.0);
 }
 
 int nsfr_gpu_set_time(nsfr_gpu_ctx* ctx, double t) {
+  ctx->proj_valid = false;  // also the re-sync point after writes through state_device_ptr
   CK(cudaMemcpyAsync(&ctx->d_step->t, &t, sizeof(double), cudaMemcpyHostToDevice, ctx->st));
   CK(cudaStreamSynchronize(ctx->st));
   return NSFR_OK;

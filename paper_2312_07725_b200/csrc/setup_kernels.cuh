@@ -5,7 +5,8 @@
 //   k_l2        L2 error partials; k_reduce deterministic sums
 //   k_step_*    adaptive-dt bookkeeping
 // Layout in HBM (element-contiguous blocks, xi fastest):
-//   state/us/acc [E][5][N^3]; ut_vol [E][8][N^3] node primitives; traces [E][6][5][N^2];
+//   state u_q/acc [E][5][N^3] at the volume quadrature nodes; ut_vol [E][6][N^3] node
+//   primitives; traces [E][6][5][N^2]; vol [E][5][N^3] and facc [E][3][5][2][N^2] (K2 -> K3);
 //   cof [E][9][N^3] = 0.5 C
 //   (component 3*n_phys + i_ref major); wj [E][N^3] = 1/(w_i w_j w_k J).
 #pragma once
@@ -263,6 +264,31 @@ __global__ void k_init(InitParams P) {
 
 
 // ---------------------------------------------------------------------------
+// State representation change at the API boundary: the solver carries u at the
+// volume quadrature nodes, u_q = chi^3 u_hat (the reference's S1); the API
+// speaks the reference's solution-node coefficients u_hat = Pi^3 u_q (Pi = chi^-1
+// for n_q = n_p). One CTA per element, 5 states.
+__global__ void k_convert(const DevTables* tab, const double* in, double* out, int E, int to_quad) {
+  extern __shared__ double sm[];
+  const DevTables& T = *tab;
+  const int e = blockIdx.x;
+  if (e >= E) return;
+  const int tid = threadIdx.x, nthr = blockDim.x;
+  const int n = T.nq, N3 = n * n * n;
+  double* src = sm;
+  double* t1 = src + N3;
+  double* t2 = t1 + N3;
+  double* dst = t2 + N3;
+  for (int s = 0; s < NS; ++s) {
+    for (int i = tid; i < N3; i += nthr) src[i] = in[((size_t)e * NS + s) * N3 + i];
+    __syncthreads();
+    tp3_rt(to_quad ? T.interp : T.proj, n, n, src, t1, t2, dst, tid, nthr);
+    for (int i = tid; i < N3; i += nthr) out[((size_t)e * NS + s) * N3 + i] = dst[i];
+    __syncthreads();
+  }
+}
+
+// ---------------------------------------------------------------------------
 // L2 error partials: per element sum w J (rho - rho_ex)^2 and (p - p_ex)^2.
 struct L2Params {
   const DevTables* tab;
@@ -299,12 +325,9 @@ __global__ void k_l2(L2Params P) {
   }
   __syncthreads();
   for (int d = 0; d < 3; ++d) tp3_rt(T.ig, n, g, xg + d * G3, t1, t2, xv + d * N3, tid, nthr);
-  for (int s = 0; s < NS; ++s) {
-    const double* src = P.u + ((size_t)e * NS + s) * N3;
-    for (int i = tid; i < N3; i += nthr) t2[i] = src[i];
-    __syncthreads();
-    tp3_rt(T.interp, n, n, t2, t1, xg, uq + s * N3, tid, nthr);
-  }
+  // the device state already holds u at the volume quadrature nodes (chi^3 u_hat)
+  for (int i = tid; i < NS * N3; i += nthr) uq[i] = P.u[(size_t)e * NS * N3 + i];
+  __syncthreads();
   for (int q = tid; q < N3; q += nthr) {
     const int i = q % n, j = (q / n) % n, k = q / (n * n);
     double w = T.wq[i];
