@@ -134,6 +134,39 @@ def test_rhs_native_setup(p, m, c1d, case, roe):
     assert_rhs_parity(g.rhs(), o.rhs(u), floor_of(o, u))
 
 
+@pytest.mark.parametrize("p,m,c1d,quad,gamma", [
+    (2, 5, 0.0, 0, 1.4),           # N = 3 instantiation
+    (2, 4, OC_PLUS[2], 0, 1.4),
+    (6, 2, 0.0, 0, 1.4),           # N = 7 instantiation (one element per CTA)
+    (3, 3, 0.0, 1, 1.4),           # LGL volume quadrature (chi = I)
+    (4, 2, OC_PLUS[4], 1, 1.4),
+    (3, 3, 0.0, 0, 5.0 / 3.0),     # gamma/(gamma-1) != 7/2: pow form of u(v)
+])
+def test_rhs_more_configs(p, m, c1d, quad, gamma):
+    """The other supported degrees, LGL quadrature and a non-air gamma, plus one
+    fixed-dt RK4 step through the quadrature-node state."""
+    cfg = dict(p=p, m=m, c1d=c1d, quad_kind=quad, gamma=gamma)
+    o = CpuSolver("oracle", Config(**cfg))
+    g = P().GpuSolver(gpu_cfg(**cfg))
+    g.init_case()
+    u = g.get_state()
+    np.testing.assert_allclose(u, o.initial_state(), rtol=1e-13, atol=1e-14)
+    assert_rhs_parity(g.rhs(), o.rhs(u), floor_of(o, u))
+    dt = 0.1 * o.dx() / o.max_wavespeed(u)
+    g.rk4_step_dt(dt)
+    uo = o.rk4_step(u.copy(), dt)
+    assert norm_rel(g.get_state() - u, uo - u) < 1e-10
+
+
+def test_state_round_trip():
+    """set_state / get_state convert u_hat <-> u_q (chi^3, Pi^3): ~1 ulp."""
+    g = P().GpuSolver(gpu_cfg(p=4, m=3, c1d=OC_PLUS[4]))
+    rng = np.random.default_rng(5)
+    u = 1.0 + rng.random(g.state_shape)
+    g.set_state(u)
+    np.testing.assert_allclose(g.get_state(), u, rtol=1e-14, atol=0)
+
+
 def test_config3_rhs_full_size():
     """BASELINE configs[2] at full size (32^3, p=4): one RHS against the oracle."""
     o = CpuSolver("oracle", Config(p=4, m=32))
