@@ -141,6 +141,10 @@ int nsfr_gpu_max_wavespeed(nsfr_gpu_ctx* ctx, double* lam);
 int nsfr_gpu_l2_error(nsfr_gpu_ctx* ctx, int case_kind, double out2[2]);
 /* -sum v_hat . R of the last RHS of the current state (allreduced). */
 int nsfr_gpu_entropy_change(nsfr_gpu_ctx* ctx, double* out);
+/* Conserved totals sum_e sum_q w_q J_q u_q of the current state: mass,
+ * x/y/z momentum, energy (DiagnosticRecord totals; Thm 3 drift
+ * check SPEC.md:650), allreduced in a fixed order. */
+int nsfr_gpu_conserved_totals(nsfr_gpu_ctx* ctx, double out5[5]);
 
 /* Bench helper: time nsteps RK4 steps (t_final unbounded) with CUDA events on
  * the context stream; inputs stay resident in HBM. kernel_ms (optional, [3])

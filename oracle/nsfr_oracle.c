@@ -1427,6 +1427,35 @@ int nsfr_oracle_entropy_total(void* ctx, const double* u, double* out) {
   return NSFR_OK;
 }
 
+/* Conserved totals sum_e sum_q w J u_q[s], s = mass, momentum x3, energy
+ * (DiagnosticRecord totals; Thm 3 drift check SPEC.md:650) */
+int nsfr_oracle_conserved_totals(void* ctx, const double* u, double out5[NS]) {
+  Ctx* c = (Ctx*)ctx;
+  const Ops* o = &c->ops;
+  const int np = c->np, nq = c->nq, nv = c->nv, nsol = c->nsol;
+  const int me[3] = {np, np, np};
+  double tot[NS] = {0.0, 0.0, 0.0, 0.0, 0.0};
+  for (int e = 0; e < c->ne; ++e) {
+    double uq[NS][MAXN * MAXN * MAXN];
+    for (int s = 0; s < NS; ++s)
+      apply_tp(&o->interp, &o->interp, &o->interp, u + ((size_t)e * NS + s) * nsol, me, uq[s]);
+    double pe[NS] = {0.0, 0.0, 0.0, 0.0, 0.0};
+    for (int k = 0; k < nq; ++k)
+      for (int j = 0; j < nq; ++j)
+        for (int i = 0; i < nq; ++i) {
+          const int q = i + nq * (j + nq * k);
+          double w = o->quad.w[i];
+          w *= o->quad.w[j];
+          w *= o->quad.w[k];
+          const double wj = w * c->jac[(size_t)e * nv + q];
+          for (int s = 0; s < NS; ++s) pe[s] += wj * uq[s][q];
+        }
+    for (int s = 0; s < NS; ++s) tot[s] += pe[s];
+  }
+  for (int s = 0; s < NS; ++s) out5[s] = tot[s];
+  return NSFR_OK;
+}
+
 /* ------------------------------------------------------------------------ */
 /* primitive probes for the golden-vector tests                              */
 double nsfr_oracle_log_mean(double a, double b) { return log_mean(a, b); }

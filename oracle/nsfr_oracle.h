@@ -80,6 +80,8 @@ int NSFR_CPU_API(max_wavespeed)(void* ctx, const double* u, double* lam);
 int NSFR_CPU_API(rk4_step)(void* ctx, double* u, double dt);
 int NSFR_CPU_API(l2_error)(void* ctx, const double* u, double t, int case_kind, double out2[2]);
 int NSFR_CPU_API(entropy_total)(void* ctx, const double* u, double* out);
+/* conserved totals sum w J u_q: mass, momentum x3, energy */
+int NSFR_CPU_API(conserved_totals)(void* ctx, const double* u, double out5[5]);
 #endif
 
 #ifdef __cplusplus

@@ -542,6 +542,36 @@ int nsfr_ref_entropy_total(void* ctx, const double* u, double* out) {
   return NSFR_OK;
 }
 
+int nsfr_ref_conserved_totals(void* ctx, const double* u, double out5[5]) {
+  RefCtx& c = *static_cast<RefCtx*>(ctx);
+  const auto& o = c.ops;
+  const int nq = c.nq;
+  const Extents me{c.np, c.np, c.np};
+  std::vector<double> work(4096), uq(kStates * c.nv);
+  double tot[kStates] = {0.0, 0.0, 0.0, 0.0, 0.0};
+  for (int e = 0; e < c.ne; ++e) {
+    const ElementMetrics& em = c.md.elem[global_elem(c, e)];
+    for (int s = 0; s < kStates; ++s)
+      apply_tensor_product(o.basis.interp, o.basis.interp, o.basis.interp,
+                           std::span<const double>(u + (static_cast<size_t>(e) * kStates + s) * c.nsol, c.nsol),
+                           me, std::span<double>(&uq[s * c.nv], c.nv), work);
+    double pe[kStates] = {0.0, 0.0, 0.0, 0.0, 0.0};
+    for (int k = 0; k < nq; ++k)
+      for (int j = 0; j < nq; ++j)
+        for (int i = 0; i < nq; ++i) {
+          const int q = i + nq * (j + nq * k);
+          double w = o.wq[i];
+          w *= o.wq[j];
+          w *= o.wq[k];
+          const double wj = w * em.jac_vol[q];
+          for (int s = 0; s < kStates; ++s) pe[s] += wj * uq[s * c.nv + q];
+        }
+    for (int s = 0; s < kStates; ++s) tot[s] += pe[s];
+  }
+  for (int s = 0; s < kStates; ++s) out5[s] = tot[s];
+  return NSFR_OK;
+}
+
 // primitive probes (golden-vector generation)
 double nsfr_ref_log_mean(double a, double b) { return log_mean(a, b); }
 int nsfr_ref_flux_ec(double g, const double* ul, const double* ur, double* f15) {

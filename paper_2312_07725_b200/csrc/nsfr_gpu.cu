@@ -519,7 +519,7 @@ int nsfr_gpu_create(const nsfr_gpu_setup* setup, nsfr_gpu_ctx** out) {
       alloc(&ctx->d_acc, ns) || alloc(&ctx->d_rhs, ns) || alloc(&ctx->d_utv, 6 * n3) ||
       alloc(&ctx->d_tr, ntr) || alloc(&ctx->d_facc, ntr) || alloc(&ctx->d_cof, 9 * n3) || alloc(&ctx->d_jac, n3) ||
       alloc(&ctx->d_wj, n3) || alloc(&ctx->d_dS, ctx->E) || alloc(&ctx->d_part, 2 * (size_t)ctx->E) ||
-      alloc(&ctx->d_red, 4) || cudaMalloc(&ctx->d_step, sizeof(StepState)) ||
+      alloc(&ctx->d_red, 8) || cudaMalloc(&ctx->d_step, sizeof(StepState)) ||
       cudaMalloc(&ctx->d_err, sizeof(unsigned)) ||
       cudaMallocHost(&ctx->h_step, sizeof(StepState)) || cudaMallocHost(&ctx->h_err, sizeof(unsigned))) {
     ctx->msg = "nsfr_gpu_create: device allocation failed";
@@ -840,6 +840,19 @@ int nsfr_gpu_l2_error(nsfr_gpu_ctx* ctx, int kind, double out2[2]) {
   CK(cudaMemcpy(h, ctx->d_red, sizeof h, cudaMemcpyDeviceToHost));
   out2[0] = std::sqrt(h[0]);
   out2[1] = std::sqrt(h[1]);
+  return NSFR_OK;
+}
+
+int nsfr_gpu_conserved_totals(nsfr_gpu_ctx* ctx, double out5[5]) {
+  if (int rc = sync_check(ctx)) return rc;
+  // per-element partials into d_vol (dead between steps), then fixed-order sums
+  k_totals<<<ctx->E, 128, 0, ctx->st>>>(ctx->d_tab, ctx->d_un, ctx->d_jac, ctx->d_vol, ctx->E);
+  k_reduce<<<1, 1024, 0, ctx->st>>>(ctx->d_vol, ctx->E, NS, ctx->d_red);
+  ctx->launches += 2;
+  CK(cudaGetLastError());
+  if (int rc = allreduce_sum(ctx, ctx->d_red, NS)) return rc;
+  if (int rc = sync_check(ctx)) return rc;
+  CK(cudaMemcpy(out5, ctx->d_red, sizeof(double) * NS, cudaMemcpyDeviceToHost));
   return NSFR_OK;
 }
 

@@ -372,6 +372,35 @@ __global__ void k_reduce(const double* in, int n, int ncomp, double* out) {
   }
 }
 
+// Conserved totals per element: sum_q w J u_q[s] (mass, momentum, energy;
+// SPEC.md:587 DiagnosticRecord, Thm 3 drift SPEC.md:650). Fixed-order sums.
+__global__ void k_totals(const DevTables* tab, const double* u, const double* jac, double* part, int E) {
+  __shared__ double red[NS][128];
+  const DevTables& T = *tab;
+  const int e = blockIdx.x;
+  if (e >= E) return;
+  const int tid = threadIdx.x, nthr = blockDim.x;  // nthr <= 128
+  const int n = T.nq, N3 = n * n * n;
+  double acc[NS] = {0.0, 0.0, 0.0, 0.0, 0.0};
+  for (int q = tid; q < N3; q += nthr) {
+    const int i = q % n, j = (q / n) % n, k = q / (n * n);
+    double w = T.wq[i];
+    w *= T.wq[j];
+    w *= T.wq[k];
+    const double wj = w * jac[(size_t)e * N3 + q];
+#pragma unroll
+    for (int s = 0; s < NS; ++s) acc[s] += wj * u[((size_t)e * NS + s) * N3 + q];
+  }
+#pragma unroll
+  for (int s = 0; s < NS; ++s) red[s][tid] = acc[s];
+  __syncthreads();
+  if (tid < NS) {
+    double t = 0.0;
+    for (int r = 0; r < nthr; ++r) t += red[tid][r];
+    part[(size_t)e * NS + tid] = t;
+  }
+}
+
 // Step bookkeeping: reset lambda, compute dt from lambda.
 struct StepState {
   double t, dt, t_final, cfl, dx;

@@ -118,6 +118,7 @@ def load_library() -> C.CDLL:
         "nsfr_gpu_max_wavespeed": (C.c_int, [V, P]),
         "nsfr_gpu_l2_error": (C.c_int, [V, C.c_int, P]),
         "nsfr_gpu_entropy_change": (C.c_int, [V, P]),
+        "nsfr_gpu_conserved_totals": (C.c_int, [V, P]),
         "nsfr_gpu_time_steps": (C.c_int, [V, C.c_int, C.c_double, P, P]),
         "nsfr_gpu_state_device_ptr": (C.c_void_p, [V]),
         "nsfr_gpu_state_count": (C.c_size_t, [V]),
@@ -357,6 +358,12 @@ class GpuSolver:
         out = np.zeros(1)
         self._check(self.lib.nsfr_gpu_entropy_change(self.ctx, _ptr(out)))
         return float(out[0])
+
+    def conserved_totals(self) -> np.ndarray:
+        """sum w J u over the (global) domain: mass, momentum x3, energy."""
+        out = np.zeros(5)
+        self._check(self.lib.nsfr_gpu_conserved_totals(self.ctx, _ptr(out)))
+        return out
 
     def time_steps(self, nsteps: int, cfl: float = 0.1, per_kernel: bool = False):
         ms = np.zeros(1)

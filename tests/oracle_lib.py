@@ -93,6 +93,7 @@ def load(kind: str) -> tuple[C.CDLL, str]:
             "rk4_step": (C.c_int, [C.c_void_p, P, C.c_double]),
             "l2_error": (C.c_int, [C.c_void_p, P, C.c_double, C.c_int, P]),
             "entropy_total": (C.c_int, [C.c_void_p, P, P]),
+            "conserved_totals": (C.c_int, [C.c_void_p, P, P]),
             "log_mean": (C.c_double, [C.c_double, C.c_double]),
             "flux_ec": (C.c_int, [C.c_double, P, P, P]),
             "roe": (C.c_int, [C.c_double, P, P, P, P]),
@@ -239,6 +240,11 @@ class CpuSolver:
         out = np.zeros(1)
         self._check(self._fn("entropy_total")(self.ctx, ptr(np.ascontiguousarray(u)), ptr(out)))
         return float(out[0])
+
+    def conserved_totals(self, u):
+        out = np.zeros(5)
+        self._check(self._fn("conserved_totals")(self.ctx, ptr(np.ascontiguousarray(u)), ptr(out)))
+        return out
 
     def run(self, u, steps, cfl=0.1, t_final=None, t0=0.0):
         """RK4 driver: dt = cfl*dx/lambda_max from u_n each step, clipped to t_final."""

@@ -224,6 +224,24 @@ def test_fixed_dt_step_matches_oracle():
     assert norm_rel(g.get_state() - u0, uo - u0) < 1e-10
 
 
+@pytest.mark.parametrize("c_plus", [False, True])
+def test_conserved_totals(c_plus):
+    """Device totals sum w J u_q against the oracle, and the Thm 3 drift over 10
+    graph-driven RK4 steps with single-valued face metrics (grid_degree = p)."""
+    c = OC_PLUS[3] if c_plus else 0.0
+    o = CpuSolver("oracle", Config(p=3, m=4, c1d=c, grid_degree=3))
+    g = P().GpuSolver(gpu_cfg(p=3, m=4, c1d=c, grid_degree=3))
+    g.init_case()
+    t0 = g.conserved_totals()
+    np.testing.assert_allclose(t0, o.conserved_totals(g.get_state()), rtol=1e-13, atol=1e-13)
+    g.advance(10)
+    np.testing.assert_allclose(g.conserved_totals(), o.conserved_totals(g.get_state()), rtol=1e-13,
+                               atol=1e-13)
+    drift = np.abs(g.conserved_totals() - t0) / np.maximum(np.abs(t0), 1.0)
+    if not c_plus:
+        assert drift.max() < 1e-12, drift
+
+
 def test_tgv_entropy_conservation():
     """BASELINE configs[3] physics on a small box: EC flux, consistent face
     metrics (grid_degree = p): entropy change at round-off of |U_total|."""

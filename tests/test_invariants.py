@@ -111,6 +111,19 @@ def test_conservation_and_entropy_consistent_metric(roe):
         assert abs(ds) < 1e-11 * abs(s.entropy_total(u))
 
 
+def test_conserved_totals_drift():
+    """Thm 3 / SPEC.md:650: with single-valued face metrics (grid_degree = p)
+    and c_DG (the weight-adjusted inverse is then exact), mass, momentum and
+    energy totals drift by round-off only over RK4 steps, for EC and EC+Roe."""
+    for roe in (False, True):
+        s = CpuSolver("oracle", Config(p=3, m=3, grid_degree=3, roe=roe))
+        u = s.initial_state()
+        t0 = s.conserved_totals(u)
+        u, _ = s.run(u, 5)
+        drift = np.abs(s.conserved_totals(u) - t0) / np.maximum(np.abs(t0), 1.0)
+        assert drift.max() < 1e-12, drift
+
+
 def test_face_metric_mismatch_documented():
     """with grid_degree = p+1 on GL, neighbour face cofactors differ
     by O(1e-3) at p=3 so EC entropy change is O(dC), not round-off."""
