@@ -145,6 +145,14 @@ int nsfr_gpu_entropy_change(nsfr_gpu_ctx* ctx, double* out);
  * x/y/z momentum, energy (DiagnosticRecord totals; Thm 3 drift
  * check SPEC.md:650), allreduced in a fixed order. */
 int nsfr_gpu_conserved_totals(nsfr_gpu_ctx* ctx, double out5[5]);
+/* sum_e sum_q w_q J_q U(u_q), U = -rho s/(gamma-1): the entropy total that
+ * normalises the entropy change. */
+int nsfr_gpu_entropy_total(nsfr_gpu_ctx* ctx, double* out);
+/* Kinetic-energy volume term of the current state (kinetic_energy_change's
+ * volume_term): sum_s v_KE,s . S6 rows of
+ * the EC flux minus the pressure work P~_ij = 1/2 (p_i + p_j) I_d 1/2 (C_i + C_j),
+ * v_KE = (-|v|^2/2, v, 0) at the volume nodes. Round-off for the KEP flux. */
+int nsfr_gpu_ke_volume(nsfr_gpu_ctx* ctx, double* out);
 
 /* Bench helper: time nsteps RK4 steps (t_final unbounded) with CUDA events on
  * the context stream; inputs stay resident in HBM. kernel_ms (optional, [3])

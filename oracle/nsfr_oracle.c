@@ -1288,6 +1288,97 @@ int nsfr_oracle_rhs(void* ctx, const double* u, const double* halo_lo, const dou
 }
 
 /* ------------------------------------------------------------------------ */
+/* Kinetic-energy volume term (SPEC.md:602-609 kinetic_energy_change volume
+ * term): sum_s v_KE,s . [(W D - D^T W) o (F~ - P~)] 1 over
+ * the volume nodes, i.e. the S6 rows (0.5 skew, D2) of the EC flux minus the
+ * pressure work P~_ij = 1/2 (p_i + p_j) I_d 1/2 (C_i + C_j), dotted with the
+ * kinetic-energy variables v_KE = (-|v|^2/2, v, 0) of the same volume states
+ * (chi v_hat_KE = v_KE at the nodes since chi Pi = I). Zero to round-off for
+ * the KEP Ranocha flux, per element. */
+typedef struct {
+  Ctx* c;
+  double* part;
+} KeArg;
+
+static void ke_elem(void* argp, int e) {
+  KeArg* A = (KeArg*)argp;
+  Ctx* c = A->c;
+  const Ops* o = &c->ops;
+  const double g = c->cfg.gamma;
+  const int n = c->nq, nv = c->nv;
+  const double* utv = c->ut_vol + (size_t)e * NS * nv;
+  const double* C = c->cof + (size_t)e * nv * 9;
+  double vol[NS * MAXN * MAXN * MAXN];
+  memset(vol, 0, sizeof(double) * NS * nv);
+  double fl[3][NS];
+  for (int dir = 0; dir < 3; ++dir) {
+    const int stride = (dir == 0) ? 1 : (dir == 1 ? n : n * n);
+    for (int t2 = 0; t2 < n; ++t2)
+      for (int t1 = 0; t1 < n; ++t1) {
+        const int base = (dir == 0) ? n * (t1 + n * t2) : (dir == 1 ? t1 + n * n * t2 : t1 + n * t2);
+        const double wt = o->quad.w[t1] * o->quad.w[t2];
+        for (int a = 0; a < n; ++a) {
+          const int ia = base + a * stride;
+          for (int b = a + 1; b < n; ++b) {
+            const double qab = OP(o->half_skew, a, b) - OP(o->half_skew, b, a);
+            if (qab == 0.0) continue;
+            const int ib = base + b * stride;
+            double ui[NS], uj[NS], f[NS];
+            for (int s = 0; s < NS; ++s) {
+              ui[s] = utv[s * nv + ia];
+              uj[s] = utv[s * nv + ib];
+            }
+            if (flux_ec(g, ui, uj, fl)) {
+              c->err[e] = NSFR_E_INADMISSIBLE;
+              return;
+            }
+            const double pbar = 0.5 * (pressure(g, ui) + pressure(g, uj));
+            for (int k = 0; k < 3; ++k) fl[k][1 + k] -= pbar; /* F~ - P~ */
+            const double cm0 = 0.5 * (C[9 * ia + 0 + dir] + C[9 * ib + 0 + dir]);
+            const double cm1 = 0.5 * (C[9 * ia + 3 + dir] + C[9 * ib + 3 + dir]);
+            const double cm2 = 0.5 * (C[9 * ia + 6 + dir] + C[9 * ib + 6 + dir]);
+            for (int s = 0; s < NS; ++s) f[s] = fl[0][s] * cm0 + fl[1][s] * cm1 + fl[2][s] * cm2;
+            const double cc = wt * qab;
+            for (int s = 0; s < NS; ++s) {
+              vol[s * nv + ia] += cc * f[s];
+              vol[s * nv + ib] -= cc * f[s];
+            }
+          }
+        }
+      }
+  }
+  double acc = 0.0;
+  for (int q = 0; q < nv; ++q) {
+    const double r = utv[q];
+    const double vx = utv[nv + q] / r, vy = utv[2 * nv + q] / r, vz = utv[3 * nv + q] / r;
+    acc += -0.5 * (vx * vx + vy * vy + vz * vz) * vol[q] + vx * vol[nv + q] + vy * vol[2 * nv + q] +
+           vz * vol[3 * nv + q];
+  }
+  A->part[e] = acc;
+}
+
+int nsfr_oracle_ke_volume(void* ctx, const double* u, double* out) {
+  Ctx* c = (Ctx*)ctx;
+  int rc = project_all(c, u);
+  if (rc) return rc;
+  double* part = calloc(c->ne, sizeof(double));
+  KeArg A = {c, part};
+  parallel_for(c->ne, c->cfg.workers, ke_elem, &A);
+  double acc = 0.0;
+  for (int e = 0; e < c->ne; ++e) {
+    if (c->err[e]) {
+      set_err(c, "ke_volume: inadmissible state in element %d", e);
+      free(part);
+      return c->err[e];
+    }
+    acc += part[e];
+  }
+  free(part);
+  *out = acc;
+  return NSFR_OK;
+}
+
+/* ------------------------------------------------------------------------ */
 /* adaptive dt wavespeed: max over volume nodes of chi u_hat */
 int nsfr_oracle_max_wavespeed(void* ctx, const double* u, double* lam) {
   Ctx* c = (Ctx*)ctx;

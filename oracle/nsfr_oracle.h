@@ -82,6 +82,9 @@ int NSFR_CPU_API(l2_error)(void* ctx, const double* u, double t, int case_kind, 
 int NSFR_CPU_API(entropy_total)(void* ctx, const double* u, double* out);
 /* conserved totals sum w J u_q: mass, momentum x3, energy */
 int NSFR_CPU_API(conserved_totals)(void* ctx, const double* u, double out5[5]);
+/* kinetic-energy volume term sum v_KE . S6 rows of (EC flux - pressure work)
+ * (SPEC.md:602-609); ~0 for the KEP flux */
+int NSFR_CPU_API(ke_volume)(void* ctx, const double* u, double* out);
 #endif
 
 #ifdef __cplusplus

@@ -418,6 +418,59 @@ int nsfr_ref_rhs(void* ctx, const double* u, const double* halo_lo, const double
   return do_rhs(c, u, halo_lo, halo_hi, dudt, entropy_change);
 }
 
+// kinetic-energy volume term: hadamard_sumfac_volume (sumfac.hpp:48-94, 0.5 skew)
+// of the reference flux minus the pressure work, dotted with v_KE
+int nsfr_ref_ke_volume(void* ctx, const double* u, double* out) {
+  RefCtx& c = *static_cast<RefCtx*>(ctx);
+  if (int rc = project_all(c, u)) return rc;
+  const int nv = c.nv, nq = c.nq;
+  const Extents qe{nq, nq, nq};
+  const std::array<const Operator1D*, 3> hs{&c.half_skew, &c.half_skew, &c.half_skew};
+  const std::span<const double> w(c.ops.wq);
+  const std::array<std::span<const double>, 3> w3{w, w, w};
+  std::vector<double> part(c.ne, 0.0);
+  std::atomic<int> bad{-1};
+  parallel_for(c.ne, c.cfg.workers, [&](int e) {
+    const ElementMetrics& em = c.md.elem[global_elem(c, e)];
+    const double* utv = &c.ut_vol[static_cast<size_t>(e) * kStates * nv];
+    std::vector<double> vol(kStates * nv, 0.0);
+    auto provider = [&](int i, int j, int dir, double* o5) {
+      const State ui = load(utv, nv, i), uj = load(utv, nv, j);
+      Flux F = two_point_flux(c.gas, TwoPointFluxKind::ChandrashekarRanochaFix, ui, uj);
+      const double pbar = 0.5 * (pressure(c.gas, ui) + pressure(c.gas, uj));
+      for (int k = 0; k < 3; ++k) F[k][1 + k] -= pbar;
+      const double* Ci = em.cof_at(i);
+      const double* Cj = em.cof_at(j);
+      const double cm0 = 0.5 * (Ci[0 + dir] + Cj[0 + dir]);
+      const double cm1 = 0.5 * (Ci[3 + dir] + Cj[3 + dir]);
+      const double cm2 = 0.5 * (Ci[6 + dir] + Cj[6 + dir]);
+      for (int s = 0; s < kStates; ++s) o5[s] = F[0][s] * cm0 + F[1][s] * cm1 + F[2][s] * cm2;
+    };
+    try {
+      hadamard_sumfac_volume(hs, w3, qe, kStates, provider, vol, nullptr);
+    } catch (const std::exception&) {
+      bad = e;
+      return;
+    }
+    double acc = 0.0;
+    for (int q = 0; q < nv; ++q) {
+      const double r = utv[q];
+      const double vx = utv[nv + q] / r, vy = utv[2 * nv + q] / r, vz = utv[3 * nv + q] / r;
+      acc += -0.5 * (vx * vx + vy * vy + vz * vz) * vol[q] + vx * vol[nv + q] + vy * vol[2 * nv + q] +
+             vz * vol[3 * nv + q];
+    }
+    part[e] = acc;
+  });
+  if (bad >= 0) {
+    c.msg = "ke_volume: inadmissible state";
+    return NSFR_E_INADMISSIBLE;
+  }
+  double acc = 0.0;
+  for (int e = 0; e < c.ne; ++e) acc += part[e];
+  *out = acc;
+  return NSFR_OK;
+}
+
 int nsfr_ref_max_wavespeed(void* ctx, const double* u, double* lam) {
   RefCtx& c = *static_cast<RefCtx*>(ctx);
   const auto& o = c.ops;

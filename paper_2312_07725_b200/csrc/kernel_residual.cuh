@@ -108,7 +108,9 @@ __device__ __forceinline__ void res_prefetch(const ResParams& P, int e0, int tid
   }
 }
 
-template <int N>
+// KE = true: the kinetic-energy diagnostic's volume rows (S6 only, flux minus
+// pressure work); no surface terms, no face rows.
+template <int N, bool KE>
 __device__ __forceinline__ void res_batch(const ResParams& P, const ResOps<N>& O, int e0, double* sm) {
   using Cfg = ResCfg<N>;
   constexpr int N2 = Cfg::N2, N3 = Cfg::N3, EPB = Cfg::EPB, LINES = Cfg::LINES;
@@ -164,7 +166,7 @@ __device__ __forceinline__ void res_batch(const ResParams& P, const ResOps<N>& O
         const PrimH pb{Pd[ib], Pd[N3 + ib], Pd[2 * N3 + ib], Pd[3 * N3 + ib],
                        Pd[4 * N3 + ib], Pd[5 * N3 + ib]};
         double f[NS];
-        d_flux_h(pa, pb, ca0 + Ch[(0 + dir) * N3 + ib], ca1 + Ch[(3 + dir) * N3 + ib],
+        d_flux_h<KE>(pa, pb, ca0 + Ch[(0 + dir) * N3 + ib], ca1 + Ch[(3 + dir) * N3 + ib],
                           ca2 + Ch[(6 + dir) * N3 + ib], f);
         const double c = wt * O.q[a * N + bb];
 #pragma unroll
@@ -178,7 +180,7 @@ __device__ __forceinline__ void res_batch(const ResParams& P, const ResOps<N>& O
     }
     // S7 hybrid surface pairs + S8 face flux for the two faces this line pierces
 #pragma unroll 1
-    for (int side = 0; side < 2; ++side) {
+    for (int side = 0; side < (KE ? 0 : 2); ++side) {
       const int f = 2 * dir + side;
       const double sign = side ? 1.0 : -1.0;
       const int k = t1 + N * t2;
@@ -259,7 +261,7 @@ __device__ __forceinline__ void res_batch(const ResParams& P, const ResOps<N>& O
     }
   }
   // face rows straight from registers: facc[e][dir][s][side][k]
-  if (lb < nb) {
+  if (!KE && lb < nb) {
     const int k = (lrem % N) + N * (lrem / N);
     double* fa = P.facc + ((size_t)(e0 + lb) * 3 + ldir) * 10 * N2 + k;
 #pragma unroll
@@ -284,14 +286,14 @@ __device__ __forceinline__ void res_batch(const ResParams& P, const ResOps<N>& O
 // lockstep measured slower). Each CTA prefetches into L2 the batch of the CTA
 // `ahead` = #resident CTAs later, which the block scheduler starts about when
 // this one retires, so that CTA's staging loads hit L2.
-template <int N>
+template <int N, bool KE = false>
 __global__ void __launch_bounds__(ResCfg<N>::THREADS, ResCfg<N>::MINB)
     k_residual(ResParams P, ResOps<N> O, int ahead) {
   extern __shared__ __align__(128) double sm[];
   constexpr int EPB = ResCfg<N>::EPB;
   const long long pe = (static_cast<long long>(blockIdx.x) + ahead) * EPB;
   if (pe < P.E) res_prefetch<N>(P, static_cast<int>(pe), threadIdx.x);
-  res_batch<N>(P, O, blockIdx.x * EPB, sm);
+  res_batch<N, KE>(P, O, blockIdx.x * EPB, sm);
 }
 
 }  // namespace nsfr_b200

@@ -83,6 +83,7 @@ int set_attrs(nsfr_gpu_ctx* ctx) {
   if (Resident<N>::res) return NSFR_OK;
   CK(cudaFuncSetAttribute(k_project<N>, cudaFuncAttributeMaxDynamicSharedMemorySize, ProjCfg<N>::SMEM));
   CK(cudaFuncSetAttribute(k_residual<N>, cudaFuncAttributeMaxDynamicSharedMemorySize, ResCfg<N>::SMEM));
+  CK(cudaFuncSetAttribute(k_residual<N, true>, cudaFuncAttributeMaxDynamicSharedMemorySize, ResCfg<N>::SMEM));
   CK(cudaFuncSetAttribute(k_update<N>, cudaFuncAttributeMaxDynamicSharedMemorySize, UpdCfg<N>::SMEM));
   int sms = 0, bp = 0, br = 0, bu = 0;
   CK(cudaDeviceGetAttribute(&sms, cudaDevAttrMultiProcessorCount, ctx->s.device));
@@ -211,7 +212,7 @@ int launch_project(nsfr_gpu_ctx* ctx, const double* u, bool want_lam) {
 }
 
 template <int N>
-int launch_residual(nsfr_gpu_ctx* ctx) {
+int launch_residual(nsfr_gpu_ctx* ctx, bool ke) {
   ResParams P{};
   P.ut_vol = ctx->d_utv;
   P.traces = ctx->d_tr;
@@ -229,8 +230,12 @@ int launch_residual(nsfr_gpu_ctx* ctx) {
   if (int rc = set_attrs<N>(ctx)) return rc;
   const int grid = (ctx->E + ResCfg<N>::EPB - 1) / ResCfg<N>::EPB;
   ev_begin(ctx, 2);
-  k_residual<N><<<grid, ResCfg<N>::THREADS, ResCfg<N>::SMEM, ctx->st>>>(P, res_ops<N>(ctx->htab),
-                                                                         Resident<N>::res);
+  if (ke)
+    k_residual<N, true><<<grid, ResCfg<N>::THREADS, ResCfg<N>::SMEM, ctx->st>>>(P, res_ops<N>(ctx->htab),
+                                                                              Resident<N>::res);
+  else
+    k_residual<N><<<grid, ResCfg<N>::THREADS, ResCfg<N>::SMEM, ctx->st>>>(P, res_ops<N>(ctx->htab),
+                                                                           Resident<N>::res);
   ev_end(ctx);
   ++ctx->launches;
   CK(cudaGetLastError());
@@ -277,7 +282,7 @@ int launch_update(nsfr_gpu_ctx* ctx, int stage, bool entropy) {
   return NSFR_E_DIM
 
 int project(nsfr_gpu_ctx* ctx, const double* u, bool lam) { NSFR_DISPATCH(launch_project, (ctx, u, lam)); }
-int residual(nsfr_gpu_ctx* ctx) { NSFR_DISPATCH(launch_residual, (ctx)); }
+int residual(nsfr_gpu_ctx* ctx, bool ke = false) { NSFR_DISPATCH(launch_residual, (ctx, ke)); }
 int update(nsfr_gpu_ctx* ctx, int stage, bool entropy) { NSFR_DISPATCH(launch_update, (ctx, stage, entropy)); }
 
 // z-face halo exchange with the two slab neighbours
@@ -843,16 +848,48 @@ int nsfr_gpu_l2_error(nsfr_gpu_ctx* ctx, int kind, double out2[2]) {
   return NSFR_OK;
 }
 
-int nsfr_gpu_conserved_totals(nsfr_gpu_ctx* ctx, double out5[5]) {
+// mass, momentum, energy and entropy-function totals of the current state
+static int totals(nsfr_gpu_ctx* ctx, double out6[NTOT]) {
   if (int rc = sync_check(ctx)) return rc;
   // per-element partials into d_vol (dead between steps), then fixed-order sums
-  k_totals<<<ctx->E, 128, 0, ctx->st>>>(ctx->d_tab, ctx->d_un, ctx->d_jac, ctx->d_vol, ctx->E);
-  k_reduce<<<1, 1024, 0, ctx->st>>>(ctx->d_vol, ctx->E, NS, ctx->d_red);
+  k_totals<<<ctx->E, 128, 0, ctx->st>>>(ctx->d_tab, ctx->d_un, ctx->d_jac, ctx->s.gamma, ctx->d_vol,
+                                         ctx->E);
+  k_reduce<<<1, 1024, 0, ctx->st>>>(ctx->d_vol, ctx->E, NTOT, ctx->d_red);
   ctx->launches += 2;
   CK(cudaGetLastError());
-  if (int rc = allreduce_sum(ctx, ctx->d_red, NS)) return rc;
+  if (int rc = allreduce_sum(ctx, ctx->d_red, NTOT)) return rc;
   if (int rc = sync_check(ctx)) return rc;
-  CK(cudaMemcpy(out5, ctx->d_red, sizeof(double) * NS, cudaMemcpyDeviceToHost));
+  CK(cudaMemcpy(out6, ctx->d_red, sizeof(double) * NTOT, cudaMemcpyDeviceToHost));
+  return NSFR_OK;
+}
+
+int nsfr_gpu_conserved_totals(nsfr_gpu_ctx* ctx, double out5[5]) {
+  double t[NTOT];
+  if (int rc = totals(ctx, t)) return rc;
+  for (int s = 0; s < NS; ++s) out5[s] = t[s];
+  return NSFR_OK;
+}
+
+int nsfr_gpu_entropy_total(nsfr_gpu_ctx* ctx, double* out) {
+  double t[NTOT];
+  if (int rc = totals(ctx, t)) return rc;
+  *out = t[NS];
+  return NSFR_OK;
+}
+
+int nsfr_gpu_ke_volume(nsfr_gpu_ctx* ctx, double* out) {
+  // volume rows of (flux - pressure work) for the projection of u_n, then
+  // sum v_KE . rows; partials go to d_rhs (the rows occupy d_vol)
+  if (int rc = project_state(ctx)) return rc;
+  if (int rc = residual(ctx, true)) return rc;
+  k_ke_dot<<<ctx->E, 128, 0, ctx->st>>>(ctx->d_un, ctx->d_vol, static_cast<int>(nsol(ctx)), ctx->d_rhs,
+                                         ctx->E);
+  k_reduce<<<1, 1024, 0, ctx->st>>>(ctx->d_rhs, ctx->E, 1, ctx->d_red);
+  ctx->launches += 2;
+  CK(cudaGetLastError());
+  if (int rc = allreduce_sum(ctx, ctx->d_red, 1)) return rc;
+  if (int rc = sync_check(ctx)) return rc;
+  CK(cudaMemcpy(out, ctx->d_red, sizeof(double), cudaMemcpyDeviceToHost));
   return NSFR_OK;
 }
 

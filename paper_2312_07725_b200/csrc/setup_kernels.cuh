@@ -372,32 +372,68 @@ __global__ void k_reduce(const double* in, int n, int ncomp, double* out) {
   }
 }
 
-// Conserved totals per element: sum_q w J u_q[s] (mass, momentum, energy;
-// SPEC.md:587 DiagnosticRecord, Thm 3 drift SPEC.md:650). Fixed-order sums.
-__global__ void k_totals(const DevTables* tab, const double* u, const double* jac, double* part, int E) {
-  __shared__ double red[NS][128];
+// Totals per element: sum_q w J u_q[s] (mass, momentum, energy; SPEC.md:587
+// DiagnosticRecord, Thm 3 drift SPEC.md:650) and sum_q w J U(u_q) with the
+// entropy function U = -rho s/(gamma-1) (the |U_total| normaliser of
+// SPEC.md:654). part[E][6]; fixed-order sums.
+constexpr int NTOT = NS + 1;
+__global__ void k_totals(const DevTables* tab, const double* u, const double* jac, double gamma,
+                         double* part, int E) {
+  __shared__ double red[NTOT][128];
   const DevTables& T = *tab;
   const int e = blockIdx.x;
   if (e >= E) return;
   const int tid = threadIdx.x, nthr = blockDim.x;  // nthr <= 128
   const int n = T.nq, N3 = n * n * n;
-  double acc[NS] = {0.0, 0.0, 0.0, 0.0, 0.0};
+  double acc[NTOT] = {0.0, 0.0, 0.0, 0.0, 0.0, 0.0};
   for (int q = tid; q < N3; q += nthr) {
     const int i = q % n, j = (q / n) % n, k = q / (n * n);
     double w = T.wq[i];
     w *= T.wq[j];
     w *= T.wq[k];
     const double wj = w * jac[(size_t)e * N3 + q];
+    double uu[NS];
 #pragma unroll
-    for (int s = 0; s < NS; ++s) acc[s] += wj * u[((size_t)e * NS + s) * N3 + q];
+    for (int s = 0; s < NS; ++s) {
+      uu[s] = u[((size_t)e * NS + s) * N3 + q];
+      acc[s] += wj * uu[s];
+    }
+    const double sp = log(d_pressure(gamma, uu)) - gamma * log(uu[0]);
+    acc[NS] += wj * (-uu[0] * sp / (gamma - 1.0));
   }
 #pragma unroll
-  for (int s = 0; s < NS; ++s) red[s][tid] = acc[s];
+  for (int s = 0; s < NTOT; ++s) red[s][tid] = acc[s];
   __syncthreads();
-  if (tid < NS) {
+  if (tid < NTOT) {
     double t = 0.0;
     for (int r = 0; r < nthr; ++r) t += red[tid][r];
-    part[(size_t)e * NS + tid] = t;
+    part[(size_t)e * NTOT + tid] = t;
+  }
+}
+
+// Kinetic-energy volume term per element: sum_q v_KE(u_q) . vol_q with the
+// volume rows of k_residual<N, true> (flux minus pressure work, S6 only) and
+// v_KE = (-|v|^2/2, v_x, v_y, v_z, 0). Fixed-order sums.
+__global__ void k_ke_dot(const double* u, const double* vol, int N3, double* part, int E) {
+  __shared__ double red[128];
+  const int e = blockIdx.x;
+  if (e >= E) return;
+  const int tid = threadIdx.x, nthr = blockDim.x;  // nthr <= 128
+  const double* ue = u + (size_t)e * NS * N3;
+  const double* ve = vol + (size_t)e * NS * N3;
+  double acc = 0.0;
+  for (int q = tid; q < N3; q += nthr) {
+    const double r = ue[q];
+    const double vx = ue[N3 + q] / r, vy = ue[2 * N3 + q] / r, vz = ue[3 * N3 + q] / r;
+    acc += -0.5 * (vx * vx + vy * vy + vz * vz) * ve[q] + vx * ve[N3 + q] + vy * ve[2 * N3 + q] +
+           vz * ve[3 * N3 + q];
+  }
+  red[tid] = acc;
+  __syncthreads();
+  if (tid == 0) {
+    double t = 0.0;
+    for (int i = 0; i < nthr; ++i) t += red[i];
+    part[e] = t;
   }
 }
 

@@ -119,6 +119,8 @@ def load_library() -> C.CDLL:
         "nsfr_gpu_l2_error": (C.c_int, [V, C.c_int, P]),
         "nsfr_gpu_entropy_change": (C.c_int, [V, P]),
         "nsfr_gpu_conserved_totals": (C.c_int, [V, P]),
+        "nsfr_gpu_entropy_total": (C.c_int, [V, P]),
+        "nsfr_gpu_ke_volume": (C.c_int, [V, P]),
         "nsfr_gpu_time_steps": (C.c_int, [V, C.c_int, C.c_double, P, P]),
         "nsfr_gpu_state_device_ptr": (C.c_void_p, [V]),
         "nsfr_gpu_state_count": (C.c_size_t, [V]),
@@ -357,6 +359,18 @@ class GpuSolver:
     def entropy_change(self) -> float:
         out = np.zeros(1)
         self._check(self.lib.nsfr_gpu_entropy_change(self.ctx, _ptr(out)))
+        return float(out[0])
+
+    def entropy_total(self) -> float:
+        """sum w J U(u) with U = -rho s/(gamma-1) (entropy-change normaliser)."""
+        out = np.zeros(1)
+        self._check(self.lib.nsfr_gpu_entropy_total(self.ctx, _ptr(out)))
+        return float(out[0])
+
+    def ke_volume(self) -> float:
+        """Kinetic-energy volume term (flux minus pressure work, S6 rows . v_KE)."""
+        out = np.zeros(1)
+        self._check(self.lib.nsfr_gpu_ke_volume(self.ctx, _ptr(out)))
         return float(out[0])
 
     def conserved_totals(self) -> np.ndarray:

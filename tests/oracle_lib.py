@@ -94,6 +94,7 @@ def load(kind: str) -> tuple[C.CDLL, str]:
             "l2_error": (C.c_int, [C.c_void_p, P, C.c_double, C.c_int, P]),
             "entropy_total": (C.c_int, [C.c_void_p, P, P]),
             "conserved_totals": (C.c_int, [C.c_void_p, P, P]),
+            "ke_volume": (C.c_int, [C.c_void_p, P, P]),
             "log_mean": (C.c_double, [C.c_double, C.c_double]),
             "flux_ec": (C.c_int, [C.c_double, P, P, P]),
             "roe": (C.c_int, [C.c_double, P, P, P, P]),
@@ -245,6 +246,11 @@ class CpuSolver:
         out = np.zeros(5)
         self._check(self._fn("conserved_totals")(self.ctx, ptr(np.ascontiguousarray(u)), ptr(out)))
         return out
+
+    def ke_volume(self, u):
+        out = np.zeros(1)
+        self._check(self._fn("ke_volume")(self.ctx, ptr(np.ascontiguousarray(u)), ptr(out)))
+        return float(out[0])
 
     def run(self, u, steps, cfl=0.1, t_final=None, t0=0.0):
         """RK4 driver: dt = cfl*dx/lambda_max from u_n each step, clipped to t_final."""

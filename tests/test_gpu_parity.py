@@ -234,12 +234,29 @@ def test_conserved_totals(c_plus):
     g.init_case()
     t0 = g.conserved_totals()
     np.testing.assert_allclose(t0, o.conserved_totals(g.get_state()), rtol=1e-13, atol=1e-13)
+    assert g.entropy_total() == pytest.approx(o.entropy_total(g.get_state()), rel=1e-13)
     g.advance(10)
     np.testing.assert_allclose(g.conserved_totals(), o.conserved_totals(g.get_state()), rtol=1e-13,
                                atol=1e-13)
     drift = np.abs(g.conserved_totals() - t0) / np.maximum(np.abs(t0), 1.0)
     if not c_plus:
         assert drift.max() < 1e-12, drift
+
+
+@pytest.mark.parametrize("quad", [0, 1])
+def test_ke_volume_term(quad):
+    """Kinetic-energy volume term on the device: round-off, like the oracle's,
+    at the TGV state and off equilibrium."""
+    o = CpuSolver("oracle", Config(p=4, m=3, quad_kind=quad, case="tgv", roe=False))
+    g = P().GpuSolver(gpu_cfg(p=4, m=3, quad_kind=quad, case="tgv", roe=False))
+    g.init_case()
+    u = g.get_state()
+    rng = np.random.default_rng(3)
+    for x in (u, u * (1 + 1e-3 * rng.uniform(-1, 1, u.shape))):
+        g.set_state(x)
+        kg, ko = g.ke_volume(), o.ke_volume(x)
+        assert abs(kg) < 1e-11 and abs(ko) < 1e-11, (kg, ko)
+    assert np.isfinite(g.rhs()).all()  # the context still steps after the diagnostic
 
 
 def test_tgv_entropy_conservation():

@@ -124,6 +124,19 @@ def test_conserved_totals_drift():
         assert drift.max() < 1e-12, drift
 
 
+@pytest.mark.parametrize("quad", [0, 1])
+def test_ke_volume_term_vanishes(quad):
+    """PAPER.md:1811-1822 / SPEC.md:605: the volume change in kinetic energy
+    without pressure work is zero to machine precision for GL and LGL nodes
+    (the Ranocha flux is kinetic-energy preserving), also off equilibrium."""
+    s = CpuSolver("oracle", Config(p=3, m=3, quad_kind=quad, case="tgv", roe=False))
+    u = s.initial_state()
+    rng = np.random.default_rng(3)
+    up = u * (1 + 1e-3 * rng.uniform(-1, 1, u.shape))
+    for x in (u, up):
+        assert abs(s.ke_volume(x)) < 1e-11
+
+
 def test_face_metric_mismatch_documented():
     """with grid_degree = p+1 on GL, neighbour face cofactors differ
     by O(1e-3) at p=3 so EC entropy change is O(dC), not round-off."""

@@ -43,6 +43,7 @@ def test_oracle_matches_reference(cfg):
     np.testing.assert_allclose(o.l2_sq(u, 0.0), r.l2_sq(u, 0.0), rtol=1e-14, atol=1e-28)
     assert o.entropy_total(u) == pytest.approx(r.entropy_total(u), rel=1e-14)
     np.testing.assert_array_equal(o.conserved_totals(u), r.conserved_totals(u))
+    assert o.ke_volume(u) == r.ke_volume(u)
 
 
 def test_oracle_rk4_matches_reference():
