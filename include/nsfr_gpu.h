@@ -117,6 +117,11 @@ int nsfr_gpu_get_metrics(nsfr_gpu_ctx* ctx, double* jac, double* cof);
 
 int nsfr_gpu_set_state(nsfr_gpu_ctx* ctx, const double* u);
 int nsfr_gpu_get_state(nsfr_gpu_ctx* ctx, double* u);
+/* The solver's own representation, u at the volume quadrature nodes
+ * (u_q = chi^3 u_hat, same [e][5][nq^3] layout), copied without conversion:
+ * a bit-exact restart (checkpoints) where set/get_state round trips to ~1 ulp. */
+int nsfr_gpu_set_state_q(nsfr_gpu_ctx* ctx, const double* uq);
+int nsfr_gpu_get_state_q(nsfr_gpu_ctx* ctx, double* uq);
 int nsfr_gpu_init_case(nsfr_gpu_ctx* ctx, int case_kind);
 int nsfr_gpu_set_time(nsfr_gpu_ctx* ctx, double t);
 int nsfr_gpu_get_time(nsfr_gpu_ctx* ctx, double* t);

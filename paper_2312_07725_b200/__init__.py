@@ -6,7 +6,11 @@ ABI of include/nsfr_gpu.h); this package is its Python mirror.
 from .solver import (C_PLUS, CASES, ConfigError, DeviceError, DimensionError, GpuSolver,
                      InvalidMeshError, NsfrError, SolverConfig, StepFailureError, halo_plan,
                      load_library, measure_fp64_peak, nccl_unique_id)
+from .runio import (DiagnosticsCSV, load_checkpoint, read_checkpoint, read_diagnostics,
+                    run_simulation, write_checkpoint)
 
 __all__ = ["C_PLUS", "CASES", "ConfigError", "DeviceError", "DimensionError", "GpuSolver",
            "InvalidMeshError", "NsfrError", "SolverConfig", "StepFailureError", "halo_plan",
-           "load_library", "measure_fp64_peak", "nccl_unique_id"]
+           "load_library", "measure_fp64_peak", "nccl_unique_id", "DiagnosticsCSV",
+           "load_checkpoint", "read_checkpoint", "read_diagnostics", "run_simulation",
+           "write_checkpoint"]

@@ -681,6 +681,19 @@ int nsfr_gpu_get_state(nsfr_gpu_ctx* ctx, double* u) {
   return NSFR_OK;
 }
 
+int nsfr_gpu_set_state_q(nsfr_gpu_ctx* ctx, const double* uq) {
+  ctx->proj_valid = false;
+  CK(cudaMemcpyAsync(ctx->d_un, uq, sizeof(double) * state_count(ctx), cudaMemcpyHostToDevice, ctx->st));
+  CK(cudaStreamSynchronize(ctx->st));
+  return NSFR_OK;
+}
+
+int nsfr_gpu_get_state_q(nsfr_gpu_ctx* ctx, double* uq) {
+  CK(cudaMemcpyAsync(uq, ctx->d_un, sizeof(double) * state_count(ctx), cudaMemcpyDeviceToHost, ctx->st));
+  CK(cudaStreamSynchronize(ctx->st));
+  return NSFR_OK;
+}
+
 int nsfr_gpu_init_case(nsfr_gpu_ctx* ctx, int kind) {
   const int g = ctx->tab.g, np = ctx->N, G3 = g * g * g, S3 = np * np * np;
   const int M = std::max(g, np), M3 = M * M * M;

@@ -120,6 +120,8 @@ def load_library() -> C.CDLL:
         "nsfr_gpu_entropy_change": (C.c_int, [V, P]),
         "nsfr_gpu_conserved_totals": (C.c_int, [V, P]),
         "nsfr_gpu_entropy_total": (C.c_int, [V, P]),
+        "nsfr_gpu_set_state_q": (C.c_int, [V, P]),
+        "nsfr_gpu_get_state_q": (C.c_int, [V, P]),
         "nsfr_gpu_ke_volume": (C.c_int, [V, P]),
         "nsfr_gpu_time_steps": (C.c_int, [V, C.c_int, C.c_double, P, P]),
         "nsfr_gpu_state_device_ptr": (C.c_void_p, [V]),
@@ -310,6 +312,18 @@ class GpuSolver:
 
     def init_case(self, case: str | None = None):
         self._check(self.lib.nsfr_gpu_init_case(self.ctx, CASES[case or self.cfg.case]))
+
+    def set_state_q(self, uq: np.ndarray):
+        """Upload the solver's own representation (u at the volume quadrature nodes)."""
+        uq = np.ascontiguousarray(uq, dtype=np.float64)
+        assert uq.shape == self.state_shape, (uq.shape, self.state_shape)
+        self._check(self.lib.nsfr_gpu_set_state_q(self.ctx, _ptr(uq)))
+
+    def get_state_q(self) -> np.ndarray:
+        """u at the volume quadrature nodes, exactly as the solver carries it."""
+        uq = np.zeros(self.state_shape)
+        self._check(self.lib.nsfr_gpu_get_state_q(self.ctx, _ptr(uq)))
+        return uq
 
     def set_time(self, t: float):
         self._check(self.lib.nsfr_gpu_set_time(self.ctx, t))
