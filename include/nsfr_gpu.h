@@ -86,7 +86,8 @@ typedef struct nsfr_gpu_setup {
   const double* jac_vol;  /* [e_local][nq^3]     or NULL: built on the device */
   const double* cof_vol;  /* [e_local][nq^3][9]  or NULL */
   /* multi-GPU: an NCCL unique id from nsfr_gpu_nccl_unique_id on rank 0,
-   * broadcast by the caller; NULL for a single rank */
+   * broadcast by the caller; NULL for a single rank, or with nranks > 1 for
+   * external halo transport (see nsfr_gpu_halo_buffers) */
   const void* nccl_id;
   int rank, nranks;
 } nsfr_gpu_setup;
@@ -168,6 +169,28 @@ int nsfr_gpu_time_steps(nsfr_gpu_ctx* ctx, int nsteps, double cfl, double* step_
 
 /* FP64 pipe peak of `device` in TFLOP/s (DFMA loop; roofline denominator). */
 int nsfr_gpu_measure_fp64_peak(int device, double* tflops);
+
+/* ---- Stage-level driving and external halo transport ----------------------
+ * A context created with nranks > 1 but nccl_id == NULL exchanges no data
+ * itself: the caller moves the z-halo planes (e.g. over MPI, or between two
+ * contexts in a test). Each plane is [m*m][5][nq^2] (halo_plan.count doubles):
+ * rank r's send_lo goes to rank r-1's recv_hi and its send_hi to rank r+1's
+ * recv_lo (periodic). The driving sequence is
+ *   nsfr_gpu_project;  [swap];  nsfr_gpu_residual            (one RHS), or
+ *   nsfr_gpu_project;  for s = 1..4: { [swap]; nsfr_gpu_stage(s, dt) }
+ * with dt = cfl dx / max over ranks of nsfr_gpu_max_wavespeed. Stage 4 leaves
+ * the projection (and send planes) of u_{n+1}, so the next step starts with a
+ * swap. In NCCL mode the same calls exchange internally. */
+int nsfr_gpu_halo_buffers(nsfr_gpu_ctx* ctx, double** send_lo, double** send_hi, double** recv_lo,
+                          double** recv_hi);
+int nsfr_gpu_halo_get(nsfr_gpu_ctx* ctx, double* send_lo, double* send_hi);
+int nsfr_gpu_halo_set(nsfr_gpu_ctx* ctx, const double* recv_lo, const double* recv_hi);
+/* Entropy projection of the current state (faces, volume primitives, send planes, lambda). */
+int nsfr_gpu_project(nsfr_gpu_ctx* ctx);
+/* dU/dt of the projected state (after nsfr_gpu_project and the halo swap). */
+int nsfr_gpu_residual(nsfr_gpu_ctx* ctx, double* dudt, double* entropy_change);
+/* One RK4 stage (1..4) with the given dt (read at stage 1). */
+int nsfr_gpu_stage(nsfr_gpu_ctx* ctx, int stage, double dt);
 
 /* Device pointers (for callers that keep inputs resident in HBM). The device
  * state holds u at the volume quadrature nodes, u_q = chi^3 u_hat ([e][5][n^3]);

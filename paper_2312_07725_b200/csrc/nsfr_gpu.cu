@@ -287,7 +287,7 @@ int update(nsfr_gpu_ctx* ctx, int stage, bool entropy) { NSFR_DISPATCH(launch_up
 
 // z-face halo exchange with the two slab neighbours
 int exchange(nsfr_gpu_ctx* ctx) {
-  if (ctx->nranks <= 1) return NSFR_OK;
+  if (!ctx->comm) return NSFR_OK;  // single rank, or external halo mode
   const size_t n = static_cast<size_t>(ctx->halo_count);
   NK(ncclGroupStart());
   NK(ncclSend(ctx->d_send_lo, n, ncclDouble, ctx->peer_lo, ctx->comm, ctx->st));
@@ -299,7 +299,7 @@ int exchange(nsfr_gpu_ctx* ctx) {
 }
 
 int allreduce_sum(nsfr_gpu_ctx* ctx, double* d, int n) {
-  if (ctx->nranks <= 1) return NSFR_OK;
+  if (!ctx->comm) return NSFR_OK;
   NK(ncclAllReduce(d, d, n, ncclDouble, ncclSum, ctx->comm, ctx->st));
   return NSFR_OK;
 }
@@ -329,7 +329,7 @@ int rhs_of_state(nsfr_gpu_ctx* ctx, bool entropy) {
 constexpr long long kLaunchesPerStep = 1 + 4 * 2 + 1;
 int enqueue_step(nsfr_gpu_ctx* ctx, bool fixed_dt) {
   if (!fixed_dt) {
-    if (ctx->nranks > 1)
+    if (ctx->comm)
       NK(ncclAllReduce(&ctx->d_step->lam_bits, &ctx->d_step->lam_bits, 1, ncclUint64, ncclMax,
                        ctx->comm, ctx->st));
     k_step_dt<<<1, 1, 0, ctx->st>>>(ctx->d_step);  // reads and clears lambda
@@ -549,15 +549,15 @@ int nsfr_gpu_create(const nsfr_gpu_setup* setup, nsfr_gpu_ctx** out) {
       ctx->msg = "nsfr_gpu_create: halo allocation failed";
       return fail(NSFR_E_CUDA);
     }
-    if (!s.nccl_id) {
-      ctx->msg = "nsfr_gpu_create: nranks > 1 needs an NCCL unique id";
-      return fail(NSFR_E_NCCL);
-    }
-    ncclUniqueId id;
-    std::memcpy(&id, s.nccl_id, sizeof id);
-    if (ncclCommInitRank(&ctx->comm, ctx->nranks, id, ctx->rank) != ncclSuccess) {
-      ctx->msg = "ncclCommInitRank failed";
-      return fail(NSFR_E_NCCL);
+    // without an NCCL id the caller moves the halo planes itself (external
+    // halo mode: nsfr_gpu_halo_buffers / halo_get / halo_set + nsfr_gpu_stage)
+    if (s.nccl_id) {
+      ncclUniqueId id;
+      std::memcpy(&id, s.nccl_id, sizeof id);
+      if (ncclCommInitRank(&ctx->comm, ctx->nranks, id, ctx->rank) != ncclSuccess) {
+        ctx->msg = "ncclCommInitRank failed";
+        return fail(NSFR_E_NCCL);
+      }
     }
   }
   StepState h{};
@@ -761,7 +761,7 @@ int nsfr_gpu_get_traces(nsfr_gpu_ctx* ctx, double* traces) {
 
 int nsfr_gpu_max_wavespeed(nsfr_gpu_ctx* ctx, double* lam) {
   if (int rc = project_state(ctx)) return rc;
-  if (ctx->nranks > 1)
+  if (ctx->comm)
     NK(ncclAllReduce(&ctx->d_step->lam_bits, &ctx->d_step->lam_bits, 1, ncclUint64, ncclMax, ctx->comm, ctx->st));
   if (int rc = sync_check(ctx)) return rc;
   unsigned long long b = ctx->h_step->lam_bits;
@@ -874,6 +874,91 @@ static int totals(nsfr_gpu_ctx* ctx, double out6[NTOT]) {
   if (int rc = sync_check(ctx)) return rc;
   CK(cudaMemcpy(out6, ctx->d_red, sizeof(double) * NTOT, cudaMemcpyDeviceToHost));
   return NSFR_OK;
+}
+
+// ---- external halo mode (nranks > 1, no NCCL id): the caller moves the planes
+int nsfr_gpu_halo_buffers(nsfr_gpu_ctx* ctx, double** send_lo, double** send_hi, double** recv_lo,
+                          double** recv_hi) {
+  *send_lo = ctx->d_send_lo;
+  *send_hi = ctx->d_send_hi;
+  *recv_lo = ctx->d_halo_lo;
+  *recv_hi = ctx->d_halo_hi;
+  return NSFR_OK;
+}
+
+int nsfr_gpu_halo_get(nsfr_gpu_ctx* ctx, double* send_lo, double* send_hi) {
+  if (ctx->nranks <= 1) {
+    ctx->msg = "halo_get: single-rank context has no halo planes";
+    return NSFR_E_CONFIG;
+  }
+  const size_t b = sizeof(double) * ctx->halo_count;
+  CK(cudaMemcpyAsync(send_lo, ctx->d_send_lo, b, cudaMemcpyDeviceToHost, ctx->st));
+  CK(cudaMemcpyAsync(send_hi, ctx->d_send_hi, b, cudaMemcpyDeviceToHost, ctx->st));
+  return sync_check(ctx);
+}
+
+int nsfr_gpu_halo_set(nsfr_gpu_ctx* ctx, const double* recv_lo, const double* recv_hi) {
+  if (ctx->nranks <= 1) {
+    ctx->msg = "halo_set: single-rank context has no halo planes";
+    return NSFR_E_CONFIG;
+  }
+  const size_t b = sizeof(double) * ctx->halo_count;
+  CK(cudaMemcpyAsync(ctx->d_halo_lo, recv_lo, b, cudaMemcpyHostToDevice, ctx->st));
+  CK(cudaMemcpyAsync(ctx->d_halo_hi, recv_hi, b, cudaMemcpyHostToDevice, ctx->st));
+  return sync_check(ctx);
+}
+
+int nsfr_gpu_project(nsfr_gpu_ctx* ctx) {
+  if (int rc = project_state(ctx)) return rc;
+  return sync_check(ctx);
+}
+
+int nsfr_gpu_residual(nsfr_gpu_ctx* ctx, double* dudt, double* entropy_change) {
+  const bool ent = entropy_change != nullptr;
+  if (ent && !ctx->d_vhat) {
+    ctx->msg = "entropy change needs setup.entropy_diag = 1";
+    return NSFR_E_CONFIG;
+  }
+  if (!ctx->proj_valid) {
+    ctx->msg = "residual: no projection of the current state (call nsfr_gpu_project)";
+    return NSFR_E_CONFIG;
+  }
+  if (int rc = exchange(ctx)) return rc;
+  if (int rc = residual(ctx)) return rc;
+  if (int rc = update(ctx, 0, ent)) return rc;
+  if (ent) {
+    k_reduce<<<1, 1024, 0, ctx->st>>>(ctx->d_dS, ctx->E, 1, ctx->d_red);
+    ++ctx->launches;
+    if (int rc = allreduce_sum(ctx, ctx->d_red, 1)) return rc;
+  }
+  if (int rc = sync_check(ctx)) return rc;
+  if (dudt) CK(cudaMemcpy(dudt, ctx->d_rhs, sizeof(double) * state_count(ctx), cudaMemcpyDeviceToHost));
+  if (ent) CK(cudaMemcpy(entropy_change, ctx->d_red, sizeof(double), cudaMemcpyDeviceToHost));
+  return NSFR_OK;
+}
+
+int nsfr_gpu_stage(nsfr_gpu_ctx* ctx, int stage, double dt) {
+  if (stage < 1 || stage > 4) {
+    ctx->msg = "stage must be 1..4";
+    return NSFR_E_DIM;
+  }
+  if (!ctx->proj_valid) {
+    ctx->msg = "stage: no projection of the stage state (call nsfr_gpu_project first)";
+    return NSFR_E_CONFIG;
+  }
+  if (stage == 1) {
+    CK(cudaMemcpyAsync(&ctx->d_step->dt, &dt, sizeof dt, cudaMemcpyHostToDevice, ctx->st));
+    k_step_begin<<<1, 1, 0, ctx->st>>>(ctx->d_step);  // lambda of u_{n+1} accumulates in stage 4
+    ++ctx->launches;
+  }
+  if (int rc = exchange(ctx)) return rc;
+  if (int rc = residual(ctx)) return rc;
+  if (int rc = update(ctx, stage, false)) return rc;
+  if (stage == 4) {
+    k_step_end<<<1, 1, 0, ctx->st>>>(ctx->d_step);
+    ++ctx->launches;
+  }
+  return sync_check(ctx);
 }
 
 int nsfr_gpu_conserved_totals(nsfr_gpu_ctx* ctx, double out5[5]) {

@@ -121,6 +121,11 @@ def load_library() -> C.CDLL:
         "nsfr_gpu_conserved_totals": (C.c_int, [V, P]),
         "nsfr_gpu_entropy_total": (C.c_int, [V, P]),
         "nsfr_gpu_set_state_q": (C.c_int, [V, P]),
+        "nsfr_gpu_halo_get": (C.c_int, [V, P, P]),
+        "nsfr_gpu_halo_set": (C.c_int, [V, P, P]),
+        "nsfr_gpu_project": (C.c_int, [V]),
+        "nsfr_gpu_residual": (C.c_int, [V, P, P]),
+        "nsfr_gpu_stage": (C.c_int, [V, C.c_int, C.c_double]),
         "nsfr_gpu_get_state_q": (C.c_int, [V, P]),
         "nsfr_gpu_ke_volume": (C.c_int, [V, P]),
         "nsfr_gpu_time_steps": (C.c_int, [V, C.c_int, C.c_double, P, P]),
@@ -386,6 +391,36 @@ class GpuSolver:
         out = np.zeros(1)
         self._check(self.lib.nsfr_gpu_ke_volume(self.ctx, _ptr(out)))
         return float(out[0])
+
+    # --- stage-level driving / external halo transport (nranks > 1, no NCCL id)
+    @property
+    def halo_shape(self):
+        return (self.cfg.m * self.cfg.m, 5, self.n * self.n)
+
+    def halo_get(self):
+        """The two send planes (face 4 of plane k0, face 5 of plane k1-1)."""
+        lo, hi = np.zeros(self.halo_shape), np.zeros(self.halo_shape)
+        self._check(self.lib.nsfr_gpu_halo_get(self.ctx, _ptr(lo), _ptr(hi)))
+        return lo, hi
+
+    def halo_set(self, recv_lo: np.ndarray, recv_hi: np.ndarray):
+        lo = np.ascontiguousarray(recv_lo, dtype=np.float64)
+        hi = np.ascontiguousarray(recv_hi, dtype=np.float64)
+        assert lo.shape == self.halo_shape and hi.shape == self.halo_shape
+        self._check(self.lib.nsfr_gpu_halo_set(self.ctx, _ptr(lo), _ptr(hi)))
+
+    def project(self):
+        self._check(self.lib.nsfr_gpu_project(self.ctx))
+
+    def residual(self, entropy: bool = False):
+        """dU/dt of the projected state (after project() and the halo swap)."""
+        out = np.zeros(self.state_shape)
+        ds = np.zeros(1) if entropy else None
+        self._check(self.lib.nsfr_gpu_residual(self.ctx, _ptr(out), _ptr(ds)))
+        return (out, float(ds[0])) if entropy else out
+
+    def stage(self, s: int, dt: float):
+        self._check(self.lib.nsfr_gpu_stage(self.ctx, s, dt))
 
     def conserved_totals(self) -> np.ndarray:
         """sum w J u over the (global) domain: mass, momentum x3, energy."""
