@@ -35,6 +35,55 @@ __device__ unsigned long long g_phase_cycles[4];
 #define PHASE_MARK(i)
 #endif
 
+// S6 volume pairs a < b of one line (sumfac.hpp:76-89): node a's row in
+// registers, node b's in the line's shared accumulator. UNR: fully unrolled
+// (compile-time indices and coefficients; p=3 K2 -1.6%), used for n <= 4;
+// rolled above (the unrolled code outgrows the instruction cache: p=4 +4%,
+// p=5 +1.5%; measured).
+#define NSFR_VOL_PAIRS_BODY                                                                    \
+  {                                                                                            \
+    const int ia = lbase + a * stride;                                                         \
+    const PrimH pa{Pd[ia], Pd[N3 + ia], Pd[2 * N3 + ia], Pd[3 * N3 + ia], Pd[4 * N3 + ia],     \
+                   Pd[5 * N3 + ia]};                                                           \
+    const double ca0 = Ch[(0 + dir) * N3 + ia], ca1 = Ch[(3 + dir) * N3 + ia],                 \
+                 ca2 = Ch[(6 + dir) * N3 + ia];                                                \
+    double fa[NS] = {0.0, 0.0, 0.0, 0.0, 0.0};                                                 \
+    NSFR_INNER_UNROLL                                                                          \
+    for (int bb = a + 1; bb < N; ++bb) {                                                       \
+      const int ib = lbase + bb * stride;                                                      \
+      const PrimH pb{Pd[ib], Pd[N3 + ib], Pd[2 * N3 + ib], Pd[3 * N3 + ib], Pd[4 * N3 + ib],   \
+                     Pd[5 * N3 + ib]};                                                         \
+      double f[NS];                                                                            \
+      d_flux_h<KE>(pa, pb, ca0 + Ch[(0 + dir) * N3 + ib], ca1 + Ch[(3 + dir) * N3 + ib],       \
+                   ca2 + Ch[(6 + dir) * N3 + ib], f);                                          \
+      const double c = wt * q[a * N + bb];                                                     \
+      _Pragma("unroll") for (int s = 0; s < NS; ++s) {                                         \
+        fa[s] = fma(c, f[s], fa[s]);                                                           \
+        acc[s * N3 + ib] = fma(-c, f[s], acc[s * N3 + ib]);                                    \
+      }                                                                                        \
+    }                                                                                          \
+    _Pragma("unroll") for (int s = 0; s < NS; ++s) acc[s * N3 + ia] += fa[s];                  \
+  }
+
+template <int N, bool KE>
+__device__ __forceinline__ void vol_pairs(const double* Pd, const double* Ch, double* acc,
+                                          const double (&q)[N * N], double wt, int lbase,
+                                          int stride, int dir) {
+  constexpr int N3 = N * N * N;
+  if constexpr (N <= 4) {
+#define NSFR_INNER_UNROLL _Pragma("unroll")
+#pragma unroll
+    for (int a = 0; a < N - 1; ++a) NSFR_VOL_PAIRS_BODY
+#undef NSFR_INNER_UNROLL
+  } else {
+#define NSFR_INNER_UNROLL _Pragma("unroll 1")
+#pragma unroll 1
+    for (int a = 0; a < N - 1; ++a) NSFR_VOL_PAIRS_BODY
+#undef NSFR_INNER_UNROLL
+  }
+}
+#undef NSFR_VOL_PAIRS_BODY
+
 struct ResParams {
   const double* ut_vol;   // [E][6][N^3] half-scaled primitives of u~ (K1 / K3)
   const double* traces;   // [E][6][5][N^2]
@@ -151,33 +200,7 @@ __device__ __forceinline__ void res_batch(const ResParams& P, const ResOps<N>& O
     for (int a = 0; a < N; ++a)
 #pragma unroll
       for (int s = 0; s < NS; ++s) acc[s * N3 + lbase + a * stride] = 0.0;
-    // S6 volume pairs a<b (sumfac.hpp:76-89)
-#pragma unroll 1
-    for (int a = 0; a < N - 1; ++a) {
-      const int ia = lbase + a * stride;
-      const PrimH pa{Pd[ia], Pd[N3 + ia], Pd[2 * N3 + ia], Pd[3 * N3 + ia],
-                     Pd[4 * N3 + ia], Pd[5 * N3 + ia]};
-      const double ca0 = Ch[(0 + dir) * N3 + ia], ca1 = Ch[(3 + dir) * N3 + ia],
-                   ca2 = Ch[(6 + dir) * N3 + ia];
-      double fa[NS] = {0.0, 0.0, 0.0, 0.0, 0.0};
-#pragma unroll 1
-      for (int bb = a + 1; bb < N; ++bb) {
-        const int ib = lbase + bb * stride;
-        const PrimH pb{Pd[ib], Pd[N3 + ib], Pd[2 * N3 + ib], Pd[3 * N3 + ib],
-                       Pd[4 * N3 + ib], Pd[5 * N3 + ib]};
-        double f[NS];
-        d_flux_h<KE>(pa, pb, ca0 + Ch[(0 + dir) * N3 + ib], ca1 + Ch[(3 + dir) * N3 + ib],
-                          ca2 + Ch[(6 + dir) * N3 + ib], f);
-        const double c = wt * O.q[a * N + bb];
-#pragma unroll
-        for (int s = 0; s < NS; ++s) {
-          fa[s] = fma(c, f[s], fa[s]);
-          acc[s * N3 + ib] = fma(-c, f[s], acc[s * N3 + ib]);
-        }
-      }
-#pragma unroll
-      for (int s = 0; s < NS; ++s) acc[s * N3 + ia] += fa[s];
-    }
+    vol_pairs<N, KE>(Pd, Ch, acc, O.q, wt, lbase, stride, dir);
     // S7 hybrid surface pairs + S8 face flux for the two faces this line pierces
 #pragma unroll 1
     for (int side = 0; side < (KE ? 0 : 2); ++side) {
