@@ -151,6 +151,7 @@ __device__ __forceinline__ void proj_core(const ProjParams& P, const ProjOps<N>&
   const int tid = threadIdx.x, nthr = blockDim.x;
   const double g = P.gamma;
   const int nbs = nb * 5;
+  PHASE_START();
   // S1 u_q = chi^3 u_hat is where the state lives: the solver carries u_q
   // (k_convert at the API boundary), so A already holds it.
   // S2 v(u_q) -> V, the wavespeed for adaptive dt, and the
@@ -202,12 +203,14 @@ __device__ __forceinline__ void proj_core(const ProjParams& P, const ProjOps<N>&
     double* dst = P.vhat + (size_t)e0 * 5 * N3;
     for (int i = tid; i < nb * 5 * N3; i += nthr) dst[i] = A[i];
   }
+  PHASE_MARK(11);
   // S4 faces: v~_f = (bs_side (x) chi (x) chi) Pi^3 v_q = (bs_side Pi) along the
   // normal applied to v_q (chi Pi = I tangentially): one contraction per line
   face_contract<N, 0>(O.bp, V, F0, nbs, tid, nthr);
   face_contract<N, 1>(O.bp, V, F1, nbs, tid, nthr);
   face_contract<N, 2>(O.bp, V, F2, nbs, tid, nthr);
   __syncthreads();
+  PHASE_MARK(12);
   // S5 u~ = u(v~) at the face nodes
   for (int it = tid; it < nb * 6 * N2; it += nthr) {
     const int b = it / (6 * N2), r = it - b * 6 * N2, f = r / N2, k = r - f * N2;
@@ -232,6 +235,7 @@ __device__ __forceinline__ void proj_core(const ProjParams& P, const ProjOps<N>&
       for (int s = 0; s < NS; ++s) P.send_hi[((size_t)plane * 5 + s) * N2 + k] = uu[s];
     }
   }
+  PHASE_MARK(13);
 }
 
 template <int N>

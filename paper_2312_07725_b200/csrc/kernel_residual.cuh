@@ -17,23 +17,6 @@
 
 namespace nsfr_b200 {
 
-// Development instrumentation (-DNSFR_PHASE_PROF): per-CTA clock64 deltas of
-// the K2 phases (staging, line, output) summed over CTAs.
-#ifdef NSFR_PHASE_PROF
-__device__ unsigned long long g_phase_cycles[4];
-#define PHASE_START() long long t_prev_ = clock64()
-#define PHASE_MARK(i)                                                        \
-  do {                                                                       \
-    if (threadIdx.x == 0) {                                                  \
-      const long long t_ = clock64();                                        \
-      atomicAdd(&g_phase_cycles[i], static_cast<unsigned long long>(t_ - t_prev_)); \
-      t_prev_ = t_;                                                          \
-    }                                                                        \
-  } while (0)
-#else
-#define PHASE_START()
-#define PHASE_MARK(i)
-#endif
 
 // S6 volume pairs a < b of one line (sumfac.hpp:76-89): node a's row in
 // registers, node b's in the line's shared accumulator. UNR: fully unrolled

@@ -164,6 +164,7 @@ __device__ __forceinline__ void upd_batch(const UpdParams& P, const UpdOps<N>& O
   const int tid = threadIdx.x, nthr = blockDim.x;
   const int nb = min(EPB, P.pj.E - e0);
   const int nbs = nb * 5;
+  PHASE_START();
   __shared__ unsigned long long bar;
   {
     const StageBlock blk[3] = {{R0, P.vol + (size_t)e0 * VS, nb * VS},
@@ -191,6 +192,7 @@ __device__ __forceinline__ void upd_batch(const UpdParams& P, const UpdOps<N>& O
   }
   stage_wait(&bar);
   __syncthreads();
+  PHASE_MARK(8);
 
   if (!P.dS) {
     // Pi~^T S9 in three fused passes; 1/(w J) in the last
@@ -229,6 +231,7 @@ __device__ __forceinline__ void upd_batch(const UpdParams& P, const UpdOps<N>& O
     tail_pass<N, 2, false, true>(T.frt, T.bs, nullptr, 0, R2, VS, R0, VS, WJ, nbs, tid, nthr);
     __syncthreads();
   }
+  PHASE_MARK(9);
   // second half of S10: Pi~ along xi, eta
   tail_pass<N, 0, false, false>(T.fr, T.bs, nullptr, 0, R0, VS, R1, VS, WJ, nbs, tid, nthr);
   __syncthreads();
@@ -281,6 +284,7 @@ __device__ __forceinline__ void upd_batch(const UpdParams& P, const UpdOps<N>& O
   }
   if (P.stage == 0) return;
   __syncthreads();
+  PHASE_MARK(10);
   proj_core<N>(P.pj, O.p, e0, nb, R0, R1, R2, R3);
 }
 

@@ -1094,11 +1094,11 @@ extern "C" int nsfr_gpu_measure_fp64_peak(int device, double* tflops) {
 
 #ifdef NSFR_PHASE_PROF
 // Development only: read and reset the K2 phase cycle counters.
-extern "C" int nsfr_gpu_phase_counters(double* out4) {
-  unsigned long long h[4];
+extern "C" int nsfr_gpu_phase_counters(double* out16) {
+  unsigned long long h[16];
   if (cudaMemcpyFromSymbol(h, g_phase_cycles, sizeof h) != cudaSuccess) return NSFR_E_CUDA;
-  for (int i = 0; i < 4; ++i) out4[i] = static_cast<double>(h[i]);
-  const unsigned long long z[4] = {0, 0, 0, 0};
+  for (int i = 0; i < 16; ++i) out16[i] = static_cast<double>(h[i]);
+  const unsigned long long z[16] = {};
   cudaMemcpyToSymbol(g_phase_cycles, z, sizeof z);
   return NSFR_OK;
 }
