@@ -38,7 +38,7 @@ namespace nsfr_b200 {
                      Pd[5 * N3 + ib]};                                                         \
       double f[NS];                                                                            \
       d_flux_h<KE>(pa, pb, ca0 + Ch[(0 + dir) * N3 + ib], ca1 + Ch[(3 + dir) * N3 + ib],       \
-                   ca2 + Ch[(6 + dir) * N3 + ib], f);                                          \
+                   ca2 + Ch[(6 + dir) * N3 + ib], f, amask);                                          \
       const double c = wt * q[a * N + bb];                                                     \
       _Pragma("unroll") for (int s = 0; s < NS; ++s) {                                         \
         fa[s] = fma(c, f[s], fa[s]);                                                           \
@@ -51,7 +51,7 @@ namespace nsfr_b200 {
 template <int N, bool KE>
 __device__ __forceinline__ void vol_pairs(const double* Pd, const double* Ch, double* acc,
                                           const double (&q)[N * N], double wt, int lbase,
-                                          int stride, int dir) {
+                                          int stride, int dir, unsigned amask) {
   constexpr int N3 = N * N * N;
   if constexpr (N <= 4) {
 #define NSFR_INNER_UNROLL _Pragma("unroll")
@@ -172,6 +172,9 @@ __device__ __forceinline__ void res_batch(const ResParams& P, const ResOps<N>& O
   const int ll = tid - lb * LINES;
   const int ldir = ll / N2, lrem = ll - ldir * N2;
   if (lb < nb) {
+    // lanes of this warp in the line phase: every line runs the same loop trip
+    // counts, so this set is active at every flux call below
+    const unsigned amask = __activemask();
     const int b = lb, e = e0 + b, dir = ldir, t1 = lrem % N, t2 = lrem / N;
     const int stride = dir == 0 ? 1 : (dir == 1 ? N : N2);
     const int lbase = dir == 0 ? N * (t1 + N * t2) : (dir == 1 ? t1 + N2 * t2 : t1 + N * t2);
@@ -183,7 +186,7 @@ __device__ __forceinline__ void res_batch(const ResParams& P, const ResOps<N>& O
     for (int a = 0; a < N; ++a)
 #pragma unroll
       for (int s = 0; s < NS; ++s) acc[s * N3 + lbase + a * stride] = 0.0;
-    vol_pairs<N, KE>(Pd, Ch, acc, O.q, wt, lbase, stride, dir);
+    vol_pairs<N, KE>(Pd, Ch, acc, O.q, wt, lbase, stride, dir, amask);
     // S7 hybrid surface pairs + S8 face flux for the two faces this line pierces
 #pragma unroll 1
     for (int side = 0; side < (KE ? 0 : 2); ++side) {
@@ -234,7 +237,7 @@ __device__ __forceinline__ void res_batch(const ResParams& P, const ResOps<N>& O
                        Pd[4 * N3 + ia], Pd[5 * N3 + ia]};
         double fl[NS];
         d_flux_h(pa, pfh, Ch[(0 + dir) * N3 + ia] + ch0, Ch[(3 + dir) * N3 + ia] + ch1,
-                          Ch[(6 + dir) * N3 + ia] + ch2, fl);
+                          Ch[(6 + dir) * N3 + ia] + ch2, fl, amask);
         const double c = sign * O.bflux[side * N + a] * wt;
 #pragma unroll
         for (int s = 0; s < NS; ++s) {
@@ -249,7 +252,7 @@ __device__ __forceinline__ void res_batch(const ResParams& P, const ResOps<N>& O
       const double nrm[3] = {v0 * ijg, v1 * ijg, v2 * ijg};
       const PrimX pn = d_primx(g, un);
       double fn[NS];
-      d_flux_h(pfh, to_half(gm1, pn), nrm[0], nrm[1], nrm[2], fn);
+      d_flux_h(pfh, to_half(gm1, pn), nrm[0], nrm[1], nrm[2], fn, amask);
       if (P.roe) {
         double d[NS];
         if (!d_roe_x(g, uf, un, pf, pn, nrm, d)) atomicOr(P.err, ERR_ROE);
