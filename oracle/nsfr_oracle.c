@@ -1349,10 +1349,11 @@ static void ke_elem(void* argp, int e) {
   }
   double acc = 0.0;
   for (int q = 0; q < nv; ++q) {
-    const double r = utv[q];
-    const double vx = utv[nv + q] / r, vy = utv[2 * nv + q] / r, vz = utv[3 * nv + q] / r;
-    acc += -0.5 * (vx * vx + vy * vy + vz * vz) * vol[q] + vx * vol[nv + q] + vy * vol[2 * nv + q] +
-           vz * vol[3 * nv + q];
+    /* kinetic_energy_variables, euler.cpp:83-87 */
+    const double iu = 1.0 / utv[q];
+    const double vx = utv[nv + q] * iu, vy = utv[2 * nv + q] * iu, vz = utv[3 * nv + q] * iu;
+    const double vk0 = -0.5 * (vx * vx + vy * vy + vz * vz);
+    acc += vk0 * vol[q] + vx * vol[nv + q] + vy * vol[2 * nv + q] + vz * vol[3 * nv + q];
   }
   A->part[e] = acc;
 }

@@ -454,10 +454,8 @@ int nsfr_ref_ke_volume(void* ctx, const double* u, double* out) {
     }
     double acc = 0.0;
     for (int q = 0; q < nv; ++q) {
-      const double r = utv[q];
-      const double vx = utv[nv + q] / r, vy = utv[2 * nv + q] / r, vz = utv[3 * nv + q] / r;
-      acc += -0.5 * (vx * vx + vy * vy + vz * vz) * vol[q] + vx * vol[nv + q] + vy * vol[2 * nv + q] +
-             vz * vol[3 * nv + q];
+      const State vk = kinetic_energy_variables(load(utv, nv, q));  // euler.cpp:83-87
+      acc += vk[0] * vol[q] + vk[1] * vol[nv + q] + vk[2] * vol[2 * nv + q] + vk[3] * vol[3 * nv + q];
     }
     part[e] = acc;
   });

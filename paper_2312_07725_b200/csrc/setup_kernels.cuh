@@ -423,10 +423,10 @@ __global__ void k_ke_dot(const double* u, const double* vol, int N3, double* par
   const double* ve = vol + (size_t)e * NS * N3;
   double acc = 0.0;
   for (int q = tid; q < N3; q += nthr) {
-    const double r = ue[q];
-    const double vx = ue[N3 + q] / r, vy = ue[2 * N3 + q] / r, vz = ue[3 * N3 + q] / r;
-    acc += -0.5 * (vx * vx + vy * vy + vz * vz) * ve[q] + vx * ve[N3 + q] + vy * ve[2 * N3 + q] +
-           vz * ve[3 * N3 + q];
+    const double iu = 1.0 / ue[q];  // kinetic_energy_variables, euler.cpp:83-87
+    const double vx = ue[N3 + q] * iu, vy = ue[2 * N3 + q] * iu, vz = ue[3 * N3 + q] * iu;
+    const double vk0 = -0.5 * (vx * vx + vy * vy + vz * vz);
+    acc += vk0 * ve[q] + vx * ve[N3 + q] + vy * ve[2 * N3 + q] + vz * ve[3 * N3 + q];
   }
   red[tid] = acc;
   __syncthreads();
