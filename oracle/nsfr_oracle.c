@@ -538,6 +538,22 @@ static int flux_ec(double g, const double* ul, const double* ur, double f[3][NS]
   return NSFR_OK;
 }
 
+/* euler.cpp:30-40 physical_flux: f[k][s] for physical direction k */
+static int physical_flux(double g, const double* u, double f[3][NS]) {
+  if (!admissible(g, u)) return NSFR_E_INADMISSIBLE;
+  const double p = pressure(g, u);
+  for (int k = 0; k < 3; ++k) {
+    const double vk = u[1 + k] / u[0];
+    f[k][0] = u[0] * vk;
+    f[k][1] = u[1] * vk;
+    f[k][2] = u[2] * vk;
+    f[k][3] = u[3] * vk;
+    f[k][4] = (u[4] + p) * vk;
+    f[k][1 + k] += p;
+  }
+  return NSFR_OK;
+}
+
 /* euler.cpp:229-301 roe_dissipation: -1/2 R|L|S R^T (v_l - v_r) */
 static int roe_diss(double g, const double* ul, const double* ur, const double* n, double* out) {
   const Prim l = prim(g, ul), r = prim(g, ur);
@@ -1019,10 +1035,56 @@ static void project_elem(void* argp, int e) {
     }
 }
 
+/* Conservative DG: no entropy projection; the volume and
+ * face states are chi u_hat at the volume quadrature nodes and
+ * (bound_sol (x) chi (x) chi) u_hat at the face nodes. */
+static void dg_states_elem(void* argp, int e) {
+  ProjArg* A = (ProjArg*)argp;
+  Ctx* c = A->c;
+  const Ops* o = &c->ops;
+  const double g = c->cfg.gamma;
+  const int np = c->np, nv = c->nv, nsol = c->nsol, nf = c->nf;
+  const int me[3] = {np, np, np};
+  const double* ue = A->u + (size_t)e * NS * nsol;
+  double* utv = c->ut_vol + (size_t)e * NS * nv;
+  for (int s = 0; s < NS; ++s) apply_tp(&o->interp, &o->interp, &o->interp, ue + s * nsol, me, utv + s * nv);
+  for (int q = 0; q < nv; ++q) {
+    double uu[NS];
+    for (int s = 0; s < NS; ++s) uu[s] = utv[s * nv + q];
+    if (!admissible(g, uu)) {
+      c->err[e] = NSFR_E_INADMISSIBLE;
+      return;
+    }
+  }
+  Op bs[2];
+  for (int side = 0; side < 2; ++side) {
+    bs[side] = op_zero(1, np);
+    for (int a = 0; a < np; ++a) OP(bs[side], 0, a) = OP(o->bound_sol, side, a);
+  }
+  for (int dir = 0; dir < 3; ++dir)
+    for (int side = 0; side < 2; ++side) {
+      const int f = 2 * dir + side;
+      const Op* a0 = dir == 0 ? &bs[side] : &o->interp;
+      const Op* a1 = dir == 1 ? &bs[side] : &o->interp;
+      const Op* a2 = dir == 2 ? &bs[side] : &o->interp;
+      double* utf = c->ut_f + ((size_t)e * 6 + f) * NS * nf;
+      for (int s = 0; s < NS; ++s) apply_tp(a0, a1, a2, ue + s * nsol, me, utf + s * nf);
+      for (int k = 0; k < nf; ++k) {
+        double uu[NS];
+        for (int s = 0; s < NS; ++s) uu[s] = utf[s * nf + k];
+        if (!admissible(g, uu)) {
+          c->err[e] = NSFR_E_INADMISSIBLE;
+          return;
+        }
+      }
+    }
+}
+
 static int project_all(Ctx* c, const double* u) {
   memset(c->err, 0, sizeof(int) * c->ne);
   ProjArg A = {c, u};
-  parallel_for(c->ne, c->cfg.workers, project_elem, &A);
+  parallel_for(c->ne, c->cfg.workers, c->cfg.scheme == NSFR_SCHEME_DG ? dg_states_elem : project_elem,
+               &A);
   for (int e = 0; e < c->ne; ++e)
     if (c->err[e]) {
       set_err(c, "entropy projection: inadmissible state in element %d", e);
@@ -1258,6 +1320,143 @@ static void rhs_elem(void* argp, int e) {
   }
 }
 
+/* Conservative strong-form DG residual ("cons DG strong";
+ * SPEC.md:457-465), own face metrics (D1), weight-adjusted inverse (D6):
+ *   R = chi^T W div^r(f^r) + sum_f (bs_f (x) chi^T (x) chi^T) W_f [J^G f*.n - n^r.phi(xi_f) f^r]
+ * with f^r_dir = sum_k C[k][dir] f_k (contravariant flux on the volume quadrature
+ * nodes, collocated flux basis), div^r by quad_diff, phi(xi_f) by bound_flux and
+ * f*.n = 1/2 (f(u-) + f(u+)).n - roe_dissipation(u-, u+, n) (the paper's Roe
+ * surface flux; roe = 0: central). dudt = -Pi~ (W J)^-1 Pi~^T R. */
+static void dg_rhs_elem(void* argp, int e) {
+  RhsArg* A = (RhsArg*)argp;
+  Ctx* c = A->c;
+  const Ops* o = &c->ops;
+  const double g = c->cfg.gamma;
+  const int np = c->np, nq = c->nq, nv = c->nv, nsol = c->nsol, nf = c->nf;
+  const double* utv = c->ut_vol + (size_t)e * NS * nv;
+  const double* C = c->cof + (size_t)e * nv * 9;
+  const int qe[3] = {nq, nq, nq};
+  static __thread double fr[3][NS][MAXN * MAXN * MAXN];
+  static __thread double vol[NS][MAXN * MAXN * MAXN];
+  double fl[3][NS];
+  for (int q = 0; q < nv; ++q) {
+    double uu[NS];
+    for (int s = 0; s < NS; ++s) uu[s] = utv[s * nv + q];
+    if (physical_flux(g, uu, fl)) {
+      c->err[e] = NSFR_E_INADMISSIBLE;
+      return;
+    }
+    for (int dir = 0; dir < 3; ++dir)
+      for (int s = 0; s < NS; ++s)
+        fr[dir][s][q] = fl[0][s] * C[9 * q + 0 + dir] + fl[1][s] * C[9 * q + 3 + dir] +
+                        fl[2][s] * C[9 * q + 6 + dir];
+  }
+  /* volume: W div^r f^r (apply_operator_dir with quad_diff per direction) */
+  double tmp[MAXN * MAXN * MAXN];
+  for (int s = 0; s < NS; ++s) {
+    apply_dir(&o->quad_diff, 0, fr[0][s], qe, vol[s]);
+    apply_dir(&o->quad_diff, 1, fr[1][s], qe, tmp);
+    for (int q = 0; q < nv; ++q) vol[s][q] += tmp[q];
+    apply_dir(&o->quad_diff, 2, fr[2][s], qe, tmp);
+    for (int q = 0; q < nv; ++q) vol[s][q] += tmp[q];
+  }
+  for (int k = 0; k < nq; ++k)
+    for (int j = 0; j < nq; ++j)
+      for (int i = 0; i < nq; ++i) {
+        const int q = i + nq * (j + nq * k);
+        double w = o->quad.w[i];
+        w *= o->quad.w[j];
+        w *= o->quad.w[k];
+        for (int s = 0; s < NS; ++s) vol[s][q] *= w;
+      }
+  /* surface: W_f [J^G f*.n - n^r . phi(xi_f) f^r] per face node */
+  double facc[6][NS * MAXN * MAXN];
+  for (int dir = 0; dir < 3; ++dir) {
+    const int stride = (dir == 0) ? 1 : (dir == 1 ? nq : nq * nq);
+    for (int side = 0; side < 2; ++side) {
+      const int fid = 2 * dir + side;
+      const double sign = side ? 1.0 : -1.0;
+      const double* utf = c->ut_f + ((size_t)e * 6 + fid) * NS * nf;
+      const double* utn = nbr_trace(A, e, fid);
+      for (int t2 = 0; t2 < nq; ++t2)
+        for (int t1 = 0; t1 < nq; ++t1) {
+          const int k = t1 + nq * t2;
+          const int base = (dir == 0) ? nq * (t1 + nq * t2) : (dir == 1 ? t1 + nq * nq * t2 : t1 + nq * t2);
+          double ul[NS], ur[NS], fn[NS], d[NS], fL[3][NS], fR[3][NS];
+          for (int s = 0; s < NS; ++s) {
+            ul[s] = utf[s * nf + k];
+            ur[s] = utn[s * nf + k];
+          }
+          const double* nr = c->nrm_f + (((size_t)e * 6 + fid) * nf + k) * 3;
+          if (physical_flux(g, ul, fL) || physical_flux(g, ur, fR)) {
+            c->err[e] = NSFR_E_INADMISSIBLE;
+            return;
+          }
+          /* CentralConservative two-point flux (euler.cpp:205-211), contracted */
+          for (int kk = 0; kk < 3; ++kk)
+            for (int s = 0; s < NS; ++s) fL[kk][s] = 0.5 * (fL[kk][s] + fR[kk][s]);
+          for (int s = 0; s < NS; ++s) fn[s] = fL[0][s] * nr[0] + fL[1][s] * nr[1] + fL[2][s] * nr[2];
+          if (c->cfg.roe) {
+            if (roe_diss(g, ul, ur, nr, d)) {
+              c->err[e] = NSFR_E_INADMISSIBLE;
+              return;
+            }
+            for (int s = 0; s < NS; ++s) fn[s] -= d[s];
+          }
+          const double jg = c->jac_f[((size_t)e * 6 + fid) * nf + k];
+          const double wt = o->quad.w[t1] * o->quad.w[t2];
+          for (int s = 0; s < NS; ++s) {
+            double fi = 0.0; /* phi(xi_f) f^r_dir along the line */
+            for (int a = 0; a < nq; ++a) fi += OP(o->bound_flux, side, a) * fr[dir][s][base + a * stride];
+            facc[fid][s * nf + k] = wt * (jg * fn[s] - sign * fi);
+          }
+        }
+    }
+  }
+  /* lifting (as S9) and the weight-adjusted inverse (as S10) */
+  double R[NS * MAXN * MAXN * MAXN];
+  for (int s = 0; s < NS; ++s) apply_tp(&o->interp_t, &o->interp_t, &o->interp_t, vol[s], qe, R + s * nsol);
+  Op bst[2];
+  for (int side = 0; side < 2; ++side) {
+    bst[side] = op_zero(np, 1);
+    for (int a = 0; a < np; ++a) OP(bst[side], a, 0) = OP(o->bound_sol, side, a);
+  }
+  for (int dir = 0; dir < 3; ++dir)
+    for (int side = 0; side < 2; ++side) {
+      const int fid = 2 * dir + side;
+      const Op* a0 = dir == 0 ? &bst[side] : &o->interp_t;
+      const Op* a1 = dir == 1 ? &bst[side] : &o->interp_t;
+      const Op* a2 = dir == 2 ? &bst[side] : &o->interp_t;
+      const int fe[3] = {dir == 0 ? 1 : nq, dir == 1 ? 1 : nq, dir == 2 ? 1 : nq};
+      for (int s = 0; s < NS; ++s) {
+        apply_tp(a0, a1, a2, facc[fid] + s * nf, fe, tmp);
+        for (int i = 0; i < nsol; ++i) R[s * nsol + i] += tmp[i];
+      }
+    }
+  const int me[3] = {np, np, np};
+  const double* J = c->jac + (size_t)e * nv;
+  double nodal[MAXN * MAXN * MAXN];
+  double* out = A->dudt + (size_t)e * NS * nsol;
+  for (int s = 0; s < NS; ++s) {
+    apply_tp(&o->fr_proj_t, &o->fr_proj_t, &o->fr_proj_t, R + s * nsol, me, nodal);
+    for (int k = 0; k < nq; ++k)
+      for (int j = 0; j < nq; ++j)
+        for (int i = 0; i < nq; ++i) {
+          const int q = i + nq * (j + nq * k);
+          double w = o->quad.w[i];
+          w *= o->quad.w[j];
+          w *= o->quad.w[k];
+          if (J[q] <= 0.0) {
+            c->err[e] = NSFR_E_MESH;
+            return;
+          }
+          nodal[q] /= (w * J[q]);
+        }
+    apply_tp(&o->fr_proj, &o->fr_proj, &o->fr_proj, nodal, qe, out + s * nsol);
+    for (int i = 0; i < nsol; ++i) out[s * nsol + i] = -out[s * nsol + i];
+  }
+}
+
 int nsfr_oracle_rhs(void* ctx, const double* u, const double* halo_lo, const double* halo_hi,
                     double* dudt, double* entropy_change) {
   Ctx* c = (Ctx*)ctx;
@@ -1268,9 +1467,13 @@ int nsfr_oracle_rhs(void* ctx, const double* u, const double* halo_lo, const dou
   }
   int rc = project_all(c, u);
   if (rc) return rc;
+  if (entropy_change && c->cfg.scheme == NSFR_SCHEME_DG) {
+    set_err(c, "rhs: the entropy diagnostic is defined for NSFR only");
+    return NSFR_E_DIM;
+  }
   double* dS = entropy_change ? calloc(c->ne, sizeof(double)) : NULL;
   RhsArg A = {c, halo_lo, halo_hi, dudt, dS};
-  parallel_for(c->ne, c->cfg.workers, rhs_elem, &A);
+  parallel_for(c->ne, c->cfg.workers, c->cfg.scheme == NSFR_SCHEME_DG ? dg_rhs_elem : rhs_elem, &A);
   for (int e = 0; e < c->ne; ++e)
     if (c->err[e]) {
       set_err(c, "rhs: %s in element %d",

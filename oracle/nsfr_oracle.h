@@ -17,7 +17,7 @@
  *   state / dudt      [e_local][5][np^3]        modal = nodal values at LGL nodes
  *   jac               [e_local][nq^3]
  *   cof               [e_local][nq^3][9]        cof[3*n_phys + i_ref]
- *   traces            [e_local][6][5][nq^2]     entropy-projected conservative
+ *   traces            [e_local][6][5][nq^2]     entropy-projected conservative (DG: chi u_hat)
  *   halo_lo / halo_hi [m*m][5][nq^2]            face 5 of plane k0-1 / face 4 of plane k1
  */
 #ifndef NSFR_ORACLE_H
@@ -39,9 +39,14 @@ typedef struct nsfr_cfg {
   double length_scale;/* warp length l; <=0 -> (xR-xL)/(2 pi) */
   int grid_degree;    /* mapping degree (reference default p+1) */
   double gamma;
-  int roe;            /* 1: EC + Roe surface flux, 0: EC only */
+  int roe;            /* 1: EC + Roe surface flux, 0: EC only (DG: central + Roe / central) */
   int workers;        /* element-parallel threads (<=1 serial) */
+  int scheme;         /* 0: NSFR-EC; 1: conservative strong-form DG
+                         (SPEC.md:457-465), overintegration allowed */
 } nsfr_cfg;
+
+#define NSFR_SCHEME_NSFR 0
+#define NSFR_SCHEME_DG 1
 
 #define NSFR_CASE_VORTEX 0
 #define NSFR_CASE_TGV 1

@@ -117,12 +117,43 @@ void project_elem(RefCtx& c, const double* u, int e) {
     }
 }
 
+// conservative DG: chi u_hat at volume and face nodes (no entropy projection)
+void dg_states_elem(RefCtx& c, const double* u, int e) {
+  const auto& o = c.ops;
+  const Extents me{c.np, c.np, c.np};
+  std::vector<double> work(8192);
+  const double* ue = u + static_cast<size_t>(e) * kStates * c.nsol;
+  double* utv = &c.ut_vol[static_cast<size_t>(e) * kStates * c.nv];
+  for (int s = 0; s < kStates; ++s)
+    apply_tensor_product(o.basis.interp, o.basis.interp, o.basis.interp,
+                         std::span<const double>(ue + s * c.nsol, c.nsol), me,
+                         std::span<double>(utv + s * c.nv, c.nv), work);
+  for (int q = 0; q < c.nv; ++q)
+    if (!admissible(c.gas, load(utv, c.nv, q))) throw InadmissibleStateError("dg: volume state");
+  for (int dir = 0; dir < 3; ++dir)
+    for (int side = 0; side < 2; ++side) {
+      const int f = 2 * dir + side;
+      const Operator1D& a0 = dir == 0 ? c.bs_row[side] : o.basis.interp;
+      const Operator1D& a1 = dir == 1 ? c.bs_row[side] : o.basis.interp;
+      const Operator1D& a2 = dir == 2 ? c.bs_row[side] : o.basis.interp;
+      double* utf = &c.ut_f[(static_cast<size_t>(e) * 6 + f) * kStates * c.nf];
+      for (int s = 0; s < kStates; ++s)
+        apply_tensor_product(a0, a1, a2, std::span<const double>(ue + s * c.nsol, c.nsol), me,
+                             std::span<double>(utf + s * c.nf, c.nf), work);
+      for (int k = 0; k < c.nf; ++k)
+        if (!admissible(c.gas, load(utf, c.nf, k))) throw InadmissibleStateError("dg: face state");
+    }
+}
+
 int project_all(RefCtx& c, const double* u) {
   std::atomic<int> bad{-1};
   std::string what;
   parallel_for(c.ne, c.cfg.workers, [&](int e) {
     try {
-      project_elem(c, u, e);
+      if (c.cfg.scheme == NSFR_SCHEME_DG)
+        dg_states_elem(c, u, e);
+      else
+        project_elem(c, u, e);
     } catch (const std::exception& ex) {
       bad = e;
     }
@@ -249,15 +280,117 @@ void rhs_elem(RefCtx& c, int e, const double* halo_lo, const double* halo_hi, do
   (void)me;
 }
 
+// conservative strong-form DG with the reference primitives
+void dg_rhs_elem(RefCtx& c, int e, const double* halo_lo, const double* halo_hi, double* dudt) {
+  const auto& o = c.ops;
+  const int nv = c.nv, nf = c.nf, nsol = c.nsol, nq = c.nq;
+  const Extents qe{nq, nq, nq};
+  const ElementMetrics& em = c.md.elem[global_elem(c, e)];
+  const double* utv = &c.ut_vol[static_cast<size_t>(e) * kStates * nv];
+  const double* utf_all = &c.ut_f[static_cast<size_t>(e) * 6 * kStates * nf];
+  std::vector<double> fr(3 * kStates * nv), vol(kStates * nv), tmpv(nv);
+  for (int q = 0; q < nv; ++q) {
+    const Flux F = physical_flux(c.gas, load(utv, nv, q));  // euler.cpp:30-40
+    const double* Cq = em.cof_at(q);
+    for (int dir = 0; dir < 3; ++dir)
+      for (int s = 0; s < kStates; ++s)
+        fr[(dir * kStates + s) * nv + q] =
+            F[0][s] * Cq[0 + dir] + F[1][s] * Cq[3 + dir] + F[2][s] * Cq[6 + dir];
+  }
+  for (int s = 0; s < kStates; ++s) {
+    std::span<double> vs(&vol[s * nv], nv);
+    apply_operator_dir(o.quad_diff, 0, std::span<const double>(&fr[(0 * kStates + s) * nv], nv), qe, vs);
+    for (int dir = 1; dir < 3; ++dir) {
+      apply_operator_dir(o.quad_diff, dir, std::span<const double>(&fr[(dir * kStates + s) * nv], nv), qe,
+                         tmpv);
+      for (int q = 0; q < nv; ++q) vs[q] += tmpv[q];
+    }
+  }
+  for (int k = 0; k < nq; ++k)
+    for (int j = 0; j < nq; ++j)
+      for (int i = 0; i < nq; ++i) {
+        const int q = i + nq * (j + nq * k);
+        double w = o.wq[i];
+        w *= o.wq[j];
+        w *= o.wq[k];
+        for (int s = 0; s < kStates; ++s) vol[s * nv + q] *= w;
+      }
+  std::array<std::vector<double>, 6> facc;
+  for (int dir = 0; dir < 3; ++dir) {
+    const int stride = (dir == 0) ? 1 : (dir == 1 ? nq : nq * nq);
+    for (int side = 0; side < 2; ++side) {
+      const int fid = 2 * dir + side;
+      const double sign = side ? 1.0 : -1.0;
+      facc[fid].assign(kStates * nf, 0.0);
+      const double* utf = utf_all + static_cast<size_t>(fid) * kStates * nf;
+      const double* utn = nbr_trace(c, e, fid, halo_lo, halo_hi);
+      const FaceNormals fnrm = physical_normals(c.md, global_elem(c, e), fid);
+      for (int t2 = 0; t2 < nq; ++t2)
+        for (int t1 = 0; t1 < nq; ++t1) {
+          const int k = t1 + nq * t2;
+          const int base = (dir == 0) ? nq * (t1 + nq * t2) : (dir == 1 ? t1 + nq * nq * t2 : t1 + nq * t2);
+          const State ul = load(utf, nf, k), ur = load(utn, nf, k);
+          const std::array<double, 3> nr{fnrm.unit_normals[3 * k], fnrm.unit_normals[3 * k + 1],
+                                         fnrm.unit_normals[3 * k + 2]};
+          const Flux F = two_point_flux(c.gas, TwoPointFluxKind::CentralConservative, ul, ur);
+          double fn[kStates];
+          for (int s = 0; s < kStates; ++s) fn[s] = F[0][s] * nr[0] + F[1][s] * nr[1] + F[2][s] * nr[2];
+          if (c.cfg.roe) {
+            const State d = roe_dissipation(c.gas, ul, ur, nr);
+            for (int s = 0; s < kStates; ++s) fn[s] -= d[s];
+          }
+          const double jg = fnrm.surface_jacobian[k];
+          const double wt = o.wq[t1] * o.wq[t2];
+          for (int s = 0; s < kStates; ++s) {
+            double fi = 0.0;
+            for (int a = 0; a < nq; ++a)
+              fi += o.bound_flux(side, a) * fr[(dir * kStates + s) * nv + base + a * stride];
+            facc[fid][s * nf + k] = wt * (jg * fn[s] - sign * fi);
+          }
+        }
+    }
+  }
+  std::vector<double> work(8192), R(kStates * nsol), tmp(nsol);
+  for (int s = 0; s < kStates; ++s)
+    apply_tensor_product(c.interp_t, c.interp_t, c.interp_t, std::span<const double>(&vol[s * nv], nv), qe,
+                         std::span<double>(&R[s * nsol], nsol), work);
+  for (int dir = 0; dir < 3; ++dir)
+    for (int side = 0; side < 2; ++side) {
+      const int fid = 2 * dir + side;
+      const Operator1D& a0 = dir == 0 ? c.bs_col[side] : c.interp_t;
+      const Operator1D& a1 = dir == 1 ? c.bs_col[side] : c.interp_t;
+      const Operator1D& a2 = dir == 2 ? c.bs_col[side] : c.interp_t;
+      const Extents fe{dir == 0 ? 1 : nq, dir == 1 ? 1 : nq, dir == 2 ? 1 : nq};
+      for (int s = 0; s < kStates; ++s) {
+        apply_tensor_product(a0, a1, a2, std::span<const double>(&facc[fid][s * nf], nf), fe, tmp, work);
+        for (int i = 0; i < nsol; ++i) R[s * nsol + i] += tmp[i];
+      }
+    }
+  std::vector<double> wa(wa_work_size(o, 3));
+  double* out = dudt + static_cast<size_t>(e) * kStates * nsol;
+  for (int s = 0; s < kStates; ++s) {
+    weight_adjusted_inverse_apply(o, 3, em.jac_vol, std::span<const double>(&R[s * nsol], nsol),
+                                  std::span<double>(out + s * nsol, nsol), wa);
+    for (int i = 0; i < nsol; ++i) out[s * nsol + i] = -out[s * nsol + i];
+  }
+}
+
 int do_rhs(RefCtx& c, const double* u, const double* halo_lo, const double* halo_hi, double* dudt,
            double* dS_total) {
+  if (dS_total && c.cfg.scheme == NSFR_SCHEME_DG) {
+    c.msg = "rhs: the entropy diagnostic is defined for NSFR only";
+    return NSFR_E_DIM;
+  }
   int rc = project_all(c, u);
   if (rc) return rc;
   std::vector<double> dS(dS_total ? c.ne : 0);
   std::atomic<int> bad{-1};
   parallel_for(c.ne, c.cfg.workers, [&](int e) {
     try {
-      rhs_elem(c, e, halo_lo, halo_hi, dudt, dS_total ? dS.data() : nullptr);
+      if (c.cfg.scheme == NSFR_SCHEME_DG)
+        dg_rhs_elem(c, e, halo_lo, halo_hi, dudt);
+      else
+        rhs_elem(c, e, halo_lo, halo_hi, dudt, dS_total ? dS.data() : nullptr);
     } catch (const std::exception&) {
       bad = e;
     }

@@ -29,7 +29,7 @@ class NsfrCfg(C.Structure):
         ("m", C.c_int), ("k0", C.c_int), ("k1", C.c_int),
         ("x_left", C.c_double), ("x_right", C.c_double), ("beta", C.c_double),
         ("length_scale", C.c_double), ("grid_degree", C.c_int), ("gamma", C.c_double),
-        ("roe", C.c_int), ("workers", C.c_int),
+        ("roe", C.c_int), ("workers", C.c_int), ("scheme", C.c_int),
     ]
 
 
@@ -51,6 +51,8 @@ class Config:
     k0: int = 0
     k1: int | None = None
     workers: int = field(default_factory=lambda: os.cpu_count() or 1)
+    scheme: str = "nsfr"   # "nsfr" (NSFR-EC) or "dg" (conservative strong-form DG)
+    overint: int = 0       # extra quadrature nodes (n_q = p + 1 + overint)
 
     def domain(self):
         if self.x_left is not None:
@@ -60,11 +62,12 @@ class Config:
 
     def to_c(self) -> NsfrCfg:
         xl, xr = self.domain()
-        return NsfrCfg(self.p, self.quad_kind, 0, self.c1d, self.m, self.k0,
+        return NsfrCfg(self.p, self.quad_kind, self.overint, self.c1d, self.m, self.k0,
                        self.m if self.k1 is None else self.k1, xl, xr, self.beta,
                        self.length_scale,
                        self.p + 1 if self.grid_degree is None else self.grid_degree,
-                       self.gamma, int(self.roe), self.workers)
+                       self.gamma, int(self.roe), self.workers,
+                       {"nsfr": 0, "dg": 1}[self.scheme])
 
 
 _loaded: dict[str, C.CDLL] = {}
