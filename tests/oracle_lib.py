@@ -136,7 +136,7 @@ class CpuSolver:
         if not self.ctx:
             raise CheckerError(err.value.decode())
         self.np_ = cfg.p + 1
-        self.nq = cfg.p + 1
+        self.nq = cfg.p + 1 + cfg.overint
         self.ne = cfg.m * cfg.m * ((cfg.m if cfg.k1 is None else cfg.k1) - cfg.k0)
         self.nsol = self.np_ ** 3
         self.nv = self.nq ** 3
