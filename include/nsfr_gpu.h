@@ -90,7 +90,17 @@ typedef struct nsfr_gpu_setup {
    * external halo transport (see nsfr_gpu_halo_buffers) */
   const void* nccl_id;
   int rank, nranks;
+  /* scheme (SolverConfig.scheme): NSFR_SCHEME_NSFR (the hot
+   * path) or NSFR_SCHEME_DG, the conservative strong-form DG residual with the
+   * Roe surface flux (roe = 1) or the central flux (roe = 0), weight-adjusted
+   * inverse (exact for overint = 0). overint: extra volume
+   * quadrature nodes, n_q = p+1+overint (DG only; p in [3,5], overint in [0,2]). */
+  int scheme;
+  int overint;
 } nsfr_gpu_setup;
+
+#define NSFR_SCHEME_NSFR 0
+#define NSFR_SCHEME_DG 1
 
 int nsfr_gpu_create(const nsfr_gpu_setup* setup, nsfr_gpu_ctx** out);
 int nsfr_gpu_destroy(nsfr_gpu_ctx* ctx);

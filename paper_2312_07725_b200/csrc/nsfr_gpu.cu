@@ -19,6 +19,9 @@ using namespace nsfr_b200;
 struct nsfr_gpu_ctx {
   nsfr_gpu_setup s{};
   int N = 0, E = 0, m = 0, nz = 0, k0 = 0, k1 = 0;
+  int NQ = 0;       // volume quadrature nodes per direction (N unless overintegrated, DG only)
+  bool dg = false;  // conservative strong-form DG instead of NSFR (kernel_dg.cuh)
+  double* d_dgus = nullptr;  // DG stage state u_hat
   Tables1D tab;
   DevTables htab{};  // host copy of the device tables (source of the kernel-parameter operators)
   DevTables* d_tab = nullptr;
@@ -71,6 +74,7 @@ thread_local std::string g_create_error;
 
 size_t nsol(const nsfr_gpu_ctx* c) { return static_cast<size_t>(c->N) * c->N * c->N; }
 size_t state_count(const nsfr_gpu_ctx* c) { return static_cast<size_t>(c->E) * NS * nsol(c); }
+size_t nquad(const nsfr_gpu_ctx* c) { return static_cast<size_t>(c->NQ) * c->NQ * c->NQ; }
 
 // Per-N launch configuration of the persistent kernels: resident CTAs on the device.
 template <int N>
@@ -285,6 +289,121 @@ int project(nsfr_gpu_ctx* ctx, const double* u, bool lam) { NSFR_DISPATCH(launch
 int residual(nsfr_gpu_ctx* ctx, bool ke = false) { NSFR_DISPATCH(launch_residual, (ctx, ke)); }
 int update(nsfr_gpu_ctx* ctx, int stage, bool entropy) { NSFR_DISPATCH(launch_update, (ctx, stage, entropy)); }
 
+// ---- conservative DG (kernel_dg.cuh) ------------------------------------------
+template <int NP, int NQ>
+DgOps<NP, NQ> dg_ops(const nsfr_gpu_ctx* ctx) {
+  const DevTables& t = ctx->htab;
+  DgOps<NP, NQ> o{};
+  for (int i = 0; i < NQ * NP; ++i) o.chi[i] = t.interp[i];
+  for (int i = 0; i < 2 * NP; ++i) o.bs[i] = t.bsol[i];
+  for (int i = 0; i < NQ * NQ; ++i) o.D[i] = t.quad_diff[i];
+  for (int i = 0; i < 2 * NQ; ++i) o.bflux[i] = t.bflux[i];
+  for (int i = 0; i < NQ; ++i) o.wq[i] = t.wq[i];
+  for (int a = 0; a < NQ; ++a)
+    for (int i = 0; i < NQ; ++i) {  // M = Pi~^T chi^T (nq x nq)
+      double v = 0.0;
+      for (int r = 0; r < NP; ++r) v += t.frproj[r * NQ + a] * t.interp[i * NP + r];
+      o.M[a * NQ + i] = v;
+    }
+  for (int side = 0; side < 2; ++side)
+    for (int a = 0; a < NQ; ++a) {
+      double v = 0.0;
+      for (int r = 0; r < NP; ++r) v += t.frproj[r * NQ + a] * t.bsol[side * NP + r];
+      o.bm[side * NQ + a] = v;
+    }
+  for (int i = 0; i < NP * NQ; ++i) o.fr[i] = t.frproj[i];
+  return o;
+}
+
+template <int NP, int NQ>
+int dg_attrs(nsfr_gpu_ctx* ctx) {
+  using Cfg = DgCfg<NP, NQ>;
+  static bool done = false;
+  if (!done) {
+    CK(cudaFuncSetAttribute(k_dg_states<NP, NQ>, cudaFuncAttributeMaxDynamicSharedMemorySize, Cfg::S_SMEM));
+    CK(cudaFuncSetAttribute(k_dg_residual<NP, NQ>, cudaFuncAttributeMaxDynamicSharedMemorySize,
+                            Cfg::R_SMEM));
+    done = true;
+  }
+  return NSFR_OK;
+}
+
+template <int NP, int NQ>
+int launch_dg_states(nsfr_gpu_ctx* ctx, const double* u, bool want_lam) {
+  using Cfg = DgCfg<NP, NQ>;
+  if (int rc = dg_attrs<NP, NQ>(ctx)) return rc;
+  DgStateParams P{};
+  P.u = u;
+  P.traces = ctx->d_tr;
+  P.send_lo = ctx->nranks > 1 ? ctx->d_send_lo : nullptr;
+  P.send_hi = ctx->nranks > 1 ? ctx->d_send_hi : nullptr;
+  P.lam = want_lam ? &ctx->d_step->lam_bits : nullptr;
+  P.err = ctx->d_err;
+  P.E = ctx->E;
+  P.m = ctx->m;
+  P.nz = ctx->nz;
+  P.gamma = ctx->s.gamma;
+  const int grid = (ctx->E + Cfg::EPB - 1) / Cfg::EPB;
+  ev_begin(ctx, 1);
+  k_dg_states<NP, NQ><<<grid, Cfg::THREADS, Cfg::S_SMEM, ctx->st>>>(P, dg_ops<NP, NQ>(ctx));
+  ev_end(ctx);
+  ++ctx->launches;
+  CK(cudaGetLastError());
+  return NSFR_OK;
+}
+
+template <int NP, int NQ>
+int launch_dg_residual(nsfr_gpu_ctx* ctx, int stage, const double* us, double* uo) {
+  using Cfg = DgCfg<NP, NQ>;
+  if (int rc = dg_attrs<NP, NQ>(ctx)) return rc;
+  DgResParams P{};
+  P.us = us;
+  P.traces = ctx->d_tr;
+  P.halo_lo = ctx->nranks > 1 ? ctx->d_halo_lo : nullptr;
+  P.halo_hi = ctx->nranks > 1 ? ctx->d_halo_hi : nullptr;
+  P.cof = ctx->d_cof;
+  P.wj = ctx->d_wj;
+  P.un = ctx->d_un;
+  P.uo = uo;
+  P.acc = ctx->d_acc;
+  P.out = ctx->d_rhs;
+  P.dt = &ctx->d_step->dt;
+  P.err = ctx->d_err;
+  P.stage = stage;
+  P.E = ctx->E;
+  P.m = ctx->m;
+  P.nz = ctx->nz;
+  P.gamma = ctx->s.gamma;
+  P.roe = ctx->s.roe;
+  const int grid = (ctx->E + Cfg::EPB - 1) / Cfg::EPB;
+  ev_begin(ctx, 2);
+  k_dg_residual<NP, NQ><<<grid, Cfg::THREADS, Cfg::R_SMEM, ctx->st>>>(P, dg_ops<NP, NQ>(ctx));
+  ev_end(ctx);
+  ++ctx->launches;
+  CK(cudaGetLastError());
+  return NSFR_OK;
+}
+
+#define NSFR_DG_DISPATCH(fn, args)                                  \
+  switch (ctx->N * 16 + ctx->NQ) {                                  \
+    case 4 * 16 + 4: return fn<4, 4> args;                          \
+    case 4 * 16 + 5: return fn<4, 5> args;                          \
+    case 4 * 16 + 6: return fn<4, 6> args;                          \
+    case 5 * 16 + 5: return fn<5, 5> args;                          \
+    case 5 * 16 + 6: return fn<5, 6> args;                          \
+    case 5 * 16 + 7: return fn<5, 7> args;                          \
+    case 6 * 16 + 6: return fn<6, 6> args;                          \
+    case 6 * 16 + 7: return fn<6, 7> args;                          \
+    case 6 * 16 + 8: return fn<6, 8> args;                          \
+  }                                                                 \
+  ctx->msg = "DG: unsupported (p, overint)";                        \
+  return NSFR_E_DIM
+
+int dg_states(nsfr_gpu_ctx* ctx, const double* u, bool lam) { NSFR_DG_DISPATCH(launch_dg_states, (ctx, u, lam)); }
+int dg_residual(nsfr_gpu_ctx* ctx, int stage, const double* us, double* uo) {
+  NSFR_DG_DISPATCH(launch_dg_residual, (ctx, stage, us, uo));
+}
+
 // z-face halo exchange with the two slab neighbours
 int exchange(nsfr_gpu_ctx* ctx) {
   if (!ctx->comm) return NSFR_OK;  // single rank, or external halo mode
@@ -304,30 +423,66 @@ int allreduce_sum(nsfr_gpu_ctx* ctx, double* d, int n) {
   return NSFR_OK;
 }
 
-// K1 of d_un with lambda_max (the step pipeline's prologue)
+// K1 of d_un with lambda_max (the step pipeline's prologue); DG: KD1 face states
 int project_state(nsfr_gpu_ctx* ctx) {
   k_step_begin<<<1, 1, 0, ctx->st>>>(ctx->d_step);
   ++ctx->launches;
-  if (int rc = project(ctx, ctx->d_un, true)) return rc;
+  if (ctx->dg) {
+    if (int rc = dg_states(ctx, ctx->d_un, true)) return rc;
+  } else if (int rc = project(ctx, ctx->d_un, true)) {
+    return rc;
+  }
   ctx->proj_valid = true;
   return NSFR_OK;
 }
 
-int ensure_projected(nsfr_gpu_ctx* ctx) { return ctx->proj_valid ? NSFR_OK : project_state(ctx); }
+// (DG steps start with their own face-state pass: nothing to cache)
+int ensure_projected(nsfr_gpu_ctx* ctx) {
+  return ctx->proj_valid || ctx->dg ? NSFR_OK : project_state(ctx);
+}
 
 // one full residual of d_un into d_rhs (stage 0)
 int rhs_of_state(nsfr_gpu_ctx* ctx, bool entropy) {
   if (int rc = project_state(ctx)) return rc;
   if (int rc = exchange(ctx)) return rc;
+  if (ctx->dg) return dg_residual(ctx, 0, ctx->d_un, nullptr);
   if (int rc = residual(ctx)) return rc;
   return update(ctx, 0, entropy);
+}
+
+// DG RK4 step: KD1 (face states of the stage state, lambda at stage 1) ->
+// halo -> KD2 (residual, WA inverse, stage update in u_hat space), 4 times
+int enqueue_step_dg(nsfr_gpu_ctx* ctx, bool fixed_dt) {
+  k_step_begin<<<1, 1, 0, ctx->st>>>(ctx->d_step);
+  ++ctx->launches;
+  if (int rc = dg_states(ctx, ctx->d_un, !fixed_dt)) return rc;
+  if (!fixed_dt) {
+    if (ctx->comm)
+      NK(ncclAllReduce(&ctx->d_step->lam_bits, &ctx->d_step->lam_bits, 1, ncclUint64, ncclMax,
+                       ctx->comm, ctx->st));
+    k_step_dt<<<1, 1, 0, ctx->st>>>(ctx->d_step);
+    ++ctx->launches;
+  }
+  for (int stage = 1; stage <= 4; ++stage) {
+    if (stage > 1)
+      if (int rc = dg_states(ctx, ctx->d_dgus, false)) return rc;
+    if (int rc = exchange(ctx)) return rc;
+    if (int rc = dg_residual(ctx, stage, stage == 1 ? ctx->d_un : ctx->d_dgus, ctx->d_dgus)) return rc;
+  }
+  k_step_end<<<1, 1, 0, ctx->st>>>(ctx->d_step);
+  ++ctx->launches;
+  CK(cudaGetLastError());
+  ctx->proj_valid = false;
+  return NSFR_OK;
 }
 
 // Enqueue one RK4 step (no host sync), graph-capturable: needs the projection
 // of d_un in place (ensure_projected) and leaves the projection of u_{n+1}.
 // fixed_dt: dt already in d_step.
 constexpr long long kLaunchesPerStep = 1 + 4 * 2 + 1;
+long long launches_per_step(const nsfr_gpu_ctx* ctx) { return ctx->dg ? 1 + 1 + 1 + 4 + 3 + 1 : kLaunchesPerStep; }
 int enqueue_step(nsfr_gpu_ctx* ctx, bool fixed_dt) {
+  if (ctx->dg) return enqueue_step_dg(ctx, fixed_dt);
   if (!fixed_dt) {
     if (ctx->comm)
       NK(ncclAllReduce(&ctx->d_step->lam_bits, &ctx->d_step->lam_bits, 1, ncclUint64, ncclMax,
@@ -419,7 +574,7 @@ int setup_kernel_smem(nsfr_gpu_ctx* ctx, size_t bytes, const void* fn) {
 
 // u_hat <-> u_q (k_convert): to_quad applies chi^3, else Pi^3
 int convert_state(nsfr_gpu_ctx* ctx, const double* in, double* out, bool to_quad) {
-  const size_t smem = sizeof(double) * 4 * nsol(ctx);
+  const size_t smem = sizeof(double) * 4 * std::max(nsol(ctx), nquad(ctx));
   k_convert<<<ctx->E, 128, smem, ctx->st>>>(ctx->d_tab, in, out, ctx->E, to_quad ? 1 : 0);
   ++ctx->launches;
   CK(cudaGetLastError());
@@ -427,7 +582,7 @@ int convert_state(nsfr_gpu_ctx* ctx, const double* in, double* out, bool to_quad
 }
 
 int build_metrics(nsfr_gpu_ctx* ctx) {
-  const int g = ctx->tab.g, n = ctx->N, G3 = g * g * g, N3 = n * n * n;
+  const int g = ctx->tab.g, n = ctx->NQ, G3 = g * g * g, N3 = n * n * n;
   const int M = std::max(g, n), M3 = M * M * M;
   const size_t smem = sizeof(double) * (13 * G3 + 2 * M3 + 20 * N3);
   if (int rc = setup_kernel_smem(ctx, smem, (const void*)k_metrics)) return rc;
@@ -489,7 +644,15 @@ int nsfr_gpu_create(const nsfr_gpu_setup* setup, nsfr_gpu_ctx** out) {
     ctx->msg = "nsfr_gpu_create: dimension/configuration out of range (p in [2,6], 0<=k0<k1<=m)";
     return fail(NSFR_E_DIM);
   }
+  ctx->dg = (s.scheme == NSFR_SCHEME_DG);
+  if (!(s.scheme == NSFR_SCHEME_NSFR || ctx->dg) || (!ctx->dg && s.overint != 0) ||
+      (ctx->dg && (s.p < 3 || s.p > 5 || s.overint < 0 || s.overint > 2))) {
+    ctx->msg = "nsfr_gpu_create: scheme/overint out of range (NSFR: overint 0; DG: p in [3,5], "
+               "overint in [0,2])";
+    return fail(NSFR_E_DIM);
+  }
   ctx->N = s.p + 1;
+  ctx->NQ = s.p + 1 + s.overint;
   ctx->m = s.m;
   ctx->k0 = s.k0;
   ctx->k1 = s.k1;
@@ -502,7 +665,7 @@ int nsfr_gpu_create(const nsfr_gpu_setup* setup, nsfr_gpu_ctx** out) {
     return fail(NSFR_E_DIM);
   }
   const char* why = nullptr;
-  if (!build_tables(s.p, s.quad_kind, s.c1d, s.grid_degree, ctx->tab, &why)) {
+  if (!build_tables(s.p, s.quad_kind, s.overint, s.c1d, s.grid_degree, ctx->tab, &why)) {
     ctx->msg = why;
     return fail(NSFR_E_DIM);
   }
@@ -517,10 +680,11 @@ int nsfr_gpu_create(const nsfr_gpu_setup* setup, nsfr_gpu_ctx** out) {
   DevTables dt;
   fill_dev_tables(ctx->tab, s.tables && s.tables->interp ? s.tables : nullptr, dt);
   ctx->htab = dt;
-  const size_t ns = state_count(ctx), n3 = static_cast<size_t>(ctx->E) * nsol(ctx);
-  const size_t ntr = static_cast<size_t>(ctx->E) * 6 * NS * ctx->N * ctx->N;
+  const size_t ns = state_count(ctx), n3 = static_cast<size_t>(ctx->E) * nquad(ctx);
+  const size_t ntr = static_cast<size_t>(ctx->E) * 6 * NS * ctx->NQ * ctx->NQ;
+  const size_t nscr = static_cast<size_t>(ctx->E) * NS * std::max(nsol(ctx), nquad(ctx));
   auto alloc = [&](double** p, size_t n) { return cudaMalloc(p, sizeof(double) * std::max<size_t>(n, 1)); };
-  if (cudaMalloc(&ctx->d_tab, sizeof(DevTables)) || alloc(&ctx->d_un, ns) || alloc(&ctx->d_vol, ns) ||
+  if (cudaMalloc(&ctx->d_tab, sizeof(DevTables)) || alloc(&ctx->d_un, ns) || alloc(&ctx->d_vol, nscr) ||
       alloc(&ctx->d_acc, ns) || alloc(&ctx->d_rhs, ns) || alloc(&ctx->d_utv, 6 * n3) ||
       alloc(&ctx->d_tr, ntr) || alloc(&ctx->d_facc, ntr) || alloc(&ctx->d_cof, 9 * n3) || alloc(&ctx->d_jac, n3) ||
       alloc(&ctx->d_wj, n3) || alloc(&ctx->d_dS, ctx->E) || alloc(&ctx->d_part, 2 * (size_t)ctx->E) ||
@@ -530,7 +694,7 @@ int nsfr_gpu_create(const nsfr_gpu_setup* setup, nsfr_gpu_ctx** out) {
     ctx->msg = "nsfr_gpu_create: device allocation failed";
     return fail(NSFR_E_CUDA);
   }
-  if (s.entropy_diag && alloc(&ctx->d_vhat, ns)) {
+  if ((s.entropy_diag && alloc(&ctx->d_vhat, ns)) || (ctx->dg && alloc(&ctx->d_dgus, ns))) {
     ctx->msg = "nsfr_gpu_create: device allocation failed";
     return fail(NSFR_E_CUDA);
   }
@@ -543,9 +707,10 @@ int nsfr_gpu_create(const nsfr_gpu_setup* setup, nsfr_gpu_ctx** out) {
     }
     ctx->peer_lo = plan.peer_lo;
     ctx->peer_hi = plan.peer_hi;
-    ctx->halo_count = plan.count;
-    if (alloc(&ctx->d_send_lo, plan.count) || alloc(&ctx->d_send_hi, plan.count) ||
-        alloc(&ctx->d_halo_lo, plan.count) || alloc(&ctx->d_halo_hi, plan.count)) {
+    ctx->halo_count = static_cast<long long>(s.m) * s.m * NS * ctx->NQ * ctx->NQ;
+    const size_t hc = static_cast<size_t>(ctx->halo_count);
+    if (alloc(&ctx->d_send_lo, hc) || alloc(&ctx->d_send_hi, hc) || alloc(&ctx->d_halo_lo, hc) ||
+        alloc(&ctx->d_halo_hi, hc)) {
       ctx->msg = "nsfr_gpu_create: halo allocation failed";
       return fail(NSFR_E_CUDA);
     }
@@ -571,16 +736,16 @@ int nsfr_gpu_create(const nsfr_gpu_setup* setup, nsfr_gpu_ctx** out) {
   }
   if (setup->jac_vol && setup->cof_vol) {
     // caller-built metrics (ElementMetrics layout [e][q][9]) -> 0.5 C as [e][9][q], wj = w J
-    const int N3 = static_cast<int>(nsol(ctx));
+    const int N3 = static_cast<int>(nquad(ctx)), nq = ctx->NQ;
     std::vector<double> cof(9 * n3), wj(n3);
-    const auto& wq = (s.tables && s.tables->wq) ? std::vector<double>(s.tables->wq, s.tables->wq + ctx->N)
+    const auto& wq = (s.tables && s.tables->wq) ? std::vector<double>(s.tables->wq, s.tables->wq + nq)
                                                 : ctx->tab.wq;
     for (int e = 0; e < ctx->E; ++e)
       for (int q = 0; q < N3; ++q) {
         for (int c = 0; c < 9; ++c)
           cof[(static_cast<size_t>(e) * 9 + c) * N3 + q] =
               0.5 * setup->cof_vol[(static_cast<size_t>(e) * N3 + q) * 9 + c];
-        const int i = q % ctx->N, j = (q / ctx->N) % ctx->N, k = q / (ctx->N * ctx->N);
+        const int i = q % nq, j = (q / nq) % nq, k = q / (nq * nq);
         double w = wq[i];
         w *= wq[j];
         w *= wq[k];
@@ -610,7 +775,7 @@ int nsfr_gpu_destroy(nsfr_gpu_ctx* ctx) {
   if (ctx->graph) cudaGraphExecDestroy(ctx->graph);
   for (auto e : ctx->ev_pool) cudaEventDestroy(e);
   if (ctx->comm) ncclCommDestroy(ctx->comm);
-  double* bufs[] = {ctx->d_un,  ctx->d_vol,  ctx->d_facc, ctx->d_acc,  ctx->d_rhs,     ctx->d_utv,     ctx->d_tr,
+  double* bufs[] = {ctx->d_dgus, ctx->d_un,  ctx->d_vol,  ctx->d_facc, ctx->d_acc,  ctx->d_rhs,     ctx->d_utv,     ctx->d_tr,
                     ctx->d_cof, ctx->d_jac,  ctx->d_wj,   ctx->d_vhat,    ctx->d_dS,      ctx->d_part,
                     ctx->d_red, ctx->d_send_lo, ctx->d_send_hi, ctx->d_halo_lo, ctx->d_halo_hi};
   for (double* b : bufs)
@@ -650,8 +815,8 @@ int nsfr_gpu_get_tables(nsfr_gpu_ctx* ctx, double* out, int cap) {
 }
 
 int nsfr_gpu_get_metrics(nsfr_gpu_ctx* ctx, double* jac, double* cof) {
-  const size_t n3 = static_cast<size_t>(ctx->E) * nsol(ctx);
-  const int N3 = static_cast<int>(nsol(ctx));
+  const size_t n3 = static_cast<size_t>(ctx->E) * nquad(ctx);
+  const int N3 = static_cast<int>(nquad(ctx));
   CK(cudaStreamSynchronize(ctx->st));
   if (jac) CK(cudaMemcpy(jac, ctx->d_jac, sizeof(double) * n3, cudaMemcpyDeviceToHost));
   if (cof) {
@@ -667,6 +832,7 @@ int nsfr_gpu_get_metrics(nsfr_gpu_ctx* ctx, double* jac, double* cof) {
 
 int nsfr_gpu_set_state(nsfr_gpu_ctx* ctx, const double* u) {
   ctx->proj_valid = false;
+  if (ctx->dg) return nsfr_gpu_set_state_q(ctx, u);  // DG carries u_hat itself
   // u_hat -> scratch (d_vol is dead between steps) -> u_q = chi^3 u_hat
   CK(cudaMemcpyAsync(ctx->d_vol, u, sizeof(double) * state_count(ctx), cudaMemcpyHostToDevice, ctx->st));
   if (int rc = convert_state(ctx, ctx->d_vol, ctx->d_un, true)) return rc;
@@ -675,6 +841,7 @@ int nsfr_gpu_set_state(nsfr_gpu_ctx* ctx, const double* u) {
 }
 
 int nsfr_gpu_get_state(nsfr_gpu_ctx* ctx, double* u) {
+  if (ctx->dg) return nsfr_gpu_get_state_q(ctx, u);
   if (int rc = convert_state(ctx, ctx->d_un, ctx->d_vol, false)) return rc;
   CK(cudaMemcpyAsync(u, ctx->d_vol, sizeof(double) * state_count(ctx), cudaMemcpyDeviceToHost, ctx->st));
   CK(cudaStreamSynchronize(ctx->st));
@@ -701,7 +868,7 @@ int nsfr_gpu_init_case(nsfr_gpu_ctx* ctx, int kind) {
   if (int rc = setup_kernel_smem(ctx, smem, (const void*)k_init)) return rc;
   InitParams P{};
   P.tab = ctx->d_tab;
-  P.u = ctx->d_vol;  // u_hat at the solution nodes, converted to u_q below
+  P.u = ctx->dg ? ctx->d_un : ctx->d_vol;  // u_hat at the solution nodes (NSFR: then u_q)
   P.E = ctx->E;
   P.m = ctx->m;
   P.k0 = ctx->k0;
@@ -715,7 +882,8 @@ int nsfr_gpu_init_case(nsfr_gpu_ctx* ctx, int kind) {
   k_init<<<ctx->E, 128, smem, ctx->st>>>(P);
   ++ctx->launches;
   CK(cudaGetLastError());
-  if (int rc = convert_state(ctx, ctx->d_vol, ctx->d_un, true)) return rc;
+  if (!ctx->dg)
+    if (int rc = convert_state(ctx, ctx->d_vol, ctx->d_un, true)) return rc;
   return nsfr_gpu_set_time(ctx, 0.0);
 }
 
@@ -734,6 +902,10 @@ int nsfr_gpu_get_time(nsfr_gpu_ctx* ctx, double* t) {
 
 int nsfr_gpu_rhs(nsfr_gpu_ctx* ctx, double* dudt, double* entropy_change) {
   const bool ent = entropy_change != nullptr;
+  if (ent && ctx->dg) {
+    ctx->msg = "entropy change: defined for the NSFR scheme only";
+    return NSFR_E_CONFIG;
+  }
   if (ent && !ctx->d_vhat) {
     ctx->msg = "entropy change needs setup.entropy_diag = 1";
     return NSFR_E_CONFIG;
@@ -754,7 +926,7 @@ int nsfr_gpu_entropy_change(nsfr_gpu_ctx* ctx, double* out) { return nsfr_gpu_rh
 
 int nsfr_gpu_get_traces(nsfr_gpu_ctx* ctx, double* traces) {
   CK(cudaStreamSynchronize(ctx->st));
-  CK(cudaMemcpy(traces, ctx->d_tr, sizeof(double) * ctx->E * 6 * NS * ctx->N * ctx->N,
+  CK(cudaMemcpy(traces, ctx->d_tr, sizeof(double) * ctx->E * 6 * NS * ctx->NQ * ctx->NQ,
                 cudaMemcpyDeviceToHost));
   return NSFR_OK;
 }
@@ -816,7 +988,7 @@ int nsfr_gpu_advance(nsfr_gpu_ctx* ctx, int nsteps, double cfl, double t_final, 
       if (int rc = enqueue_step(ctx, false)) return rc;
     } else {
       CK(cudaGraphLaunch(ctx->graph, ctx->st));
-      ctx->launches += kLaunchesPerStep;
+      ctx->launches += launches_per_step(ctx);
     }
     if (chunk < nsteps && (i + 1) % chunk == 0) {
       if (int rc = sync_check(ctx)) return rc;
@@ -829,14 +1001,16 @@ int nsfr_gpu_advance(nsfr_gpu_ctx* ctx, int nsteps, double cfl, double t_final, 
 }
 
 int nsfr_gpu_l2_error(nsfr_gpu_ctx* ctx, int kind, double out2[2]) {
-  const int g = ctx->tab.g, n = ctx->N, G3 = g * g * g, N3 = n * n * n;
+  const int g = ctx->tab.g, n = ctx->NQ, G3 = g * g * g, N3 = n * n * n;
   const int M = std::max(g, n), M3 = M * M * M;
   const size_t smem = sizeof(double) * (3 * G3 + 2 * M3 + 10 * N3);
   if (int rc = setup_kernel_smem(ctx, smem, (const void*)k_l2)) return rc;
   if (int rc = sync_check(ctx)) return rc;
+  if (ctx->dg)  // u at the quadrature nodes: chi^3 u_hat into the scratch
+    if (int rc = convert_state(ctx, ctx->d_un, ctx->d_vol, true)) return rc;
   L2Params P{};
   P.tab = ctx->d_tab;
-  P.u = ctx->d_un;
+  P.u = ctx->dg ? ctx->d_vol : ctx->d_un;
   P.jac = ctx->d_jac;
   P.part = ctx->d_part;
   P.E = ctx->E;
@@ -864,10 +1038,13 @@ int nsfr_gpu_l2_error(nsfr_gpu_ctx* ctx, int kind, double out2[2]) {
 // mass, momentum, energy and entropy-function totals of the current state
 static int totals(nsfr_gpu_ctx* ctx, double out6[NTOT]) {
   if (int rc = sync_check(ctx)) return rc;
-  // per-element partials into d_vol (dead between steps), then fixed-order sums
-  k_totals<<<ctx->E, 128, 0, ctx->st>>>(ctx->d_tab, ctx->d_un, ctx->d_jac, ctx->s.gamma, ctx->d_vol,
-                                         ctx->E);
-  k_reduce<<<1, 1024, 0, ctx->st>>>(ctx->d_vol, ctx->E, NTOT, ctx->d_red);
+  // u_q (DG: chi^3 u_hat into d_vol); per-element partials into d_acc (dead
+  // between steps), then fixed-order sums
+  if (ctx->dg)
+    if (int rc = convert_state(ctx, ctx->d_un, ctx->d_vol, true)) return rc;
+  k_totals<<<ctx->E, 128, 0, ctx->st>>>(ctx->d_tab, ctx->dg ? ctx->d_vol : ctx->d_un, ctx->d_jac,
+                                         ctx->s.gamma, ctx->d_acc, ctx->E);
+  k_reduce<<<1, 1024, 0, ctx->st>>>(ctx->d_acc, ctx->E, NTOT, ctx->d_red);
   ctx->launches += 2;
   CK(cudaGetLastError());
   if (int rc = allreduce_sum(ctx, ctx->d_red, NTOT)) return rc;
@@ -909,11 +1086,19 @@ int nsfr_gpu_halo_set(nsfr_gpu_ctx* ctx, const double* recv_lo, const double* re
 }
 
 int nsfr_gpu_project(nsfr_gpu_ctx* ctx) {
+  if (ctx->dg) {
+    ctx->msg = "project: defined for the NSFR scheme only";
+    return NSFR_E_CONFIG;
+  }
   if (int rc = project_state(ctx)) return rc;
   return sync_check(ctx);
 }
 
 int nsfr_gpu_residual(nsfr_gpu_ctx* ctx, double* dudt, double* entropy_change) {
+  if (ctx->dg) {
+    ctx->msg = "residual: defined for the NSFR scheme only";
+    return NSFR_E_CONFIG;
+  }
   const bool ent = entropy_change != nullptr;
   if (ent && !ctx->d_vhat) {
     ctx->msg = "entropy change needs setup.entropy_diag = 1";
@@ -938,6 +1123,10 @@ int nsfr_gpu_residual(nsfr_gpu_ctx* ctx, double* dudt, double* entropy_change) {
 }
 
 int nsfr_gpu_stage(nsfr_gpu_ctx* ctx, int stage, double dt) {
+  if (ctx->dg) {
+    ctx->msg = "stage: defined for the NSFR scheme only";
+    return NSFR_E_CONFIG;
+  }
   if (stage < 1 || stage > 4) {
     ctx->msg = "stage must be 1..4";
     return NSFR_E_DIM;
@@ -976,6 +1165,10 @@ int nsfr_gpu_entropy_total(nsfr_gpu_ctx* ctx, double* out) {
 }
 
 int nsfr_gpu_ke_volume(nsfr_gpu_ctx* ctx, double* out) {
+  if (ctx->dg) {
+    ctx->msg = "ke_volume: defined for the NSFR scheme only";
+    return NSFR_E_CONFIG;
+  }
   // volume rows of (flux - pressure work) for the projection of u_n, then
   // sum v_KE . rows; partials go to d_rhs (the rows occupy d_vol)
   if (int rc = project_state(ctx)) return rc;
@@ -1018,7 +1211,7 @@ int nsfr_gpu_time_steps(nsfr_gpu_ctx* ctx, int nsteps, double cfl, double* step_
       rc = enqueue_step(ctx, false);
     } else {
       CK(cudaGraphLaunch(ctx->graph, ctx->st));
-      ctx->launches += kLaunchesPerStep;
+      ctx->launches += launches_per_step(ctx);
     }
   }
   CK(cudaEventRecord(b, ctx->st));

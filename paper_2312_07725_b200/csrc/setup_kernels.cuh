@@ -274,16 +274,19 @@ __global__ void k_convert(const DevTables* tab, const double* in, double* out, i
   const int e = blockIdx.x;
   if (e >= E) return;
   const int tid = threadIdx.x, nthr = blockDim.x;
-  const int n = T.nq, N3 = n * n * n;
+  const int np = T.np, nq = T.nq;
+  const int nin = to_quad ? np : nq, nout = to_quad ? nq : np;  // chi: nq x np, Pi: np x nq
+  const int IN3 = nin * nin * nin, OUT3 = nout * nout * nout;
+  const int M = np > nq ? np : nq, M3 = M * M * M;
   double* src = sm;
-  double* t1 = src + N3;
-  double* t2 = t1 + N3;
-  double* dst = t2 + N3;
+  double* t1 = src + M3;
+  double* t2 = t1 + M3;
+  double* dst = t2 + M3;
   for (int s = 0; s < NS; ++s) {
-    for (int i = tid; i < N3; i += nthr) src[i] = in[((size_t)e * NS + s) * N3 + i];
+    for (int i = tid; i < IN3; i += nthr) src[i] = in[((size_t)e * NS + s) * IN3 + i];
     __syncthreads();
-    tp3_rt(to_quad ? T.interp : T.proj, n, n, src, t1, t2, dst, tid, nthr);
-    for (int i = tid; i < N3; i += nthr) out[((size_t)e * NS + s) * N3 + i] = dst[i];
+    tp3_rt(to_quad ? T.interp : T.proj, nout, nin, src, t1, t2, dst, tid, nthr);
+    for (int i = tid; i < OUT3; i += nthr) out[((size_t)e * NS + s) * OUT3 + i] = dst[i];
     __syncthreads();
   }
 }

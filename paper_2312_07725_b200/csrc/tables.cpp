@@ -189,14 +189,14 @@ double c_plus(int p) {
   }
 }
 
-bool build_tables(int p, int quad_kind, double c1d, int grid_degree, Tables1D& t,
+bool build_tables(int p, int quad_kind, int overint, double c1d, int grid_degree, Tables1D& t,
                   const char** msg) {
-  const int np = p + 1, nq = p + 1;
+  const int np = p + 1, nq = p + 1 + overint;  // fr_operators.cpp:93
   t.p = p;
   t.np = np;
   t.nq = nq;
   const Rule1D sol = make_rule(1, np), quad = make_rule(quad_kind, nq);
-  const bool collocated = (quad_kind == 1);
+  const bool collocated = (quad_kind == 1 && nq == np);
   const Bary lb(sol.x);
   t.sol_nodes = sol.x;
   t.quad_nodes = quad.x;

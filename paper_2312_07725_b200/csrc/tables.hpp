@@ -37,7 +37,9 @@ struct Tables1D {
 };
 
 // Returns false (with msg) on a singular system or a negative c.
-bool build_tables(int p, int quad_kind, double c1d, int grid_degree, Tables1D& t, const char** msg);
+// n_q = p + 1 + overint volume quadrature nodes per direction (fr_operators.cpp:89-113)
+bool build_tables(int p, int quad_kind, int overint, double c1d, int grid_degree, Tables1D& t,
+                  const char** msg);
 
 double c_plus(int p);  // fr_operators.cpp:36-46 (halved von Neumann values); <0 if absent
 

@@ -65,6 +65,9 @@ class _Tables(C.Structure):
                 ("interp", "proj", "fr_proj", "skew", "bound_flux", "bound_sol", "wq")]
 
 
+SCHEMES = {"nsfr": 0, "dg": 1}
+
+
 class _Setup(C.Structure):
     _fields_ = [
         ("p", C.c_int), ("quad_kind", C.c_int), ("c1d", C.c_double), ("gamma", C.c_double),
@@ -74,6 +77,7 @@ class _Setup(C.Structure):
         ("entropy_diag", C.c_int), ("tables", C.POINTER(_Tables)),
         ("jac_vol", C.POINTER(C.c_double)), ("cof_vol", C.POINTER(C.c_double)),
         ("nccl_id", C.c_void_p), ("rank", C.c_int), ("nranks", C.c_int),
+        ("scheme", C.c_int), ("overint", C.c_int),
     ]
 
 
@@ -195,6 +199,8 @@ class SolverConfig:
     nranks: int = 1
     x_left: float | None = None
     x_right: float | None = None
+    scheme: str = "nsfr"            # "nsfr" (hot path) or "dg" (conservative strong-form DG)
+    overint: int = 0                # extra quadrature nodes, n_q = p+1+overint (dg only)
 
     def domain(self):
         if self.x_left is not None:
@@ -238,13 +244,16 @@ class GpuSolver:
                    cfg.beta, cfg.length_scale,
                    cfg.p + 1 if cfg.grid_degree is None else cfg.grid_degree, cfg.device,
                    int(cfg.entropy_diag), tab_ptr, _ptr(jac), _ptr(cof),
-                   C.cast(idbuf, C.c_void_p) if idbuf is not None else None, cfg.rank, cfg.nranks)
+                   C.cast(idbuf, C.c_void_p) if idbuf is not None else None, cfg.rank, cfg.nranks,
+                   SCHEMES[cfg.scheme], cfg.overint)
         h = C.c_void_p()
         rc = self.lib.nsfr_gpu_create(C.byref(s), C.byref(h))
         if rc:
             raise _ERRORS.get(rc, NsfrError)(self.lib.nsfr_gpu_create_error().decode())
         self.ctx = h
-        self.n = cfg.p + 1
+        self.n = cfg.p + 1                 # solution nodes per direction
+        self.nq = cfg.p + 1 + cfg.overint  # volume quadrature nodes per direction
+        self.nquad = self.nq ** 3
         self.ne = cfg.m * cfg.m * (k1 - k0)
         self.nsol = self.n ** 3
 
@@ -282,12 +291,12 @@ class GpuSolver:
 
     # --- setup products -------------------------------------------------------
     def tables(self) -> dict[str, np.ndarray]:
-        n = self.n
+        n, q = self.n, self.nq
         buf = np.zeros(4096)
         cnt = self.lib.nsfr_gpu_get_tables(self.ctx, _ptr(buf), buf.size)
-        shapes = [("interp", (n, n)), ("proj", (n, n)), ("fr_proj", (n, n)), ("skew", (n, n)),
-                  ("bound_flux", (2, n)), ("bound_sol", (2, n)), ("wq", (n,)), ("quad_nodes", (n,)),
-                  ("sol_nodes", (n,)), ("mmass1d", (n, n)), ("quad_diff", (n, n))]
+        shapes = [("interp", (q, n)), ("proj", (n, q)), ("fr_proj", (n, q)), ("skew", (q, q)),
+                  ("bound_flux", (2, q)), ("bound_sol", (2, n)), ("wq", (q,)), ("quad_nodes", (q,)),
+                  ("sol_nodes", (n,)), ("mmass1d", (n, n)), ("quad_diff", (q, q))]
         out, pos = {}, 0
         for name, shp in shapes:
             sz = int(np.prod(shp))
@@ -297,8 +306,8 @@ class GpuSolver:
         return out
 
     def metrics(self):
-        jac = np.zeros((self.ne, self.nsol))
-        cof = np.zeros((self.ne, self.nsol, 9))
+        jac = np.zeros((self.ne, self.nquad))
+        cof = np.zeros((self.ne, self.nquad, 9))
         self._check(self.lib.nsfr_gpu_get_metrics(self.ctx, _ptr(jac), _ptr(cof)))
         return jac, cof
 
@@ -348,7 +357,7 @@ class GpuSolver:
         return (out, float(ds[0])) if entropy else out
 
     def traces(self) -> np.ndarray:
-        tr = np.zeros((self.ne, 6, 5, self.n * self.n))
+        tr = np.zeros((self.ne, 6, 5, self.nq * self.nq))
         self._check(self.lib.nsfr_gpu_get_traces(self.ctx, _ptr(tr)))
         return tr
 
@@ -395,7 +404,7 @@ class GpuSolver:
     # --- stage-level driving / external halo transport (nranks > 1, no NCCL id)
     @property
     def halo_shape(self):
-        return (self.cfg.m * self.cfg.m, 5, self.n * self.n)
+        return (self.cfg.m * self.cfg.m, 5, self.nq * self.nq)
 
     def halo_get(self):
         """The two send planes (face 4 of plane k0, face 5 of plane k1-1)."""
