@@ -105,16 +105,20 @@ struct DgOps {
 template <int NP, int NQ>
 struct DgCfg {
   static constexpr int P3 = NP * NP * NP, Q3 = NQ * NQ * NQ, Q2 = NQ * NQ;
-  static constexpr int EPB = Q3 <= 64 ? 2 : 1;
   static constexpr int THREADS = 256;
+  // KD2 per-element shared memory (doubles), see below; elements per CTA fill
+  // the 256 threads in the pointwise phases within ~112 KB (2 CTAs per SM)
+  static constexpr int R_EL = 5 * P3 + 9 * Q3 + Q3 + 5 * Q3 + 15 * Q3 + 5 * Q3 + 60 * Q2;
+  static constexpr int E_FILL = 256 / Q3 > 1 ? 256 / Q3 : 1;
+  static constexpr int E_SMEM = (112 * 1024) / (R_EL * 8) > 1 ? (112 * 1024) / (R_EL * 8) : 1;
+  static constexpr int EPB = E_FILL < E_SMEM ? E_FILL : E_SMEM;
   // KD1 smem: U (5 P3), T1 (5 NQ NP^2), T2 (5 NQ^2 NP), six face buffers of
   // 5 x 2 NQ^2 (A1, A2, B1 intermediates; F0, F1, F2 results), UQ (5 Q3)
   static constexpr int S_PER_EL = 5 * P3 + 5 * NQ * NP * NP + 5 * NQ * NQ * NP + 60 * Q2 + 5 * Q3;
   static constexpr int S_SMEM = EPB * S_PER_EL * 8;
   // KD2 smem: U, CH (9 Q3), WJ (Q3), Q (5 Q3), FR (15 Q3, also S1/S2 and tail R1/R2),
   // VOL (5 Q3), FACC (30 Q2), G (30 Q2)
-  static constexpr int R_PER_EL = 5 * P3 + 9 * Q3 + Q3 + 5 * Q3 + 15 * Q3 + 5 * Q3 + 60 * Q2;
-  static constexpr int R_SMEM = EPB * R_PER_EL * 8;
+  static constexpr int R_SMEM = EPB * R_EL * 8;
 };
 
 // KD1: face states and lambda
@@ -333,17 +337,16 @@ __global__ void __launch_bounds__(256, 2) k_dg_residual(DgResParams P, DgOps<NP,
       dst[r * Q2] = (dst[r * Q2] + acc) * (wij * O.wq[r]);
     }
   }
-  // face terms: one thread per line (b, dir, t1, t2), both ends
-  for (int it = tid; it < nb * 3 * Q2; it += nthr) {
-    const int b = it / (3 * Q2), r = it - b * 3 * Q2, dir = r / Q2, k = r - dir * Q2;
+  // face terms: one thread per (b, face f = 2 dir + side, node k) at the end of line k
+  for (int it = tid; it < nb * 6 * Q2; it += nthr) {
+    const int b = it / (6 * Q2), r = it - b * 6 * Q2, f = r / Q2, k = r - f * Q2;
+    const int dir = f >> 1, side = f & 1;
     const int t1 = k % NQ, t2 = k / NQ, e = e0 + b;
     const int stride = dir == 0 ? 1 : (dir == 1 ? NQ : Q2);
     const int base = dir == 0 ? NQ * (t1 + NQ * t2) : (dir == 1 ? t1 + Q2 * t2 : t1 + NQ * t2);
     const double wt = O.wq[t1] * O.wq[t2];
     const double* Cb = CH + b * 9 * Q3;
-#pragma unroll 1
-    for (int side = 0; side < 2; ++side) {
-      const int f = 2 * dir + side;
+    {
       const double sign = side ? 1.0 : -1.0;
       double fi[NS], cf0 = 0.0, cf1 = 0.0, cf2 = 0.0;
 #pragma unroll
