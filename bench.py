@@ -101,6 +101,17 @@ def dist_env():
     return world, rank, local
 
 
+def cpu_model() -> str:
+    try:
+        with open("/proc/cpuinfo") as f:
+            for line in f:
+                if line.startswith("model name"):
+                    return line.split(":", 1)[1].strip()
+    except OSError:
+        pass
+    return "unknown"
+
+
 def cpu_reference_run(steps: int, warmup: int, threads: int):
     """Reference CPU path (oracle/_ref) RK4 steps on the bounded sample; returns
     (DOF-updates/s, seconds per step, kind, cores)."""
@@ -135,7 +146,8 @@ def run_reference_arm(args):
         "higher_is_better": True, "scaling": "strong", "vs_baseline": None, "dtype": "f64",
         "data": "synthetic (analytic isentropic vortex IC)",
         "config": {"workload": WORKLOAD, "p": P_DEG, "elements": f"{CPU_SAMPLE_M}^3 sample of 128^3"},
-        "cpu_baseline": {"value": val, "unit": UNIT, "cores": cores, "kind": kind, "sample": sample},
+        "cpu_baseline": {"value": val, "unit": UNIT, "cores": cores, "kind": kind, "sample": sample,
+                         "cpu_model": cpu_model()},
         "e2e": {"value": val, "unit": UNIT, "h2d_bytes_per_step": 0, "d2h_bytes_per_step": 0},
     }), flush=True)
 
@@ -219,6 +231,7 @@ def run_gpu_arm(args):
     out = {
         "metric": METRIC, "value": value, "unit": UNIT, "n_gpus": world, "steps": args.steps,
         "warmup": args.warmup, "ms_per_step": ms_max / args.steps, "higher_is_better": True,
+        "node_updates_per_s": value / 5,  # the metric per node (5 states per node)
         "scaling": "strong", "vs_baseline": None, "dtype": "f64",
         "data": "synthetic (analytic isentropic vortex IC on the reference's warped grid)",
         "config": {"workload": WORKLOAD, "elements": f"{M}^3", "p": P_DEG, "c1d": C_PLUS4,
@@ -246,6 +259,7 @@ def run_gpu_arm(args):
         threads = os.cpu_count() or 1
         val, sec, kind, cores = cpu_reference_run(1, 1, threads)
         out["cpu_baseline"] = {"value": val, "unit": UNIT, "cores": cores, "kind": kind,
+                               "cpu_model": cpu_model(),
                                "sample": f"1 RK4 step (4 RHS) on a periodic {CPU_SAMPLE_M}^3 box, "
                                          f"same p=4/c_+/EC+Roe per-element work, {cores} threads"}
     g.close()
