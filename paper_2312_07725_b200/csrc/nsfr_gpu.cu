@@ -35,6 +35,8 @@ struct nsfr_gpu_ctx {
   unsigned* d_err = nullptr;
   unsigned* h_err = nullptr;    // pinned
   cudaStream_t st = nullptr;
+  cudaStream_t st_copy = nullptr;  // host<->device state transfers, chunk-pipelined with st
+  std::vector<cudaEvent_t> chunk_ev;
   ncclComm_t comm = nullptr;
   int rank = 0, nranks = 1, peer_lo = 0, peer_hi = 0;
   long long halo_count = 0;
@@ -572,12 +574,33 @@ int setup_kernel_smem(nsfr_gpu_ctx* ctx, size_t bytes, const void* fn) {
   return NSFR_OK;
 }
 
-// u_hat <-> u_q (k_convert): to_quad applies chi^3, else Pi^3
-int convert_state(nsfr_gpu_ctx* ctx, const double* in, double* out, bool to_quad) {
+// u_hat <-> u_q (k_convert) of elements [e0, e1): to_quad applies chi^3, else Pi^3
+int convert_range(nsfr_gpu_ctx* ctx, const double* in, double* out, bool to_quad, int e0, int e1) {
   const size_t smem = sizeof(double) * 4 * std::max(nsol(ctx), nquad(ctx));
-  k_convert<<<ctx->E, 128, smem, ctx->st>>>(ctx->d_tab, in, out, ctx->E, to_quad ? 1 : 0);
+  const size_t in_per = NS * (to_quad ? nsol(ctx) : nquad(ctx)), out_per = NS * (to_quad ? nquad(ctx) : nsol(ctx));
+  k_convert<<<e1 - e0, 128, smem, ctx->st>>>(ctx->d_tab, in + e0 * in_per, out + e0 * out_per, e1 - e0,
+                                             to_quad ? 1 : 0);
   ++ctx->launches;
   CK(cudaGetLastError());
+  return NSFR_OK;
+}
+
+int convert_state(nsfr_gpu_ctx* ctx, const double* in, double* out, bool to_quad) {
+  return convert_range(ctx, in, out, to_quad, 0, ctx->E);
+}
+
+// state transfers: ~64 MB chunks (at least one)
+int transfer_chunks(const nsfr_gpu_ctx* ctx) {
+  const size_t bytes = sizeof(double) * state_count(ctx);
+  return static_cast<int>(std::min<size_t>(64, std::max<size_t>(1, bytes >> 26)));
+}
+
+int ensure_chunk_events(nsfr_gpu_ctx* ctx, int n) {
+  while (static_cast<int>(ctx->chunk_ev.size()) < n) {
+    cudaEvent_t e;
+    CK(cudaEventCreateWithFlags(&e, cudaEventDisableTiming));
+    ctx->chunk_ev.push_back(e);
+  }
   return NSFR_OK;
 }
 
@@ -673,7 +696,8 @@ int nsfr_gpu_create(const nsfr_gpu_setup* setup, nsfr_gpu_ctx** out) {
     ctx->msg = "cudaSetDevice failed (no CUDA device?)";
     return fail(NSFR_E_CUDA);
   }
-  if (cudaStreamCreateWithFlags(&ctx->st, cudaStreamNonBlocking) != cudaSuccess) {
+  if (cudaStreamCreateWithFlags(&ctx->st, cudaStreamNonBlocking) != cudaSuccess ||
+      cudaStreamCreateWithFlags(&ctx->st_copy, cudaStreamNonBlocking) != cudaSuccess) {
     ctx->msg = "cudaStreamCreate failed (no CUDA device?)";
     return fail(NSFR_E_CUDA);
   }
@@ -785,6 +809,8 @@ int nsfr_gpu_destroy(nsfr_gpu_ctx* ctx) {
   if (ctx->d_err) cudaFree(ctx->d_err);
   if (ctx->h_step) cudaFreeHost(ctx->h_step);
   if (ctx->h_err) cudaFreeHost(ctx->h_err);
+  for (auto e : ctx->chunk_ev) cudaEventDestroy(e);
+  if (ctx->st_copy) cudaStreamDestroy(ctx->st_copy);
   if (ctx->st) cudaStreamDestroy(ctx->st);
   delete ctx;
   return NSFR_OK;
@@ -833,17 +859,44 @@ int nsfr_gpu_get_metrics(nsfr_gpu_ctx* ctx, double* jac, double* cof) {
 int nsfr_gpu_set_state(nsfr_gpu_ctx* ctx, const double* u) {
   ctx->proj_valid = false;
   if (ctx->dg) return nsfr_gpu_set_state_q(ctx, u);  // DG carries u_hat itself
-  // u_hat -> scratch (d_vol is dead between steps) -> u_q = chi^3 u_hat
-  CK(cudaMemcpyAsync(ctx->d_vol, u, sizeof(double) * state_count(ctx), cudaMemcpyHostToDevice, ctx->st));
-  if (int rc = convert_state(ctx, ctx->d_vol, ctx->d_un, true)) return rc;
+  // u_hat -> scratch (d_vol is dead between steps) -> u_q = chi^3 u_hat, in
+  // element chunks: the copy of chunk c+1 overlaps the conversion of chunk c
+  const int nch = transfer_chunks(ctx);
+  if (int rc = ensure_chunk_events(ctx, nch)) return rc;
+  const size_t per = nsol(ctx) * NS;
+  CK(cudaStreamSynchronize(ctx->st));  // d_vol / d_un are free
+  for (int c = 0; c < nch; ++c) {
+    const int e0 = static_cast<int>(static_cast<long long>(ctx->E) * c / nch);
+    const int e1 = static_cast<int>(static_cast<long long>(ctx->E) * (c + 1) / nch);
+    if (e1 <= e0) continue;
+    CK(cudaMemcpyAsync(ctx->d_vol + e0 * per, u + e0 * per, sizeof(double) * per * (e1 - e0),
+                       cudaMemcpyHostToDevice, ctx->st_copy));
+    CK(cudaEventRecord(ctx->chunk_ev[c], ctx->st_copy));
+    CK(cudaStreamWaitEvent(ctx->st, ctx->chunk_ev[c], 0));
+    if (int rc = convert_range(ctx, ctx->d_vol, ctx->d_un, true, e0, e1)) return rc;
+  }
   CK(cudaStreamSynchronize(ctx->st));
   return NSFR_OK;
 }
 
 int nsfr_gpu_get_state(nsfr_gpu_ctx* ctx, double* u) {
   if (ctx->dg) return nsfr_gpu_get_state_q(ctx, u);
-  if (int rc = convert_state(ctx, ctx->d_un, ctx->d_vol, false)) return rc;
-  CK(cudaMemcpyAsync(u, ctx->d_vol, sizeof(double) * state_count(ctx), cudaMemcpyDeviceToHost, ctx->st));
+  // u_q -> Pi^3 -> u_hat in element chunks; the copy of chunk c overlaps the
+  // conversion of chunk c+1
+  const int nch = transfer_chunks(ctx);
+  if (int rc = ensure_chunk_events(ctx, nch)) return rc;
+  const size_t per = nsol(ctx) * NS;
+  for (int c = 0; c < nch; ++c) {
+    const int e0 = static_cast<int>(static_cast<long long>(ctx->E) * c / nch);
+    const int e1 = static_cast<int>(static_cast<long long>(ctx->E) * (c + 1) / nch);
+    if (e1 <= e0) continue;
+    if (int rc = convert_range(ctx, ctx->d_un, ctx->d_vol, false, e0, e1)) return rc;
+    CK(cudaEventRecord(ctx->chunk_ev[c], ctx->st));
+    CK(cudaStreamWaitEvent(ctx->st_copy, ctx->chunk_ev[c], 0));
+    CK(cudaMemcpyAsync(u + e0 * per, ctx->d_vol + e0 * per, sizeof(double) * per * (e1 - e0),
+                       cudaMemcpyDeviceToHost, ctx->st_copy));
+  }
+  CK(cudaStreamSynchronize(ctx->st_copy));
   CK(cudaStreamSynchronize(ctx->st));
   return NSFR_OK;
 }
