@@ -192,8 +192,8 @@ ProjParams proj_params(nsfr_gpu_ctx* ctx, const double* u, bool want_lam) {
   P.ut_vol = ctx->d_utv;
   P.traces = ctx->d_tr;
   P.vhat = ctx->d_vhat;
-  P.send_lo = ctx->nranks > 1 ? ctx->d_send_lo : nullptr;
-  P.send_hi = ctx->nranks > 1 ? ctx->d_send_hi : nullptr;
+  P.send_lo = ctx->d_send_lo;
+  P.send_hi = ctx->d_send_hi;
   P.lam = want_lam ? &ctx->d_step->lam_bits : nullptr;
   P.err = ctx->d_err;
   P.E = ctx->E;
@@ -222,8 +222,8 @@ int launch_residual(nsfr_gpu_ctx* ctx, bool ke) {
   ResParams P{};
   P.ut_vol = ctx->d_utv;
   P.traces = ctx->d_tr;
-  P.halo_lo = ctx->nranks > 1 ? ctx->d_halo_lo : nullptr;
-  P.halo_hi = ctx->nranks > 1 ? ctx->d_halo_hi : nullptr;
+  P.halo_lo = ctx->d_halo_lo;
+  P.halo_hi = ctx->d_halo_hi;
   P.cof = ctx->d_cof;
   P.vol = ctx->d_vol;
   P.facc = ctx->d_facc;
@@ -337,8 +337,8 @@ int launch_dg_states(nsfr_gpu_ctx* ctx, const double* u, bool want_lam) {
   DgStateParams P{};
   P.u = u;
   P.traces = ctx->d_tr;
-  P.send_lo = ctx->nranks > 1 ? ctx->d_send_lo : nullptr;
-  P.send_hi = ctx->nranks > 1 ? ctx->d_send_hi : nullptr;
+  P.send_lo = ctx->d_send_lo;
+  P.send_hi = ctx->d_send_hi;
   P.lam = want_lam ? &ctx->d_step->lam_bits : nullptr;
   P.err = ctx->d_err;
   P.E = ctx->E;
@@ -361,8 +361,8 @@ int launch_dg_residual(nsfr_gpu_ctx* ctx, int stage, const double* us, double* u
   DgResParams P{};
   P.us = us;
   P.traces = ctx->d_tr;
-  P.halo_lo = ctx->nranks > 1 ? ctx->d_halo_lo : nullptr;
-  P.halo_hi = ctx->nranks > 1 ? ctx->d_halo_hi : nullptr;
+  P.halo_lo = ctx->d_halo_lo;
+  P.halo_hi = ctx->d_halo_hi;
   P.cof = ctx->d_cof;
   P.wj = ctx->d_wj;
   P.un = ctx->d_un;
@@ -722,7 +722,10 @@ int nsfr_gpu_create(const nsfr_gpu_setup* setup, nsfr_gpu_ctx** out) {
     ctx->msg = "nsfr_gpu_create: device allocation failed";
     return fail(NSFR_E_CUDA);
   }
-  if (ctx->nranks > 1) {
+  // halo planes: z-slabs of nranks > 1, or a 1-rank NCCL communicator (nccl_id
+  // given): its halo is a send/recv to itself, i.e. the periodic wrap through
+  // the real NCCL path (tests/test_gpu_parity.py::test_nccl_loopback_*)
+  if (ctx->nranks > 1 || s.nccl_id) {
     nsfr_gpu_halo_plan plan;
     if (nsfr_gpu_halo_plan_for(s.m, s.p, ctx->rank, ctx->nranks, &plan) || plan.k0 != s.k0 ||
         plan.k1 != s.k1) {
@@ -1117,7 +1120,7 @@ int nsfr_gpu_halo_buffers(nsfr_gpu_ctx* ctx, double** send_lo, double** send_hi,
 }
 
 int nsfr_gpu_halo_get(nsfr_gpu_ctx* ctx, double* send_lo, double* send_hi) {
-  if (ctx->nranks <= 1) {
+  if (!ctx->d_send_lo) {
     ctx->msg = "halo_get: single-rank context has no halo planes";
     return NSFR_E_CONFIG;
   }
@@ -1128,7 +1131,7 @@ int nsfr_gpu_halo_get(nsfr_gpu_ctx* ctx, double* send_lo, double* send_hi) {
 }
 
 int nsfr_gpu_halo_set(nsfr_gpu_ctx* ctx, const double* recv_lo, const double* recv_hi) {
-  if (ctx->nranks <= 1) {
+  if (!ctx->d_halo_lo) {
     ctx->msg = "halo_set: single-rank context has no halo planes";
     return NSFR_E_CONFIG;
   }

@@ -400,3 +400,24 @@ def test_slab_halo_path_matches_whole_box(nranks):
     uq = np.concatenate([g.get_state_q() for g in ranks])
     np.testing.assert_array_equal(uq, whole.get_state_q())
     assert all(g.time == whole.time for g in ranks)
+
+
+@pytest.mark.parametrize("scheme", ["nsfr", "dg"])
+def test_nccl_loopback_matches_plain(scheme):
+    """The real NCCL path on one GPU: a 1-rank communicator whose z-halo is a
+    grouped send/recv to itself (= the periodic wrap), the lambda MAX allreduce
+    and the diagnostics SUM allreduce, also inside the captured CUDA graph of a
+    step. Bitwise equal to the single-rank context that wraps locally."""
+    pkg = P()
+    cfg = gpu_cfg(p=4, m=4, c1d=OC_PLUS[4] if scheme == "nsfr" else 0.0, scheme=scheme)
+    a = pkg.GpuSolver(cfg)
+    b = pkg.GpuSolver(cfg, nccl_id=pkg.nccl_unique_id())
+    a.init_case()
+    b.init_case()
+    np.testing.assert_array_equal(b.rhs(), a.rhs())
+    assert b.max_wavespeed() == a.max_wavespeed()
+    ta, tb = a.advance(3, cfl=0.1), b.advance(3, cfl=0.1)
+    assert ta == tb
+    np.testing.assert_array_equal(b.get_state_q(), a.get_state_q())
+    np.testing.assert_array_equal(b.l2_error(), a.l2_error())
+    np.testing.assert_array_equal(b.conserved_totals(), a.conserved_totals())
