@@ -25,9 +25,10 @@ namespace nsfr_b200 {
 __device__ __forceinline__ bool d_physical_flux(double g, const double* u, double (&f)[3][NS]) {
   if (!d_admissible(g, u)) return false;
   const double p = d_pressure(g, u);
+  const double ir = 1.0 / u[0];
 #pragma unroll
   for (int k = 0; k < 3; ++k) {
-    const double vk = u[1 + k] / u[0];
+    const double vk = u[1 + k] * ir;
     f[k][0] = u[0] * vk;
     f[k][1] = u[1] * vk;
     f[k][2] = u[2] * vk;
@@ -252,6 +253,9 @@ __global__ void __launch_bounds__(256, 2) k_dg_residual(DgResParams P, DgOps<NP,
                                {WJ, P.wj + (size_t)e0 * Q3, nb * Q3}};
     stage_issue<3>(blk, &bar);
   }
+  // the RK operands of the epilogue, into L2 meanwhile
+  if (P.stage >= 1 && tid == 32) l2_prefetch(P.un + (size_t)e0 * 5 * P3, (size_t)nb * 5 * P3 * 8);
+  if (P.stage >= 2 && tid == 64) l2_prefetch(P.acc + (size_t)e0 * 5 * P3, (size_t)nb * 5 * P3 * 8);
   __syncthreads();
   stage_wait(&bar);
   __syncthreads();
