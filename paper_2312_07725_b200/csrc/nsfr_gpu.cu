@@ -96,11 +96,17 @@ int set_attrs(nsfr_gpu_ctx* ctx) {
   CK(cudaOccupancyMaxActiveBlocksPerMultiprocessor(&bp, k_project<N>, ProjCfg<N>::THREADS, ProjCfg<N>::SMEM));
   CK(cudaOccupancyMaxActiveBlocksPerMultiprocessor(&br, k_residual<N>, ResCfg<N>::THREADS, ResCfg<N>::SMEM));
   CK(cudaOccupancyMaxActiveBlocksPerMultiprocessor(&bu, k_update<N>, UpdCfg<N>::THREADS, UpdCfg<N>::SMEM));
-  // NSFR_NO_PREFETCH=1 disables the look-ahead L2 prefetch (A/B measurements)
-  const bool pf = std::getenv("NSFR_NO_PREFETCH") == nullptr;
-  Resident<N>::proj = pf ? sms * std::max(bp, 1) : (1 << 30);
-  Resident<N>::res = pf ? sms * std::max(br, 1) : (1 << 30);
-  Resident<N>::upd = pf ? sms * std::max(bu, 1) : (1 << 30);
+  // Look-ahead L2 prefetch distance in resident waves. Measured (64^3/48^3,
+  // A/B in one session): a quarter wave helps at p=4 (K2 -0.7%, K3 -0.8% vs
+  // one wave), none is best at p=3 (K2 -5%) and p=5 (K2 -2%).
+  // NSFR_PF_WAVES overrides, NSFR_NO_PREFETCH=1 disables.
+  const char* w = std::getenv("NSFR_PF_WAVES");
+  const double waves = w ? std::atof(w) : (N == 5 ? 0.25 : 0.0);
+  const bool pf = std::getenv("NSFR_NO_PREFETCH") == nullptr && waves > 0.0;
+  auto ahead = [&](int blocks) { return pf ? static_cast<int>(waves * sms * std::max(blocks, 1)) : (1 << 30); };
+  Resident<N>::proj = ahead(bp);
+  Resident<N>::res = ahead(br);
+  Resident<N>::upd = ahead(bu);
   return NSFR_OK;
 }
 
