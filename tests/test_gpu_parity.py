@@ -200,6 +200,23 @@ def test_config2_to_final_time(name, c1d):
     np.testing.assert_allclose(g.l2_error(), gold["l2"], rtol=1e-10)
 
 
+@pytest.mark.parametrize("p", [4, 5])
+def test_config3_to_final_time(p):
+    """BASELINE configs[2]: 32^3 vortex, c_DG, EC+Roe, RK4 at CFL 0.1 to t_f = 2
+    (~763 steps at p=4, ~916 at p=5); final L2(rho), L2(p) within 1e-10
+    relative of the reference build (tests/golden/config3.json,
+    tests/golden/make_golden_config3.py; the p=4 run took ~2 h on 8 cores)."""
+    with open(os.path.join(GOLD, "config3.json")) as f:
+        gold = json.load(f).get(f"p{p}")
+    if gold is None:
+        pytest.skip(f"config3 golden for p={p} not generated")
+    g = P().GpuSolver(gpu_cfg(p=p, m=32))
+    g.init_case()
+    t = g.advance(3000, cfl=0.1, t_final=2.0)
+    assert t == pytest.approx(gold["t_final"], abs=1e-12)
+    np.testing.assert_allclose(g.l2_error(), gold["l2"], rtol=1e-10)
+
+
 def test_advance_graph_equals_stepwise():
     cfg = gpu_cfg(p=3, m=4)
     a = P().GpuSolver(cfg)
