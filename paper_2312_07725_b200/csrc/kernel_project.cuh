@@ -113,30 +113,6 @@ __device__ __forceinline__ void face_contract(const double (&bp)[2 * N], const d
   }
 }
 
-// Line pass on face arrays [batch][N2] (index t1 + N t2) along t1 (T=0) or t2 (T=1).
-template <int N, int T>
-__device__ __forceinline__ void face_pass(const double (&op)[N * N], const double* in, double* out,
-                                          int nbatch, int tid, int nthr) {
-  constexpr int N2 = N * N;
-  constexpr int stride = T == 0 ? 1 : N;
-  for (int it = tid; it < nbatch * N; it += nthr) {
-    const int bi = it / N, l = it - bi * N;
-    const int base = T == 0 ? N * l : l;
-    const double* src = in + bi * N2 + base;
-    double x[N];
-#pragma unroll
-    for (int a = 0; a < N; ++a) x[a] = src[a * stride];
-    double* dst = out + bi * N2 + base;
-#pragma unroll
-    for (int r = 0; r < N; ++r) {
-      double acc = 0.0;
-#pragma unroll
-      for (int a = 0; a < N; ++a) acc = fma(op[r * N + a], x[a], acc);
-      dst[r * stride] = acc;
-    }
-  }
-}
-
 // S2-S5 for the nb elements whose state u_q (volume quadrature nodes) sits in
 // shared memory A ([EPB*5][N3], synchronised by the caller). B, V: [EPB*5][N3] scratch;
 // F: [3][EPB*5][2][N2] face scratch. Shared by K1 and the fused K3 (kernel_update.cuh).
