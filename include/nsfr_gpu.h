@@ -169,6 +169,12 @@ int nsfr_gpu_entropy_total(nsfr_gpu_ctx* ctx, double* out);
  * the EC flux minus the pressure work P~_ij = 1/2 (p_i + p_j) I_d 1/2 (C_i + C_j),
  * v_KE = (-|v|^2/2, v, 0) at the volume nodes. Round-off for the KEP flux. */
 int nsfr_gpu_ke_volume(nsfr_gpu_ctx* ctx, double* out);
+/* Kinetic-energy change minus pressure work (kinetic_energy_change's
+ * total_minus_pressure_work):
+ * -sum v_hat_KE . R with R the pre-inverse residual rows (volume, hybrid
+ * surface, face; chi^T lifted) of the EC flux minus the pressure work and no
+ * Roe term, v_hat_KE = Pi^3 v_KE(u_q). Round-off for LGL, not for GL (Lemma 1). */
+int nsfr_gpu_ke_total(nsfr_gpu_ctx* ctx, double* out);
 
 /* Bench helper: time nsteps RK4 steps (t_final unbounded) with CUDA events on
  * the context stream; inputs stay resident in HBM. kernel_ms (optional, [3])

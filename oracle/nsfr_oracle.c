@@ -1126,7 +1126,16 @@ typedef struct {
   const double* halo_hi;
   double* dudt;
   double* dS; /* per element entropy change partial or NULL */
+  const double* u; /* state (kinetic-energy mode only) */
+  double* keS;     /* non-NULL: kinetic-energy mode, per element -v_hat_KE . R^{F-P} */
 } RhsArg;
+
+/* F~ - P~: the two-point flux without the pressure work 1/2 (p_i + p_j) I_d
+ * (PAPER.md:1811-1822), for the kinetic-energy diagnostics */
+static void strip_pressure(double g, const double* ui, const double* uj, double f[3][NS]) {
+  const double pbar = 0.5 * (pressure(g, ui) + pressure(g, uj));
+  for (int k = 0; k < 3; ++k) f[k][1 + k] -= pbar;
+}
 
 /* neighbour trace pointer for face f of local element e (geometry.hpp:24-29) */
 static const double* nbr_trace(const RhsArg* A, int e, int f) {
@@ -1185,6 +1194,7 @@ static void rhs_elem(void* argp, int e) {
               c->err[e] = NSFR_E_INADMISSIBLE;
               return;
             }
+            if (A->keS) strip_pressure(g, ui, uj, fl);
             const double cm0 = 0.5 * (C[9 * ia + 0 + dir] + C[9 * ib + 0 + dir]);
             const double cm1 = 0.5 * (C[9 * ia + 3 + dir] + C[9 * ib + 3 + dir]);
             const double cm2 = 0.5 * (C[9 * ia + 6 + dir] + C[9 * ib + 6 + dir]);
@@ -1222,6 +1232,7 @@ static void rhs_elem(void* argp, int e) {
               c->err[e] = NSFR_E_INADMISSIBLE;
               return;
             }
+            if (A->keS) strip_pressure(g, ui, uf, fl);
             const double cm0 = 0.5 * (C[9 * ia + 0 + dir] + cfk[0 + dir]);
             const double cm1 = 0.5 * (C[9 * ia + 3 + dir] + cfk[3 + dir]);
             const double cm2 = 0.5 * (C[9 * ia + 6 + dir] + cfk[6 + dir]);
@@ -1252,8 +1263,9 @@ static void rhs_elem(void* argp, int e) {
           c->err[e] = NSFR_E_INADMISSIBLE;
           return;
         }
+        if (A->keS) strip_pressure(g, ul, ur, fl);
         for (int s = 0; s < NS; ++s) fn[s] = fl[0][s] * nr[0] + fl[1][s] * nr[1] + fl[2][s] * nr[2];
-        if (c->cfg.roe) {
+        if (c->cfg.roe && !A->keS) {
           if (roe_diss(g, ul, ur, nr, d)) {
             c->err[e] = NSFR_E_INADMISSIBLE;
             return;
@@ -1287,6 +1299,29 @@ static void rhs_elem(void* argp, int e) {
         for (int i = 0; i < nsol; ++i) R[s * nsol + i] += tmp[i];
       }
     }
+  /* kinetic energy: -sum_s v_hat_KE,s . R_s with v_hat_KE = Pi^3 v_KE(chi^3 u_hat)
+   * (kinetic_energy_variables, euler.cpp:83-87) */
+  if (A->keS) {
+    const int me[3] = {np, np, np}, qe3[3] = {nq, nq, nq};
+    double uq[NS][MAXN * MAXN * MAXN], vk[NS][MAXN * MAXN * MAXN], vkh[MAXN * MAXN * MAXN];
+    const double* ue = A->u + (size_t)e * NS * nsol;
+    for (int s = 0; s < NS; ++s) apply_tp(&o->interp, &o->interp, &o->interp, ue + s * nsol, me, uq[s]);
+    for (int q = 0; q < nv; ++q) {
+      const double iu = 1.0 / uq[0][q];
+      const double vx = uq[1][q] * iu, vy = uq[2][q] * iu, vz = uq[3][q] * iu;
+      vk[0][q] = -0.5 * (vx * vx + vy * vy + vz * vz);
+      vk[1][q] = vx;
+      vk[2][q] = vy;
+      vk[3][q] = vz;
+    }
+    double acc = 0.0;
+    for (int s = 0; s < 4; ++s) {
+      apply_tp(&o->proj, &o->proj, &o->proj, vk[s], qe3, vkh);
+      for (int i = 0; i < nsol; ++i) acc += vkh[i] * R[s * nsol + i];
+    }
+    A->keS[e] = -acc;
+    return;
+  }
   /* D9 entropy change: -sum_s v_hat_s . R_s */
   if (A->dS) {
     const double* vh = c->vhat + (size_t)e * NS * nsol;
@@ -1472,7 +1507,7 @@ int nsfr_oracle_rhs(void* ctx, const double* u, const double* halo_lo, const dou
     return NSFR_E_DIM;
   }
   double* dS = entropy_change ? calloc(c->ne, sizeof(double)) : NULL;
-  RhsArg A = {c, halo_lo, halo_hi, dudt, dS};
+  RhsArg A = {c, halo_lo, halo_hi, dudt, dS, NULL, NULL};
   parallel_for(c->ne, c->cfg.workers, c->cfg.scheme == NSFR_SCHEME_DG ? dg_rhs_elem : rhs_elem, &A);
   for (int e = 0; e < c->ne; ++e)
     if (c->err[e]) {
@@ -1578,6 +1613,36 @@ int nsfr_oracle_ke_volume(void* ctx, const double* u, double* out) {
     acc += part[e];
   }
   free(part);
+  *out = acc;
+  return NSFR_OK;
+}
+
+/* Kinetic-energy change minus pressure work ("total_minus_
+ * pressure_work"): -sum v_hat_KE . R^{F-P}, R^{F-P} the
+ * pre-inverse residual (S6-S9) with every two-point flux replaced by F~ - P~
+ * and no Roe term, v_hat_KE = Pi^3 v_KE(u_q). Lemma 1: round-off when the
+ * surface nodes are volume nodes (LGL), not for GL. Whole box only. */
+int nsfr_oracle_ke_total(void* ctx, const double* u, double* out) {
+  Ctx* c = (Ctx*)ctx;
+  if (c->cfg.scheme != NSFR_SCHEME_NSFR || !(c->cfg.k0 == 0 && c->cfg.k1 == c->cfg.m)) {
+    set_err(c, "ke_total: NSFR on the whole box only");
+    return NSFR_E_DIM;
+  }
+  int rc = project_all(c, u);
+  if (rc) return rc;
+  double* keS = calloc(c->ne, sizeof(double));
+  RhsArg A = {c, NULL, NULL, NULL, NULL, u, keS};
+  parallel_for(c->ne, c->cfg.workers, rhs_elem, &A);
+  double acc = 0.0;
+  for (int e = 0; e < c->ne; ++e) {
+    if (c->err[e]) {
+      set_err(c, "ke_total: inadmissible state in element %d", e);
+      free(keS);
+      return c->err[e];
+    }
+    acc += keS[e];
+  }
+  free(keS);
   *out = acc;
   return NSFR_OK;
 }

@@ -90,6 +90,9 @@ int NSFR_CPU_API(conserved_totals)(void* ctx, const double* u, double out5[5]);
 /* kinetic-energy volume term sum v_KE . S6 rows of (EC flux - pressure work)
  * (SPEC.md:602-609); ~0 for the KEP flux */
 int NSFR_CPU_API(ke_volume)(void* ctx, const double* u, double* out);
+/* kinetic-energy change minus pressure work: -sum v_hat_KE . R with every
+ * two-point flux minus the pressure work, no Roe; whole box */
+int NSFR_CPU_API(ke_total)(void* ctx, const double* u, double* out);
 #endif
 
 #ifdef __cplusplus

@@ -182,8 +182,14 @@ const double* nbr_trace(const RefCtx& c, int e, int f, const double* halo_lo,
 }
 
 // S6-S10
+// F~ - P~ (kinetic-energy diagnostics)
+void strip_pressure(const RefCtx& c, const State& ui, const State& uj, Flux& F) {
+  const double pbar = 0.5 * (pressure(c.gas, ui) + pressure(c.gas, uj));
+  for (int k = 0; k < 3; ++k) F[k][1 + k] -= pbar;
+}
+
 void rhs_elem(RefCtx& c, int e, const double* halo_lo, const double* halo_hi, double* dudt,
-              double* dS) {
+              double* dS, const double* uke = nullptr, double* keS = nullptr) {
   const auto& o = c.ops;
   const int nv = c.nv, nf = c.nf, nsol = c.nsol, nq = c.nq;
   const Extents qe{nq, nq, nq}, me{c.np, c.np, c.np};
@@ -197,8 +203,9 @@ void rhs_elem(RefCtx& c, int e, const double* halo_lo, const double* halo_hi, do
   const std::span<const double> w(o.wq);
   const std::array<std::span<const double>, 3> w3{w, w, w};
   auto vol_provider = [&](int i, int j, int dir, double* out) {
-    const Flux F = two_point_flux(c.gas, TwoPointFluxKind::ChandrashekarRanochaFix,
-                                  load(utv, nv, i), load(utv, nv, j));
+    Flux F = two_point_flux(c.gas, TwoPointFluxKind::ChandrashekarRanochaFix,
+                            load(utv, nv, i), load(utv, nv, j));
+    if (keS) strip_pressure(c, load(utv, nv, i), load(utv, nv, j), F);
     const double* Ci = em.cof_at(i);
     const double* Cj = em.cof_at(j);
     const double cm0 = 0.5 * (Ci[0 + dir] + Cj[0 + dir]);
@@ -210,8 +217,9 @@ void rhs_elem(RefCtx& c, int e, const double* halo_lo, const double* halo_hi, do
   const std::array<const Operator1D*, 3> bf{&o.bound_flux, &o.bound_flux, &o.bound_flux};
   auto surf_provider = [&](int i, int fid, int k, int dir, double* out) {
     const double* utf = utf_all + static_cast<size_t>(fid) * kStates * nf;
-    const Flux F = two_point_flux(c.gas, TwoPointFluxKind::ChandrashekarRanochaFix,
-                                  load(utv, nv, i), load(utf, nf, k));
+    Flux F = two_point_flux(c.gas, TwoPointFluxKind::ChandrashekarRanochaFix,
+                            load(utv, nv, i), load(utf, nf, k));
+    if (keS) strip_pressure(c, load(utv, nv, i), load(utf, nf, k), F);
     const double* Ci = em.cof_at(i);
     const double* Cf = em.cof_face_at(fid, k);
     const double cm0 = 0.5 * (Ci[0 + dir] + Cf[0 + dir]);
@@ -232,10 +240,11 @@ void rhs_elem(RefCtx& c, int e, const double* halo_lo, const double* halo_hi, do
         const State ul = load(utf, nf, k), ur = load(utn, nf, k);
         const std::array<double, 3> nr{fnrm.unit_normals[3 * k], fnrm.unit_normals[3 * k + 1],
                                        fnrm.unit_normals[3 * k + 2]};
-        const Flux F = two_point_flux(c.gas, TwoPointFluxKind::ChandrashekarRanochaFix, ul, ur);
+        Flux F = two_point_flux(c.gas, TwoPointFluxKind::ChandrashekarRanochaFix, ul, ur);
+        if (keS) strip_pressure(c, ul, ur, F);
         double fn[kStates];
         for (int s = 0; s < kStates; ++s) fn[s] = F[0][s] * nr[0] + F[1][s] * nr[1] + F[2][s] * nr[2];
-        if (c.cfg.roe) {
+        if (c.cfg.roe && !keS) {
           const State d = roe_dissipation(c.gas, ul, ur, nr);
           for (int s = 0; s < kStates; ++s) fn[s] -= d[s];
         }
@@ -262,6 +271,24 @@ void rhs_elem(RefCtx& c, int e, const double* halo_lo, const double* halo_hi, do
         for (int i = 0; i < nsol; ++i) R[s * nsol + i] += tmp[i];
       }
     }
+  if (keS) {  // -sum v_hat_KE . R, v_hat_KE = Pi^3 kinetic_energy_variables(chi^3 u_hat)
+    std::vector<double> uq(kStates * nv), vk(4 * nv), vkh(nsol);
+    for (int s = 0; s < kStates; ++s)
+      apply_tensor_product(o.basis.interp, o.basis.interp, o.basis.interp,
+                           std::span<const double>(uke + (static_cast<size_t>(e) * kStates + s) * nsol, nsol),
+                           me, std::span<double>(&uq[s * nv], nv), work);
+    for (int q = 0; q < nv; ++q) {
+      const State v = kinetic_energy_variables(load(uq.data(), nv, q));
+      for (int s = 0; s < 4; ++s) vk[s * nv + q] = v[s];
+    }
+    double acc = 0.0;
+    for (int s = 0; s < 4; ++s) {
+      apply_tensor_product(o.proj, o.proj, o.proj, std::span<const double>(&vk[s * nv], nv), qe, vkh, work);
+      for (int i = 0; i < nsol; ++i) acc += vkh[i] * R[s * nsol + i];
+    }
+    keS[e] = -acc;
+    return;
+  }
   if (dS) {
     const double* vh = &c.vhat[static_cast<size_t>(e) * kStates * nsol];
     double acc = 0.0;
@@ -598,6 +625,32 @@ int nsfr_ref_ke_volume(void* ctx, const double* u, double* out) {
   }
   double acc = 0.0;
   for (int e = 0; e < c.ne; ++e) acc += part[e];
+  *out = acc;
+  return NSFR_OK;
+}
+
+int nsfr_ref_ke_total(void* ctx, const double* u, double* out) {
+  RefCtx& c = *static_cast<RefCtx*>(ctx);
+  if (c.cfg.scheme != NSFR_SCHEME_NSFR || !(c.cfg.k0 == 0 && c.cfg.k1 == c.cfg.m)) {
+    c.msg = "ke_total: NSFR on the whole box only";
+    return NSFR_E_DIM;
+  }
+  if (int rc = project_all(c, u)) return rc;
+  std::vector<double> keS(c.ne, 0.0);
+  std::atomic<int> bad{-1};
+  parallel_for(c.ne, c.cfg.workers, [&](int e) {
+    try {
+      rhs_elem(c, e, nullptr, nullptr, nullptr, nullptr, u, keS.data());
+    } catch (const std::exception&) {
+      bad = e;
+    }
+  });
+  if (bad >= 0) {
+    c.msg = "ke_total: inadmissible state";
+    return NSFR_E_INADMISSIBLE;
+  }
+  double acc = 0.0;
+  for (int e = 0; e < c.ne; ++e) acc += keS[e];
   *out = acc;
   return NSFR_OK;
 }

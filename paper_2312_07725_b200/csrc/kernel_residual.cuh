@@ -140,9 +140,10 @@ __device__ __forceinline__ void res_prefetch(const ResParams& P, int e0, int tid
   }
 }
 
-// KE = true: the kinetic-energy diagnostic's volume rows (S6 only, flux minus
-// pressure work); no surface terms, no face rows.
-template <int N, bool KE>
+// KM (kinetic-energy diagnostics; every two-point flux minus the pressure work):
+//   0 the residual; 1 volume rows only (S6); 2 all rows (S6-S8) without Roe.
+
+template <int N, int KM>
 __device__ __forceinline__ void res_batch(const ResParams& P, const ResOps<N>& O, int e0, double* sm) {
   using Cfg = ResCfg<N>;
   constexpr int N2 = Cfg::N2, N3 = Cfg::N3, EPB = Cfg::EPB, LINES = Cfg::LINES;
@@ -186,10 +187,10 @@ __device__ __forceinline__ void res_batch(const ResParams& P, const ResOps<N>& O
     for (int a = 0; a < N; ++a)
 #pragma unroll
       for (int s = 0; s < NS; ++s) acc[s * N3 + lbase + a * stride] = 0.0;
-    vol_pairs<N, KE>(Pd, Ch, acc, O.q, wt, lbase, stride, dir, amask);
+    vol_pairs<N, (KM != 0)>(Pd, Ch, acc, O.q, wt, lbase, stride, dir, amask);
     // S7 hybrid surface pairs + S8 face flux for the two faces this line pierces
 #pragma unroll 1
-    for (int side = 0; side < (KE ? 0 : 2); ++side) {
+    for (int side = 0; side < (KM == 1 ? 0 : 2); ++side) {
       const int f = 2 * dir + side;
       const double sign = side ? 1.0 : -1.0;
       const int k = t1 + N * t2;
@@ -236,8 +237,8 @@ __device__ __forceinline__ void res_batch(const ResParams& P, const ResOps<N>& O
         const PrimH pa{Pd[ia], Pd[N3 + ia], Pd[2 * N3 + ia], Pd[3 * N3 + ia],
                        Pd[4 * N3 + ia], Pd[5 * N3 + ia]};
         double fl[NS];
-        d_flux_h(pa, pfh, Ch[(0 + dir) * N3 + ia] + ch0, Ch[(3 + dir) * N3 + ia] + ch1,
-                          Ch[(6 + dir) * N3 + ia] + ch2, fl, amask);
+        d_flux_h<(KM != 0)>(pa, pfh, Ch[(0 + dir) * N3 + ia] + ch0, Ch[(3 + dir) * N3 + ia] + ch1,
+                            Ch[(6 + dir) * N3 + ia] + ch2, fl, amask);
         const double c = sign * O.bflux[side * N + a] * wt;
 #pragma unroll
         for (int s = 0; s < NS; ++s) {
@@ -252,8 +253,8 @@ __device__ __forceinline__ void res_batch(const ResParams& P, const ResOps<N>& O
       const double nrm[3] = {v0 * ijg, v1 * ijg, v2 * ijg};
       const PrimX pn = d_primx(g, un);
       double fn[NS];
-      d_flux_h(pfh, to_half(gm1, pn), nrm[0], nrm[1], nrm[2], fn, amask);
-      if (P.roe) {
+      d_flux_h<(KM != 0)>(pfh, to_half(gm1, pn), nrm[0], nrm[1], nrm[2], fn, amask);
+      if (P.roe && KM == 0) {
         double d[NS];
         if (!d_roe_x(g, uf, un, pf, pn, nrm, d)) atomicOr(P.err, ERR_ROE);
 #pragma unroll
@@ -270,7 +271,7 @@ __device__ __forceinline__ void res_batch(const ResParams& P, const ResOps<N>& O
     }
   }
   // face rows straight from registers: facc[e][dir][s][side][k]
-  if (!KE && lb < nb) {
+  if (KM != 1 && lb < nb) {
     const int k = (lrem % N) + N * (lrem / N);
     double* fa = P.facc + ((size_t)(e0 + lb) * 3 + ldir) * 10 * N2 + k;
 #pragma unroll
@@ -295,14 +296,14 @@ __device__ __forceinline__ void res_batch(const ResParams& P, const ResOps<N>& O
 // lockstep measured slower). Each CTA prefetches into L2 the batch of the CTA
 // `ahead` = #resident CTAs later, which the block scheduler starts about when
 // this one retires, so that CTA's staging loads hit L2.
-template <int N, bool KE = false>
+template <int N, int KM = 0>
 __global__ void __launch_bounds__(ResCfg<N>::THREADS, ResCfg<N>::MINB)
     k_residual(ResParams P, ResOps<N> O, int ahead) {
   extern __shared__ __align__(128) double sm[];
   constexpr int EPB = ResCfg<N>::EPB;
   const long long pe = (static_cast<long long>(blockIdx.x) + ahead) * EPB;
   if (pe < P.E) res_prefetch<N>(P, static_cast<int>(pe), threadIdx.x);
-  res_batch<N, KE>(P, O, blockIdx.x * EPB, sm);
+  res_batch<N, KM>(P, O, blockIdx.x * EPB, sm);
 }
 
 }  // namespace nsfr_b200

@@ -89,7 +89,8 @@ int set_attrs(nsfr_gpu_ctx* ctx) {
   if (Resident<N>::res) return NSFR_OK;
   CK(cudaFuncSetAttribute(k_project<N>, cudaFuncAttributeMaxDynamicSharedMemorySize, ProjCfg<N>::SMEM));
   CK(cudaFuncSetAttribute(k_residual<N>, cudaFuncAttributeMaxDynamicSharedMemorySize, ResCfg<N>::SMEM));
-  CK(cudaFuncSetAttribute(k_residual<N, true>, cudaFuncAttributeMaxDynamicSharedMemorySize, ResCfg<N>::SMEM));
+  CK(cudaFuncSetAttribute(k_residual<N, 1>, cudaFuncAttributeMaxDynamicSharedMemorySize, ResCfg<N>::SMEM));
+  CK(cudaFuncSetAttribute(k_residual<N, 2>, cudaFuncAttributeMaxDynamicSharedMemorySize, ResCfg<N>::SMEM));
   CK(cudaFuncSetAttribute(k_update<N>, cudaFuncAttributeMaxDynamicSharedMemorySize, UpdCfg<N>::SMEM));
   int sms = 0, bp = 0, br = 0, bu = 0;
   CK(cudaDeviceGetAttribute(&sms, cudaDevAttrMultiProcessorCount, ctx->s.device));
@@ -224,7 +225,7 @@ int launch_project(nsfr_gpu_ctx* ctx, const double* u, bool want_lam) {
 }
 
 template <int N>
-int launch_residual(nsfr_gpu_ctx* ctx, bool ke) {
+int launch_residual(nsfr_gpu_ctx* ctx, int km) {
   ResParams P{};
   P.ut_vol = ctx->d_utv;
   P.traces = ctx->d_tr;
@@ -242,9 +243,12 @@ int launch_residual(nsfr_gpu_ctx* ctx, bool ke) {
   if (int rc = set_attrs<N>(ctx)) return rc;
   const int grid = (ctx->E + ResCfg<N>::EPB - 1) / ResCfg<N>::EPB;
   ev_begin(ctx, 2);
-  if (ke)
-    k_residual<N, true><<<grid, ResCfg<N>::THREADS, ResCfg<N>::SMEM, ctx->st>>>(P, res_ops<N>(ctx->htab),
-                                                                              Resident<N>::res);
+  if (km == 1)
+    k_residual<N, 1><<<grid, ResCfg<N>::THREADS, ResCfg<N>::SMEM, ctx->st>>>(P, res_ops<N>(ctx->htab),
+                                                                           Resident<N>::res);
+  else if (km == 2)
+    k_residual<N, 2><<<grid, ResCfg<N>::THREADS, ResCfg<N>::SMEM, ctx->st>>>(P, res_ops<N>(ctx->htab),
+                                                                           Resident<N>::res);
   else
     k_residual<N><<<grid, ResCfg<N>::THREADS, ResCfg<N>::SMEM, ctx->st>>>(P, res_ops<N>(ctx->htab),
                                                                            Resident<N>::res);
@@ -257,12 +261,12 @@ int launch_residual(nsfr_gpu_ctx* ctx, bool ke) {
 // stage 0: dU/dt (+ entropy change); stages 1-4: RK update and projection of
 // the next stage state (lambda_max after stage 4)
 template <int N>
-int launch_update(nsfr_gpu_ctx* ctx, int stage, bool entropy) {
+int launch_update(nsfr_gpu_ctx* ctx, int stage, bool entropy, const double* vhat) {
   UpdParams P{};
   P.vol = ctx->d_vol;
   P.facc = ctx->d_facc;
   P.wj = ctx->d_wj;
-  P.vhat = entropy ? ctx->d_vhat : nullptr;
+  P.vhat = entropy ? (vhat ? vhat : ctx->d_vhat) : nullptr;
   P.dS = entropy ? ctx->d_dS : nullptr;
   P.un = ctx->d_un;
   P.acc = ctx->d_acc;
@@ -294,8 +298,12 @@ int launch_update(nsfr_gpu_ctx* ctx, int stage, bool entropy) {
   return NSFR_E_DIM
 
 int project(nsfr_gpu_ctx* ctx, const double* u, bool lam) { NSFR_DISPATCH(launch_project, (ctx, u, lam)); }
-int residual(nsfr_gpu_ctx* ctx, bool ke = false) { NSFR_DISPATCH(launch_residual, (ctx, ke)); }
-int update(nsfr_gpu_ctx* ctx, int stage, bool entropy) { NSFR_DISPATCH(launch_update, (ctx, stage, entropy)); }
+// km: 0 the residual, 1 / 2 kinetic-energy diagnostic rows (kernel_residual.cuh)
+int residual(nsfr_gpu_ctx* ctx, int km = 0) { NSFR_DISPATCH(launch_residual, (ctx, km)); }
+// entropy: stage-0 diagnostic -vhat . R, with vhat = v_hat (default) or the given coefficients
+int update(nsfr_gpu_ctx* ctx, int stage, bool entropy, const double* vhat = nullptr) {
+  NSFR_DISPATCH(launch_update, (ctx, stage, entropy, vhat));
+}
 
 // ---- conservative DG (kernel_dg.cuh) ------------------------------------------
 template <int NP, int NQ>
@@ -1234,12 +1242,36 @@ int nsfr_gpu_ke_volume(nsfr_gpu_ctx* ctx, double* out) {
   // volume rows of (flux - pressure work) for the projection of u_n, then
   // sum v_KE . rows; partials go to d_rhs (the rows occupy d_vol)
   if (int rc = project_state(ctx)) return rc;
-  if (int rc = residual(ctx, true)) return rc;
+  if (int rc = residual(ctx, 1)) return rc;
   k_ke_dot<<<ctx->E, 128, 0, ctx->st>>>(ctx->d_un, ctx->d_vol, static_cast<int>(nsol(ctx)), ctx->d_rhs,
                                          ctx->E);
   k_reduce<<<1, 1024, 0, ctx->st>>>(ctx->d_rhs, ctx->E, 1, ctx->d_red);
   ctx->launches += 2;
   CK(cudaGetLastError());
+  if (int rc = allreduce_sum(ctx, ctx->d_red, 1)) return rc;
+  if (int rc = sync_check(ctx)) return rc;
+  CK(cudaMemcpy(out, ctx->d_red, sizeof(double), cudaMemcpyDeviceToHost));
+  return NSFR_OK;
+}
+
+int nsfr_gpu_ke_total(nsfr_gpu_ctx* ctx, double* out) {
+  if (ctx->dg) {
+    ctx->msg = "ke_total: defined for the NSFR scheme only";
+    return NSFR_E_CONFIG;
+  }
+  // rows of (flux - pressure work) everywhere, no Roe (K2 km = 2); v_hat_KE =
+  // Pi^3 v_KE(u_q) into d_acc (dead between steps); K3's diagnostic path forms
+  // R = chi^T-lifted rows and -v_hat_KE . R per element
+  if (int rc = project_state(ctx)) return rc;
+  if (int rc = exchange(ctx)) return rc;
+  if (int rc = residual(ctx, 2)) return rc;
+  const size_t smem = sizeof(double) * 4 * nsol(ctx);
+  k_ke_vars<<<ctx->E, 128, smem, ctx->st>>>(ctx->d_tab, ctx->d_un, ctx->d_acc, ctx->E);
+  ++ctx->launches;
+  CK(cudaGetLastError());
+  if (int rc = update(ctx, 0, true, ctx->d_acc)) return rc;
+  k_reduce<<<1, 1024, 0, ctx->st>>>(ctx->d_dS, ctx->E, 1, ctx->d_red);
+  ++ctx->launches;
   if (int rc = allreduce_sum(ctx, ctx->d_red, 1)) return rc;
   if (int rc = sync_check(ctx)) return rc;
   CK(cudaMemcpy(out, ctx->d_red, sizeof(double), cudaMemcpyDeviceToHost));

@@ -440,6 +440,34 @@ __global__ void k_ke_dot(const double* u, const double* vol, int N3, double* par
   }
 }
 
+// Kinetic-energy variables projected to the solution nodes: v_hat_KE =
+// Pi^3 v_KE(u_q), v_KE = (-|v|^2/2, v, 0) (kinetic_energy_variables,
+// euler.cpp:83-87), for the KE change diagnostic. One CTA per element.
+__global__ void k_ke_vars(const DevTables* tab, const double* uq, double* vhat, int E) {
+  extern __shared__ double sm[];
+  const DevTables& T = *tab;
+  const int e = blockIdx.x;
+  if (e >= E) return;
+  const int tid = threadIdx.x, nthr = blockDim.x;
+  const int n = T.nq, N3 = n * n * n;  // n_q = n_p
+  double* vk = sm;
+  double* t1 = vk + N3;
+  double* t2 = t1 + N3;
+  double* dst = t2 + N3;
+  const double* ue = uq + (size_t)e * NS * N3;
+  for (int s = 0; s < NS; ++s) {
+    for (int q = tid; q < N3; q += nthr) {
+      const double iu = 1.0 / ue[q];
+      const double vx = ue[N3 + q] * iu, vy = ue[2 * N3 + q] * iu, vz = ue[3 * N3 + q] * iu;
+      vk[q] = s == 0 ? -0.5 * (vx * vx + vy * vy + vz * vz) : (s == 1 ? vx : (s == 2 ? vy : (s == 3 ? vz : 0.0)));
+    }
+    __syncthreads();
+    tp3_rt(T.proj, n, n, vk, t1, t2, dst, tid, nthr);
+    for (int i = tid; i < N3; i += nthr) vhat[((size_t)e * NS + s) * N3 + i] = dst[i];
+    __syncthreads();
+  }
+}
+
 // Step bookkeeping: reset lambda, compute dt from lambda.
 struct StepState {
   double t, dt, t_final, cfl, dx;

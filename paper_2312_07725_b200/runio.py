@@ -109,7 +109,8 @@ def load_checkpoint(path: str, solver) -> dict:
     return head
 
 
-COLUMNS = ("t", "entropy_change", "entropy_change_normalized", "ke_change_volume", "mass",
+COLUMNS = ("t", "entropy_change", "entropy_change_normalized", "ke_change_volume",
+           "ke_change_total_minus_pressure_work", "mass",
            "momentum_x", "momentum_y", "momentum_z", "energy", "max_wavespeed", "l2_density",
            "l2_pressure")
 
@@ -126,6 +127,7 @@ def diagnostic_record(solver, u_total0: float | None) -> dict:
     else:
         rec["entropy_change"] = rec["entropy_change_normalized"] = math.nan
     rec["ke_change_volume"] = solver.ke_volume()
+    rec["ke_change_total_minus_pressure_work"] = solver.ke_total() if cfg.nranks == 1 else math.nan
     tot = solver.conserved_totals()
     for k, v in zip(("mass", "momentum_x", "momentum_y", "momentum_z", "energy"), tot):
         rec[k] = float(v)

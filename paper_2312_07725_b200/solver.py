@@ -132,6 +132,7 @@ def load_library() -> C.CDLL:
         "nsfr_gpu_stage": (C.c_int, [V, C.c_int, C.c_double]),
         "nsfr_gpu_get_state_q": (C.c_int, [V, P]),
         "nsfr_gpu_ke_volume": (C.c_int, [V, P]),
+        "nsfr_gpu_ke_total": (C.c_int, [V, P]),
         "nsfr_gpu_time_steps": (C.c_int, [V, C.c_int, C.c_double, P, P]),
         "nsfr_gpu_state_device_ptr": (C.c_void_p, [V]),
         "nsfr_gpu_state_count": (C.c_size_t, [V]),
@@ -430,6 +431,12 @@ class GpuSolver:
 
     def stage(self, s: int, dt: float):
         self._check(self.lib.nsfr_gpu_stage(self.ctx, s, dt))
+
+    def ke_total(self) -> float:
+        """Kinetic-energy change minus pressure work (-v_hat_KE . R of F - P, no Roe)."""
+        out = np.zeros(1)
+        self._check(self.lib.nsfr_gpu_ke_total(self.ctx, _ptr(out)))
+        return float(out[0])
 
     def conserved_totals(self) -> np.ndarray:
         """sum w J u over the (global) domain: mass, momentum x3, energy."""

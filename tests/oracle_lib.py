@@ -98,6 +98,7 @@ def load(kind: str) -> tuple[C.CDLL, str]:
             "entropy_total": (C.c_int, [C.c_void_p, P, P]),
             "conserved_totals": (C.c_int, [C.c_void_p, P, P]),
             "ke_volume": (C.c_int, [C.c_void_p, P, P]),
+            "ke_total": (C.c_int, [C.c_void_p, P, P]),
             "log_mean": (C.c_double, [C.c_double, C.c_double]),
             "flux_ec": (C.c_int, [C.c_double, P, P, P]),
             "roe": (C.c_int, [C.c_double, P, P, P, P]),
@@ -253,6 +254,11 @@ class CpuSolver:
     def ke_volume(self, u):
         out = np.zeros(1)
         self._check(self._fn("ke_volume")(self.ctx, ptr(np.ascontiguousarray(u)), ptr(out)))
+        return float(out[0])
+
+    def ke_total(self, u):
+        out = np.zeros(1)
+        self._check(self._fn("ke_total")(self.ctx, ptr(np.ascontiguousarray(u)), ptr(out)))
         return float(out[0])
 
     def run(self, u, steps, cfl=0.1, t_final=None, t0=0.0):

@@ -276,6 +276,23 @@ def test_ke_volume_term(quad):
     assert np.isfinite(g.rhs()).all()  # the context still steps after the diagnostic
 
 
+@pytest.mark.parametrize("quad", [0, 1])
+def test_ke_total(quad):
+    """KE change minus pressure work on the device against the oracle (Lemma 1:
+    round-off on LGL, O(1e-5) on GL for this state)."""
+    o = CpuSolver("oracle", Config(p=4, m=3, quad_kind=quad, case="tgv", roe=False))
+    g = P().GpuSolver(gpu_cfg(p=4, m=3, quad_kind=quad, case="tgv", roe=False))
+    g.init_case()
+    u = g.get_state()
+    kg, ko = g.ke_total(), o.ke_total(u)
+    if quad == 1:
+        assert abs(kg) < 1e-11 and abs(ko) < 1e-11, (kg, ko)
+    else:
+        # a sum of O(1) terms cancelling to ~1e-5: agreement at absolute round-off
+        assert abs(ko) > 1e-8 and abs(kg - ko) <= 1e-11, (kg, ko)
+    assert np.isfinite(g.rhs()).all()
+
+
 def test_tgv_entropy_conservation():
     """BASELINE configs[3] physics on a small box: EC flux, consistent face
     metrics (grid_degree = p): entropy change at round-off of |U_total|."""

@@ -157,6 +157,16 @@ def test_dg_free_stream_and_conservation(overint):
     assert drift.max() < 1e-12, drift
 
 
+def test_ke_total_lemma_1():
+    """PAPER.md Lemma 1 / SPEC.md:605-607: the kinetic-energy change minus
+    pressure work is conserved (round-off) when the surface nodes are volume
+    nodes (LGL), and not on GL nodes."""
+    lgl = CpuSolver("oracle", Config(p=3, m=3, quad_kind=1, case="tgv", roe=False))
+    gl = CpuSolver("oracle", Config(p=3, m=3, quad_kind=0, case="tgv", roe=False))
+    assert abs(lgl.ke_total(lgl.initial_state())) < 1e-11
+    assert abs(gl.ke_total(gl.initial_state())) > 1e-8
+
+
 def test_face_metric_mismatch_documented():
     """with grid_degree = p+1 on GL, neighbour face cofactors differ
     by O(1e-3) at p=3 so EC entropy change is O(dC), not round-off."""

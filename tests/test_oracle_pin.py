@@ -44,6 +44,8 @@ def test_oracle_matches_reference(cfg):
     assert o.entropy_total(u) == pytest.approx(r.entropy_total(u), rel=1e-14)
     np.testing.assert_array_equal(o.conserved_totals(u), r.conserved_totals(u))
     assert o.ke_volume(u) == r.ke_volume(u)
+    kt_o, kt_r = o.ke_total(u), r.ke_total(u)
+    assert abs(kt_o - kt_r) <= 1e-11 * max(1.0, abs(kt_r)) + 1e-12
 
 
 def test_oracle_rk4_matches_reference():
