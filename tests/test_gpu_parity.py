@@ -396,6 +396,33 @@ def _swap(ranks):
         g.halo_set(sends[(r - 1) % n][1], sends[(r + 1) % n][0])
 
 
+@pytest.mark.parametrize("scheme", ["nsfr", "dg"])
+def test_single_element_box(scheme):
+    """m = 1: the element is its own neighbour across all six faces (periodic)."""
+    kw = dict(p=4, m=1, scheme=scheme)
+    o = CpuSolver("oracle", Config(**kw))
+    g = P().GpuSolver(gpu_cfg(**kw), metrics=o.metrics())
+    g.init_case()
+    u = g.get_state()
+    assert_rhs_parity(g.rhs(), o.rhs(u), floor_of(o, u))
+
+
+@pytest.mark.parametrize("m,nranks", [(5, 2), (3, 3), (4, 4)])
+def test_uneven_and_thin_slabs(m, nranks):
+    """Uneven slabs (5 planes over 2 ranks) and one-plane slabs, where both z
+    neighbours of every element come from halo planes: bitwise the whole box."""
+    kw = dict(p=3, m=m)
+    whole = P().GpuSolver(gpu_cfg(**kw))
+    whole.init_case()
+    ranks = [P().GpuSolver(gpu_cfg(rank=r, nranks=nranks, **kw)) for r in range(nranks)]
+    for g in ranks:
+        g.init_case()
+        g.project()
+    _swap(ranks)
+    rhs = np.concatenate([g.residual() for g in ranks])
+    np.testing.assert_array_equal(rhs, whole.rhs())
+
+
 @pytest.mark.parametrize("nranks", [2, 3])
 def test_slab_halo_path_matches_whole_box(nranks):
     """The multi-GPU data path on one GPU: z-slab contexts in external-halo mode
