@@ -4,6 +4,7 @@
 #include <nccl.h>
 
 #include <algorithm>
+#include <atomic>
 #include <cmath>
 #include <cstdio>
 #include <cstring>
@@ -44,6 +45,7 @@ struct nsfr_gpu_ctx {
   // ut_vol/traces hold the projection of d_un and lam_bits its lambda_max
   // (K3 re-projects after every stage); cleared when d_un changes from outside
   bool proj_valid = false;
+  int ahead_proj = 0, ahead_res = 0, ahead_upd = 0;  // look-ahead L2 prefetch distances (CTAs)
   long long launches = 0;
   // per-launch event timing (bench roofline)
   bool timing = false;
@@ -78,20 +80,26 @@ size_t nsol(const nsfr_gpu_ctx* c) { return static_cast<size_t>(c->N) * c->N * c
 size_t state_count(const nsfr_gpu_ctx* c) { return static_cast<size_t>(c->E) * NS * nsol(c); }
 size_t nquad(const nsfr_gpu_ctx* c) { return static_cast<size_t>(c->NQ) * c->NQ * c->NQ; }
 
-// Per-N launch configuration of the persistent kernels: resident CTAs on the device.
+// Kernel attributes (dynamic shared memory above 48 KB) are per device: the
+// devices already configured, per instantiation (one thread per GPU may share
+// the process). The look-ahead distances live in the context.
 template <int N>
-struct Resident {
-  static inline int proj = 0, res = 0, upd = 0;
+struct AttrsDone {
+  static inline std::atomic<unsigned> mask{0};
 };
 
 template <int N>
 int set_attrs(nsfr_gpu_ctx* ctx) {
-  if (Resident<N>::res) return NSFR_OK;
-  CK(cudaFuncSetAttribute(k_project<N>, cudaFuncAttributeMaxDynamicSharedMemorySize, ProjCfg<N>::SMEM));
-  CK(cudaFuncSetAttribute(k_residual<N>, cudaFuncAttributeMaxDynamicSharedMemorySize, ResCfg<N>::SMEM));
-  CK(cudaFuncSetAttribute(k_residual<N, 1>, cudaFuncAttributeMaxDynamicSharedMemorySize, ResCfg<N>::SMEM));
-  CK(cudaFuncSetAttribute(k_residual<N, 2>, cudaFuncAttributeMaxDynamicSharedMemorySize, ResCfg<N>::SMEM));
-  CK(cudaFuncSetAttribute(k_update<N>, cudaFuncAttributeMaxDynamicSharedMemorySize, UpdCfg<N>::SMEM));
+  if (ctx->ahead_res) return NSFR_OK;
+  const unsigned bit = 1u << (ctx->s.device & 31);
+  if (!(AttrsDone<N>::mask.load() & bit)) {
+    CK(cudaFuncSetAttribute(k_project<N>, cudaFuncAttributeMaxDynamicSharedMemorySize, ProjCfg<N>::SMEM));
+    CK(cudaFuncSetAttribute(k_residual<N>, cudaFuncAttributeMaxDynamicSharedMemorySize, ResCfg<N>::SMEM));
+    CK(cudaFuncSetAttribute(k_residual<N, 1>, cudaFuncAttributeMaxDynamicSharedMemorySize, ResCfg<N>::SMEM));
+    CK(cudaFuncSetAttribute(k_residual<N, 2>, cudaFuncAttributeMaxDynamicSharedMemorySize, ResCfg<N>::SMEM));
+    CK(cudaFuncSetAttribute(k_update<N>, cudaFuncAttributeMaxDynamicSharedMemorySize, UpdCfg<N>::SMEM));
+    AttrsDone<N>::mask.fetch_or(bit);
+  }
   int sms = 0, bp = 0, br = 0, bu = 0;
   CK(cudaDeviceGetAttribute(&sms, cudaDevAttrMultiProcessorCount, ctx->s.device));
   CK(cudaOccupancyMaxActiveBlocksPerMultiprocessor(&bp, k_project<N>, ProjCfg<N>::THREADS, ProjCfg<N>::SMEM));
@@ -105,9 +113,9 @@ int set_attrs(nsfr_gpu_ctx* ctx) {
   const double waves = w ? std::atof(w) : (N == 5 ? 0.25 : 0.0);
   const bool pf = std::getenv("NSFR_NO_PREFETCH") == nullptr && waves > 0.0;
   auto ahead = [&](int blocks) { return pf ? static_cast<int>(waves * sms * std::max(blocks, 1)) : (1 << 30); };
-  Resident<N>::proj = ahead(bp);
-  Resident<N>::res = ahead(br);
-  Resident<N>::upd = ahead(bu);
+  ctx->ahead_proj = ahead(bp);
+  ctx->ahead_res = ahead(br);
+  ctx->ahead_upd = ahead(bu);
   return NSFR_OK;
 }
 
@@ -217,7 +225,7 @@ int launch_project(nsfr_gpu_ctx* ctx, const double* u, bool want_lam) {
   const int grid = (ctx->E + ProjCfg<N>::EPB - 1) / ProjCfg<N>::EPB;
   ev_begin(ctx, 1);
   k_project<N><<<grid, ProjCfg<N>::THREADS, ProjCfg<N>::SMEM, ctx->st>>>(P, proj_ops<N>(ctx),
-                                                                         Resident<N>::proj);
+                                                                         ctx->ahead_proj);
   ev_end(ctx);
   ++ctx->launches;
   CK(cudaGetLastError());
@@ -245,13 +253,13 @@ int launch_residual(nsfr_gpu_ctx* ctx, int km) {
   ev_begin(ctx, 2);
   if (km == 1)
     k_residual<N, 1><<<grid, ResCfg<N>::THREADS, ResCfg<N>::SMEM, ctx->st>>>(P, res_ops<N>(ctx->htab),
-                                                                           Resident<N>::res);
+                                                                           ctx->ahead_res);
   else if (km == 2)
     k_residual<N, 2><<<grid, ResCfg<N>::THREADS, ResCfg<N>::SMEM, ctx->st>>>(P, res_ops<N>(ctx->htab),
-                                                                           Resident<N>::res);
+                                                                           ctx->ahead_res);
   else
     k_residual<N><<<grid, ResCfg<N>::THREADS, ResCfg<N>::SMEM, ctx->st>>>(P, res_ops<N>(ctx->htab),
-                                                                           Resident<N>::res);
+                                                                           ctx->ahead_res);
   ev_end(ctx);
   ++ctx->launches;
   CK(cudaGetLastError());
@@ -279,7 +287,7 @@ int launch_update(nsfr_gpu_ctx* ctx, int stage, bool entropy, const double* vhat
   const int grid = (ctx->E + UpdCfg<N>::EPB - 1) / UpdCfg<N>::EPB;
   ev_begin(ctx, 3);
   k_update<N><<<grid, UpdCfg<N>::THREADS, UpdCfg<N>::SMEM, ctx->st>>>(P, upd_ops<N>(ctx, stage),
-                                                                      Resident<N>::upd);
+                                                                      ctx->ahead_upd);
   ev_end(ctx);
   ++ctx->launches;
   CK(cudaGetLastError());
@@ -332,14 +340,19 @@ DgOps<NP, NQ> dg_ops(const nsfr_gpu_ctx* ctx) {
 }
 
 template <int NP, int NQ>
+struct DgAttrsDone {
+  static inline std::atomic<unsigned> mask{0};
+};
+
+template <int NP, int NQ>
 int dg_attrs(nsfr_gpu_ctx* ctx) {
   using Cfg = DgCfg<NP, NQ>;
-  static bool done = false;
-  if (!done) {
+  const unsigned bit = 1u << (ctx->s.device & 31);
+  if (!(DgAttrsDone<NP, NQ>::mask.load() & bit)) {
     CK(cudaFuncSetAttribute(k_dg_states<NP, NQ>, cudaFuncAttributeMaxDynamicSharedMemorySize, Cfg::S_SMEM));
     CK(cudaFuncSetAttribute(k_dg_residual<NP, NQ>, cudaFuncAttributeMaxDynamicSharedMemorySize,
                             Cfg::R_SMEM));
-    done = true;
+    DgAttrsDone<NP, NQ>::mask.fetch_or(bit);
   }
   return NSFR_OK;
 }
