@@ -149,7 +149,9 @@ __device__ __forceinline__ void upd_prefetch(const UpdParams& P, int e0, int tid
   }
 }
 
-template <int N>
+// IDF: chi Pi~ = I (c_DG, where Pi~ = Pi = chi^-1): the RK stages skip the final
+// three (chi Pi~) passes (round-off-level change; the host decides).
+template <int N, bool IDF>
 __device__ __forceinline__ void upd_batch(const UpdParams& P, const UpdOps<N>& O, int e0, double* sm) {
   using Cfg = UpdCfg<N>;
   constexpr int N2 = Cfg::N2, N3 = Cfg::N3, EPB = Cfg::EPB;
@@ -233,10 +235,12 @@ __device__ __forceinline__ void upd_batch(const UpdParams& P, const UpdOps<N>& O
   }
   PHASE_MARK(9);
   // second half of S10: Pi~ along xi, eta
-  tail_pass<N, 0, false, false>(T.fr, T.bs, nullptr, 0, R0, VS, R1, VS, WJ, nbs, tid, nthr);
-  __syncthreads();
-  tail_pass<N, 1, false, false>(T.fr, T.bs, nullptr, 0, R1, VS, R2, VS, WJ, nbs, tid, nthr);
-  __syncthreads();
+  if constexpr (!IDF) {
+    tail_pass<N, 0, false, false>(T.fr, T.bs, nullptr, 0, R0, VS, R1, VS, WJ, nbs, tid, nthr);
+    __syncthreads();
+    tail_pass<N, 1, false, false>(T.fr, T.bs, nullptr, 0, R1, VS, R2, VS, WJ, nbs, tid, nthr);
+    __syncthreads();
+  }
   // Pi~ along zeta, negate, RK stage epilogue (zeta lines: coalesced across the
   // warp); u_{s+1} also lands in R0 for the projection below
   const double dt = P.stage ? *P.dt : 0.0;
@@ -246,7 +250,7 @@ __device__ __forceinline__ void upd_batch(const UpdParams& P, const UpdOps<N>& O
     const int it = tid + j * nthr;
     if (it >= nbs * N2) break;
     const int bsi = it / N2, l = it - bsi * N2;
-    const double* src = R2 + bsi * N3 + l;
+    const double* src = (IDF ? R0 : R2) + bsi * N3 + l;  // IDF: each thread rewrites only its own line
     double x[N];
 #pragma unroll
     for (int a = 0; a < N; ++a) x[a] = src[a * N2];
@@ -255,8 +259,12 @@ __device__ __forceinline__ void upd_batch(const UpdParams& P, const UpdOps<N>& O
 #pragma unroll
     for (int c = 0; c < N; ++c) {
       double z = 0.0;
+      if constexpr (IDF) {
+        z = x[c];
+      } else {
 #pragma unroll
-      for (int a = 0; a < N; ++a) z = fma(T.fr[c * N + a], x[a], z);
+        for (int a = 0; a < N; ++a) z = fma(T.fr[c * N + a], x[a], z);
+      }
       const double kv = -z;
       const size_t gi = gb + c * N2;
       switch (P.stage) {
@@ -289,14 +297,14 @@ __device__ __forceinline__ void upd_batch(const UpdParams& P, const UpdOps<N>& O
 }
 
 // One batch per CTA with look-ahead L2 prefetch (see k_residual).
-template <int N>
+template <int N, bool IDF = false>
 __global__ void __launch_bounds__(UpdCfg<N>::THREADS, UpdCfg<N>::MINB)
     k_update(UpdParams P, UpdOps<N> O, int ahead) {
   extern __shared__ __align__(128) double sm[];
   constexpr int EPB = UpdCfg<N>::EPB;
   const long long pe = (static_cast<long long>(blockIdx.x) + ahead) * EPB;
   if (pe < P.pj.E) upd_prefetch<N>(P, static_cast<int>(pe), threadIdx.x);
-  upd_batch<N>(P, O, blockIdx.x * EPB, sm);
+  upd_batch<N, IDF>(P, O, blockIdx.x * EPB, sm);
 }
 
 }  // namespace nsfr_b200

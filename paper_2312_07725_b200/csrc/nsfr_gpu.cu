@@ -45,6 +45,7 @@ struct nsfr_gpu_ctx {
   // ut_vol/traces hold the projection of d_un and lam_bits its lambda_max
   // (K3 re-projects after every stage); cleared when d_un changes from outside
   bool proj_valid = false;
+  bool chi_pi_identity = false;  // chi Pi~ = I to 1e-13 (c_DG): K3 skips the final passes
   int ahead_proj = 0, ahead_res = 0, ahead_upd = 0;  // look-ahead L2 prefetch distances (CTAs)
   long long launches = 0;
   // per-launch event timing (bench roofline)
@@ -98,6 +99,7 @@ int set_attrs(nsfr_gpu_ctx* ctx) {
     CK(cudaFuncSetAttribute(k_residual<N, 1>, cudaFuncAttributeMaxDynamicSharedMemorySize, ResCfg<N>::SMEM));
     CK(cudaFuncSetAttribute(k_residual<N, 2>, cudaFuncAttributeMaxDynamicSharedMemorySize, ResCfg<N>::SMEM));
     CK(cudaFuncSetAttribute(k_update<N>, cudaFuncAttributeMaxDynamicSharedMemorySize, UpdCfg<N>::SMEM));
+    CK(cudaFuncSetAttribute(k_update<N, true>, cudaFuncAttributeMaxDynamicSharedMemorySize, UpdCfg<N>::SMEM));
     AttrsDone<N>::mask.fetch_or(bit);
   }
   int sms = 0, bp = 0, br = 0, bu = 0;
@@ -286,8 +288,12 @@ int launch_update(nsfr_gpu_ctx* ctx, int stage, bool entropy, const double* vhat
   if (int rc = set_attrs<N>(ctx)) return rc;
   const int grid = (ctx->E + UpdCfg<N>::EPB - 1) / UpdCfg<N>::EPB;
   ev_begin(ctx, 3);
-  k_update<N><<<grid, UpdCfg<N>::THREADS, UpdCfg<N>::SMEM, ctx->st>>>(P, upd_ops<N>(ctx, stage),
-                                                                      ctx->ahead_upd);
+  if (stage > 0 && ctx->chi_pi_identity)
+    k_update<N, true><<<grid, UpdCfg<N>::THREADS, UpdCfg<N>::SMEM, ctx->st>>>(P, upd_ops<N>(ctx, stage),
+                                                                            ctx->ahead_upd);
+  else
+    k_update<N><<<grid, UpdCfg<N>::THREADS, UpdCfg<N>::SMEM, ctx->st>>>(P, upd_ops<N>(ctx, stage),
+                                                                        ctx->ahead_upd);
   ev_end(ctx);
   ++ctx->launches;
   CK(cudaGetLastError());
@@ -731,6 +737,16 @@ int nsfr_gpu_create(const nsfr_gpu_setup* setup, nsfr_gpu_ctx** out) {
   DevTables dt;
   fill_dev_tables(ctx->tab, s.tables && s.tables->interp ? s.tables : nullptr, dt);
   ctx->htab = dt;
+  if (!ctx->dg && std::getenv("NSFR_NO_IDENTITY_SKIP") == nullptr) {
+    double dev = 0.0;  // max |chi Pi~ - I| (n_q = n_p)
+    for (int c = 0; c < ctx->N; ++c)
+      for (int a = 0; a < ctx->N; ++a) {
+        double v = 0.0;
+        for (int r = 0; r < ctx->N; ++r) v += dt.interp[c * ctx->N + r] * dt.frproj[r * ctx->N + a];
+        dev = std::max(dev, std::fabs(v - (c == a ? 1.0 : 0.0)));
+      }
+    ctx->chi_pi_identity = dev < 1e-13;
+  }
   const size_t ns = state_count(ctx), n3 = static_cast<size_t>(ctx->E) * nquad(ctx);
   const size_t ntr = static_cast<size_t>(ctx->E) * 6 * NS * ctx->NQ * ctx->NQ;
   const size_t nscr = static_cast<size_t>(ctx->E) * NS * std::max(nsol(ctx), nquad(ctx));
