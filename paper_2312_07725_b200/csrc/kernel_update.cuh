@@ -149,9 +149,11 @@ __device__ __forceinline__ void upd_prefetch(const UpdParams& P, int e0, int tid
   }
 }
 
-// IDF: chi Pi~ = I (c_DG, where Pi~ = Pi = chi^-1): the RK stages skip the final
-// three (chi Pi~) passes (round-off-level change; the host decides).
-template <int N, bool IDF>
+// chi Pi~ = I (c_DG, where Pi~ = Pi = chi^-1; the host decides, round-off-level
+// change): IDM: M = Pi~^T chi^T = I as well, so lift + first half of the WA
+// inverse reduce to the pointwise face injection and 1/(w J) (same fma order);
+// IDF: the RK stages also skip the final three (chi Pi~) passes.
+template <int N, bool IDM, bool IDF>
 __device__ __forceinline__ void upd_batch(const UpdParams& P, const UpdOps<N>& O, int e0, double* sm) {
   using Cfg = UpdCfg<N>;
   constexpr int N2 = Cfg::N2, N3 = Cfg::N3, EPB = Cfg::EPB;
@@ -196,7 +198,24 @@ __device__ __forceinline__ void upd_batch(const UpdParams& P, const UpdOps<N>& O
   __syncthreads();
   PHASE_MARK(8);
 
-  if (!P.dS) {
+  if (IDM && !P.dS) {
+    // M = I: vol + b_f (x) facc_f injected per node (x, y, z faces in the pass
+    // order), times 1/(w J)
+    for (int it = tid; it < nbs * N3; it += nthr) {
+      const int bsi = it / N3, q = it - bsi * N3, b = bsi / 5, s = bsi - 5 * b;
+      const int i = q % N, j = (q / N) % N, k = q / N2;
+      const double* fb = R3 + b * FS + (s * 2) * N2;
+      double v = R0[it];
+      v = fma(T.bm[i], fb[j + N * k], v);
+      v = fma(T.bm[N + i], fb[N2 + j + N * k], v);
+      v = fma(T.bm[j], fb[10 * N2 + i + N * k], v);
+      v = fma(T.bm[N + j], fb[10 * N2 + N2 + i + N * k], v);
+      v = fma(T.bm[k], fb[20 * N2 + i + N * j], v);
+      v = fma(T.bm[N + k], fb[20 * N2 + N2 + i + N * j], v);
+      R0[it] = v * WJ[b * N3 + q];
+    }
+    __syncthreads();
+  } else if (!P.dS) {
     // Pi~^T S9 in three fused passes; 1/(w J) in the last
     tail_pass<N, 0, true, false>(T.M, T.bm, R3, FS, R0, VS, R1, VS, WJ, nbs, tid, nthr);
     tail_face_pass<N, 0>(T.M, R3 + 10 * N2, FS, R4, FS, nb, tid, nthr);
@@ -297,14 +316,14 @@ __device__ __forceinline__ void upd_batch(const UpdParams& P, const UpdOps<N>& O
 }
 
 // One batch per CTA with look-ahead L2 prefetch (see k_residual).
-template <int N, bool IDF = false>
+template <int N, bool IDM = false, bool IDF = false>
 __global__ void __launch_bounds__(UpdCfg<N>::THREADS, UpdCfg<N>::MINB)
     k_update(UpdParams P, UpdOps<N> O, int ahead) {
   extern __shared__ __align__(128) double sm[];
   constexpr int EPB = UpdCfg<N>::EPB;
   const long long pe = (static_cast<long long>(blockIdx.x) + ahead) * EPB;
   if (pe < P.pj.E) upd_prefetch<N>(P, static_cast<int>(pe), threadIdx.x);
-  upd_batch<N, IDF>(P, O, blockIdx.x * EPB, sm);
+  upd_batch<N, IDM, IDF>(P, O, blockIdx.x * EPB, sm);
 }
 
 }  // namespace nsfr_b200

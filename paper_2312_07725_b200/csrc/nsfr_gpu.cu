@@ -99,7 +99,10 @@ int set_attrs(nsfr_gpu_ctx* ctx) {
     CK(cudaFuncSetAttribute(k_residual<N, 1>, cudaFuncAttributeMaxDynamicSharedMemorySize, ResCfg<N>::SMEM));
     CK(cudaFuncSetAttribute(k_residual<N, 2>, cudaFuncAttributeMaxDynamicSharedMemorySize, ResCfg<N>::SMEM));
     CK(cudaFuncSetAttribute(k_update<N>, cudaFuncAttributeMaxDynamicSharedMemorySize, UpdCfg<N>::SMEM));
-    CK(cudaFuncSetAttribute(k_update<N, true>, cudaFuncAttributeMaxDynamicSharedMemorySize, UpdCfg<N>::SMEM));
+    CK(cudaFuncSetAttribute(k_update<N, true, false>, cudaFuncAttributeMaxDynamicSharedMemorySize,
+                            UpdCfg<N>::SMEM));
+    CK(cudaFuncSetAttribute(k_update<N, true, true>, cudaFuncAttributeMaxDynamicSharedMemorySize,
+                            UpdCfg<N>::SMEM));
     AttrsDone<N>::mask.fetch_or(bit);
   }
   int sms = 0, bp = 0, br = 0, bu = 0;
@@ -288,9 +291,12 @@ int launch_update(nsfr_gpu_ctx* ctx, int stage, bool entropy, const double* vhat
   if (int rc = set_attrs<N>(ctx)) return rc;
   const int grid = (ctx->E + UpdCfg<N>::EPB - 1) / UpdCfg<N>::EPB;
   ev_begin(ctx, 3);
-  if (stage > 0 && ctx->chi_pi_identity)
-    k_update<N, true><<<grid, UpdCfg<N>::THREADS, UpdCfg<N>::SMEM, ctx->st>>>(P, upd_ops<N>(ctx, stage),
-                                                                            ctx->ahead_upd);
+  if (ctx->chi_pi_identity && stage > 0)
+    k_update<N, true, true><<<grid, UpdCfg<N>::THREADS, UpdCfg<N>::SMEM, ctx->st>>>(
+        P, upd_ops<N>(ctx, stage), ctx->ahead_upd);
+  else if (ctx->chi_pi_identity && !entropy)
+    k_update<N, true, false><<<grid, UpdCfg<N>::THREADS, UpdCfg<N>::SMEM, ctx->st>>>(
+        P, upd_ops<N>(ctx, stage), ctx->ahead_upd);
   else
     k_update<N><<<grid, UpdCfg<N>::THREADS, UpdCfg<N>::SMEM, ctx->st>>>(P, upd_ops<N>(ctx, stage),
                                                                         ctx->ahead_upd);
