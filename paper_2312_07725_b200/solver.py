@@ -68,6 +68,12 @@ class _Tables(C.Structure):
 SCHEMES = {"nsfr": 0, "dg": 1}
 
 
+def _scheme_id(name: str) -> int:
+    if name not in SCHEMES:
+        raise ConfigError(f"scheme must be one of {sorted(SCHEMES)}, got {name!r}")
+    return SCHEMES[name]
+
+
 class _Setup(C.Structure):
     _fields_ = [
         ("p", C.c_int), ("quad_kind", C.c_int), ("c1d", C.c_double), ("gamma", C.c_double),
@@ -246,7 +252,7 @@ class GpuSolver:
                    cfg.p + 1 if cfg.grid_degree is None else cfg.grid_degree, cfg.device,
                    int(cfg.entropy_diag), tab_ptr, _ptr(jac), _ptr(cof),
                    C.cast(idbuf, C.c_void_p) if idbuf is not None else None, cfg.rank, cfg.nranks,
-                   SCHEMES[cfg.scheme], cfg.overint)
+                   _scheme_id(cfg.scheme), cfg.overint)
         h = C.c_void_p()
         rc = self.lib.nsfr_gpu_create(C.byref(s), C.byref(h))
         if rc:
@@ -263,7 +269,9 @@ class GpuSolver:
         if rc:
             msg = self.lib.nsfr_gpu_last_error(self.ctx).decode()
             if rc == NSFR_E_INADMISSIBLE:
-                raise StepFailureError(msg)
+                t = np.zeros(1)  # the failing stage's step time (StepFailureError{t})
+                ok = self.lib.nsfr_gpu_get_time(self.ctx, _ptr(t)) == NSFR_OK
+                raise StepFailureError(msg, float(t[0]) if ok else None)
             raise _ERRORS.get(rc, NsfrError)(msg)
 
     def close(self):

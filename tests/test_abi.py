@@ -66,3 +66,9 @@ def test_no_cpu_fallback_without_device():
 def test_bad_config_raises_dimension_error():
     with pytest.raises(P.DimensionError):
         P.GpuSolver(P.SolverConfig(p=9, m=2))
+
+
+def test_unknown_scheme_is_a_config_error():
+    import paper_2312_07725_b200 as pkg
+    with pytest.raises(pkg.ConfigError):
+        pkg.GpuSolver(pkg.SolverConfig(p=3, m=2, scheme="bogus"))

@@ -335,8 +335,9 @@ def test_inadmissible_state_raises():
     u = g.get_state()
     u[3, 0, 5] = -1.0  # negative density
     g.set_state(u)
-    with pytest.raises(pkg.StepFailureError):
+    with pytest.raises(pkg.StepFailureError) as ei:
         g.rhs()
+    assert ei.value.t == 0.0
     g.init_case()  # the context stays usable
     assert np.isfinite(g.rhs()).all()
 
