@@ -49,7 +49,8 @@ namespace nsfr_b200 {
   }
 
 template <int N, bool KE>
-__device__ __forceinline__ void vol_pairs(const double* Pd, const double* Ch, double* acc,
+__device__ __forceinline__ void vol_pairs(const double* __restrict__ Pd, const double* __restrict__ Ch,
+                                          double* __restrict__ acc,
                                           const double (&q)[N * N], double wt, int lbase,
                                           int stride, int dir, unsigned amask) {
   constexpr int N3 = N * N * N;
@@ -179,9 +180,10 @@ __device__ __forceinline__ void res_batch(const ResParams& P, const ResOps<N>& O
     const int b = lb, e = e0 + b, dir = ldir, t1 = lrem % N, t2 = lrem / N;
     const int stride = dir == 0 ? 1 : (dir == 1 ? N : N2);
     const int lbase = dir == 0 ? N * (t1 + N * t2) : (dir == 1 ? t1 + N2 * t2 : t1 + N * t2);
-    const double* Pd = PRIM + b * 6 * N3;
-    const double* Ch = COF + b * 9 * N3;
-    double* acc = ACCV + b * AS + dir * 5 * N3;
+    // disjoint shared-memory regions: lets the next pair's loads pass this pair's stores
+    const double* __restrict__ Pd = PRIM + b * 6 * N3;
+    const double* __restrict__ Ch = COF + b * 9 * N3;
+    double* __restrict__ acc = ACCV + b * AS + dir * 5 * N3;
     const double wt = O.wq[t1] * O.wq[t2];
 #pragma unroll
     for (int a = 0; a < N; ++a)
