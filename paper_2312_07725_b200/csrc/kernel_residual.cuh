@@ -48,13 +48,16 @@ namespace nsfr_b200 {
     _Pragma("unroll") for (int s = 0; s < NS; ++s) acc[s * N3 + ia] += fa[s];                  \
   }
 
+#ifndef NSFR_UNROLL_MAXN
+#define NSFR_UNROLL_MAXN 4
+#endif
 template <int N, bool KE>
 __device__ __forceinline__ void vol_pairs(const double* __restrict__ Pd, const double* __restrict__ Ch,
                                           double* __restrict__ acc,
                                           const double (&q)[N * N], double wt, int lbase,
                                           int stride, int dir, unsigned amask) {
   constexpr int N3 = N * N * N;
-  if constexpr (N <= 4) {
+  if constexpr (N <= NSFR_UNROLL_MAXN) {
 #define NSFR_INNER_UNROLL _Pragma("unroll")
 #pragma unroll
     for (int a = 0; a < N - 1; ++a) NSFR_VOL_PAIRS_BODY
