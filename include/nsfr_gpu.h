@@ -150,6 +150,21 @@ int nsfr_gpu_rk4_step(nsfr_gpu_ctx* ctx, double cfl, double t_final, double* dt_
 int nsfr_gpu_advance(nsfr_gpu_ctx* ctx, int nsteps, double cfl, double t_final, double* t_out);
 /* Fixed dt variant (no wavespeed reduction): used by the parity tests. */
 int nsfr_gpu_rk4_step_dt(nsfr_gpu_ctx* ctx, double dt);
+/* One RK4 step on HOST buffers (replaces rk4_step(field, dt) on the caller's
+ * std::span state, and adaptive_dt(field, cfl),
+ * SPEC.md:475-483): the same result as set_state(u_in); dt > 0 ?
+ * rk4_step_dt(dt) : rk4_step(cfl, t_final); get_state(u_out), bitwise, with
+ * the host->device copy, the compute and the device->host copy pipelined over
+ * element chunks (pinned buffers overlap; pageable ones work without
+ * overlap). u_out may alias u_in. dt_next (may be NULL) receives
+ * adaptive_dt(u_out, cfl) clipped to t_final, computed on the way out, so a
+ * reference-style loop `dt = adaptive_dt(u); u = rk4_step(u, dt)` runs as
+ * rk4_step_host(u, u, dt, cfl, t_final, NULL, &dt) with no global reduction
+ * inside the step (dt <= 0 takes lambda_max of u_in first: one barrier).
+ * Single-rank NSFR contexts stream; slab / DG contexts run the calls in
+ * sequence. */
+int nsfr_gpu_rk4_step_host(nsfr_gpu_ctx* ctx, const double* u_in, double* u_out, double dt,
+                           double cfl, double t_final, double* dt_used, double* dt_next);
 int nsfr_gpu_max_wavespeed(nsfr_gpu_ctx* ctx, double* lam);
 
 /* L2 density/pressure error against the case's exact solution at the

@@ -1,0 +1,88 @@
+// u_hat <-> u_q state conversion (chi^3 on the way in, Pi^3 on the way out;
+// SPEC S1 / sumfac.cpp:57-78 apply_tensor_product) for n_q = n_p: the host
+// transfers of set_state / get_state and the streamed host step run it once
+// per element on the critical path, so it is a line-pass kernel at the HBM
+// roofline instead of one element per CTA. Same arithmetic as k_convert
+// (passes xi, eta, zeta; each output an fma chain from 0 in column order), so
+// the two are bitwise interchangeable.
+#pragma once
+#include "setup_kernels.cuh"
+
+namespace nsfr_b200 {
+
+template <int N>
+struct ConvOps {
+  double A[N * N];  // chi (to_quad) or Pi, row-major N x N
+};
+
+template <int N>
+struct ConvCfg {
+  static constexpr int N2 = N * N, N3 = N * N * N, LINES = 5 * N2;
+  static constexpr int EPB = N <= 5 ? 4 : 2;
+  static constexpr int THREADS = 256;
+  static constexpr int SMEM = EPB * 5 * N3 * 8;
+};
+
+// elements [e_begin, e_end): one CTA per EPB elements; each thread owns whole
+// lines, so a pass updates its lines in place (no other thread touches them).
+// LAM: no output; lambda_max = max(|u| + a) over the admissible nodes of the
+// converted state into *lam (atomicMax on the bits; u_q = chi^3 u_hat, the
+// node set and formula of K1, so adaptive_dt of a state about to leave the
+// device equals what K1 finds when it comes back).
+template <int N, bool LAM = false>
+__global__ void __launch_bounds__(ConvCfg<N>::THREADS)
+    k_convert_lines(ConvOps<N> O, const double* __restrict__ in, double* __restrict__ out, int e_begin,
+                    int e_end, double gamma = 0.0, unsigned long long* lam = nullptr) {
+  using Cfg = ConvCfg<N>;
+  constexpr int N2 = Cfg::N2, N3 = Cfg::N3, EPB = Cfg::EPB, LINES = Cfg::LINES;
+  extern __shared__ __align__(128) double S[];
+  const int e0 = e_begin + blockIdx.x * EPB;
+  const int nb = min(EPB, e_end - e0);
+  const int tid = threadIdx.x, nthr = blockDim.x;
+  __shared__ unsigned long long bar;
+  {
+    const StageBlock blk[1] = {{S, in + (size_t)e0 * 5 * N3, nb * 5 * N3}};
+    stage_issue<1>(blk, &bar);
+  }
+  __syncthreads();
+  stage_wait(&bar);
+  __syncthreads();
+#pragma unroll
+  for (int D = 0; D < 3; ++D) {
+    const int stride = D == 0 ? 1 : (D == 1 ? N : N2);
+    for (int l = tid; l < nb * LINES; l += nthr) {
+      const int b = l / LINES, r = l - b * LINES, s = r / N2, t = r - s * N2;
+      const int t1 = t % N, t2 = t / N;
+      const int base = D == 0 ? N * t1 + N2 * t2 : (D == 1 ? t1 + N2 * t2 : t1 + N * t2);
+      double* x = S + (b * 5 + s) * N3 + base;
+      double v[N];
+#pragma unroll
+      for (int a = 0; a < N; ++a) v[a] = x[a * stride];
+#pragma unroll
+      for (int row = 0; row < N; ++row) {
+        double acc = 0.0;
+#pragma unroll
+        for (int a = 0; a < N; ++a) acc = fma(O.A[row * N + a], v[a], acc);
+        if (D < 2 || LAM)
+          x[row * stride] = acc;
+        else  // zeta lines: consecutive threads write consecutive nodes
+          out[((size_t)(e0 + b) * 5 + s) * N3 + base + row * N2] = acc;
+      }
+    }
+    if (D < 2 || LAM) __syncthreads();
+  }
+  if (LAM) {
+    double lm = 0.0;
+    for (int it = tid; it < nb * N3; it += nthr) {
+      const int b = it / N3, q = it - b * N3;
+      double uu[NS];
+#pragma unroll
+      for (int s = 0; s < NS; ++s) uu[s] = S[(b * 5 + s) * N3 + q];
+      if (d_admissible(gamma, uu)) lm = fmax(lm, d_node_wavespeed(gamma, uu));
+    }
+    for (int o = 16; o > 0; o >>= 1) lm = fmax(lm, __shfl_xor_sync(0xffffffffu, lm, o));
+    if ((tid & 31) == 0 && lm > 0.0) atomicMax(lam, dbl_bits(lm));
+  }
+}
+
+}  // namespace nsfr_b200

@@ -25,8 +25,9 @@ struct ProjParams {
   double* send_hi;       // [m*m][5][N^2] face 5 of plane nz-1, or nullptr
   unsigned long long* lam;  // lambda_max bits or nullptr
   unsigned* err;
-  int E, m, nz;
+  int E, m, nz;          // E: end of the launched element range [e_begin, E) (the slab by default)
   double gamma;
+  int e_begin;           // first element of the launched range (a multiple of 8)
 };
 
 template <int N>
@@ -146,10 +147,7 @@ __device__ __forceinline__ void proj_core(const ProjParams& P, const ProjOps<N>&
 #pragma unroll
       for (int s = 0; s < NS; ++s) vv[s] = (s == 4) ? -1.0 : 0.0;
     } else if (P.lam) {
-      const double vx = uu[1] / uu[0], vy = uu[2] / uu[0], vz = uu[3] / uu[0];
-      const double speed = sqrt(vx * vx + vy * vy + vz * vz);
-      const double a = sqrt(g * d_pressure(g, uu) / uu[0]);
-      lam = fmax(lam, speed + a);
+      lam = fmax(lam, d_node_wavespeed(g, uu));
     }
 #pragma unroll
     for (int s = 0; s < NS; ++s) V[(b * 5 + s) * N3 + q] = vv[s];
@@ -239,13 +237,13 @@ template <int N>
 __global__ void __launch_bounds__(ProjCfg<N>::THREADS) k_project(ProjParams P, ProjOps<N> O, int ahead) {
   extern __shared__ __align__(128) double sm[];
   constexpr int EPB = ProjCfg<N>::EPB, N3 = N * N * N;
-  const int nbatch = (P.E + EPB - 1) / EPB;
+  const int nbatch = (P.E - P.e_begin + EPB - 1) / EPB;
   const long long pb = static_cast<long long>(blockIdx.x) + ahead;
   if (threadIdx.x == 0 && pb < nbatch) {
-    const int e0 = pb * EPB, nb = min(EPB, P.E - e0);
+    const int e0 = P.e_begin + pb * EPB, nb = min(EPB, P.E - e0);
     l2_prefetch(P.u + (size_t)e0 * 5 * N3, (size_t)nb * 5 * N3 * sizeof(double));
   }
-  proj_batch<N>(P, O, blockIdx.x * EPB, sm);
+  proj_batch<N>(P, O, P.e_begin + blockIdx.x * EPB, sm);
 }
 
 }  // namespace nsfr_b200

@@ -80,9 +80,10 @@ struct ResParams {
   double* vol;            // [E][5][N^3] volume rows
   double* facc;           // [E][3][5][2][N^2] face rows
   unsigned* err;
-  int E, m, nz;
+  int E, m, nz;           // E: end of the launched element range [e_begin, E)
   double gamma;
   int roe;
+  int e_begin;            // first element of the launched range (a multiple of 8)
 };
 
 template <int N>
@@ -306,9 +307,9 @@ __global__ void __launch_bounds__(ResCfg<N>::THREADS, ResCfg<N>::MINB)
     k_residual(ResParams P, ResOps<N> O, int ahead) {
   extern __shared__ __align__(128) double sm[];
   constexpr int EPB = ResCfg<N>::EPB;
-  const long long pe = (static_cast<long long>(blockIdx.x) + ahead) * EPB;
+  const long long pe = P.e_begin + (static_cast<long long>(blockIdx.x) + ahead) * EPB;
   if (pe < P.E) res_prefetch<N>(P, static_cast<int>(pe), threadIdx.x);
-  res_batch<N, KM>(P, O, blockIdx.x * EPB, sm);
+  res_batch<N, KM>(P, O, P.e_begin + blockIdx.x * EPB, sm);
 }
 
 }  // namespace nsfr_b200

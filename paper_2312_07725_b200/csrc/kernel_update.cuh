@@ -321,9 +321,9 @@ __global__ void __launch_bounds__(UpdCfg<N>::THREADS, UpdCfg<N>::MINB)
     k_update(UpdParams P, UpdOps<N> O, int ahead) {
   extern __shared__ __align__(128) double sm[];
   constexpr int EPB = UpdCfg<N>::EPB;
-  const long long pe = (static_cast<long long>(blockIdx.x) + ahead) * EPB;
+  const long long pe = P.pj.e_begin + (static_cast<long long>(blockIdx.x) + ahead) * EPB;
   if (pe < P.pj.E) upd_prefetch<N>(P, static_cast<int>(pe), threadIdx.x);
-  upd_batch<N, IDM, IDF>(P, O, blockIdx.x * EPB, sm);
+  upd_batch<N, IDM, IDF>(P, O, P.pj.e_begin + blockIdx.x * EPB, sm);
 }
 
 }  // namespace nsfr_b200

@@ -4,8 +4,10 @@
 //   kernel_residual.cuh K2: Hadamard volume/surface pairs, EC+Roe faces -> volume/face rows
 //   kernel_update.cuh   K3: lift, WA inverse, RK stage update + projection of the next stage
 //   kernel_dg.cuh       conservative strong-form DG: KD1 face states, KD2 residual
+//   kernel_convert.cuh  u_hat <-> u_q conversion of the host transfers (line passes)
 #pragma once
 #include "kernel_project.cuh"
 #include "kernel_residual.cuh"
 #include "kernel_update.cuh"
 #include "kernel_dg.cuh"
+#include "kernel_convert.cuh"

@@ -37,6 +37,7 @@ struct nsfr_gpu_ctx {
   unsigned* h_err = nullptr;    // pinned
   cudaStream_t st = nullptr;
   cudaStream_t st_copy = nullptr;  // host<->device state transfers, chunk-pipelined with st
+  cudaStream_t st_d2h = nullptr;   // device->host leg of the streamed step (runs beside st_copy)
   std::vector<cudaEvent_t> chunk_ev;
   ncclComm_t comm = nullptr;
   int rank = 0, nranks = 1, peer_lo = 0, peer_hi = 0;
@@ -223,11 +224,17 @@ ProjParams proj_params(nsfr_gpu_ctx* ctx, const double* u, bool want_lam) {
   return P;
 }
 
+// Launches cover the element range [ea, eb) (eb < 0: the whole slab); ea is a
+// multiple of 8 so every batch's TMA blocks stay 16-byte aligned.
+int range_end(const nsfr_gpu_ctx* ctx, int eb) { return eb < 0 ? ctx->E : eb; }
+
 template <int N>
-int launch_project(nsfr_gpu_ctx* ctx, const double* u, bool want_lam) {
+int launch_project(nsfr_gpu_ctx* ctx, const double* u, bool want_lam, int ea, int eb) {
   if (int rc = set_attrs<N>(ctx)) return rc;
-  const ProjParams P = proj_params(ctx, u, want_lam);
-  const int grid = (ctx->E + ProjCfg<N>::EPB - 1) / ProjCfg<N>::EPB;
+  ProjParams P = proj_params(ctx, u, want_lam);
+  P.e_begin = ea;
+  P.E = range_end(ctx, eb);
+  const int grid = (P.E - ea + ProjCfg<N>::EPB - 1) / ProjCfg<N>::EPB;
   ev_begin(ctx, 1);
   k_project<N><<<grid, ProjCfg<N>::THREADS, ProjCfg<N>::SMEM, ctx->st>>>(P, proj_ops<N>(ctx),
                                                                          ctx->ahead_proj);
@@ -238,7 +245,7 @@ int launch_project(nsfr_gpu_ctx* ctx, const double* u, bool want_lam) {
 }
 
 template <int N>
-int launch_residual(nsfr_gpu_ctx* ctx, int km) {
+int launch_residual(nsfr_gpu_ctx* ctx, int km, int ea, int eb) {
   ResParams P{};
   P.ut_vol = ctx->d_utv;
   P.traces = ctx->d_tr;
@@ -253,8 +260,10 @@ int launch_residual(nsfr_gpu_ctx* ctx, int km) {
   P.nz = ctx->nz;
   P.gamma = ctx->s.gamma;
   P.roe = ctx->s.roe;
+  P.e_begin = ea;
+  P.E = range_end(ctx, eb);
   if (int rc = set_attrs<N>(ctx)) return rc;
-  const int grid = (ctx->E + ResCfg<N>::EPB - 1) / ResCfg<N>::EPB;
+  const int grid = (P.E - ea + ResCfg<N>::EPB - 1) / ResCfg<N>::EPB;
   ev_begin(ctx, 2);
   if (km == 1)
     k_residual<N, 1><<<grid, ResCfg<N>::THREADS, ResCfg<N>::SMEM, ctx->st>>>(P, res_ops<N>(ctx->htab),
@@ -274,7 +283,7 @@ int launch_residual(nsfr_gpu_ctx* ctx, int km) {
 // stage 0: dU/dt (+ entropy change); stages 1-4: RK update and projection of
 // the next stage state (lambda_max after stage 4)
 template <int N>
-int launch_update(nsfr_gpu_ctx* ctx, int stage, bool entropy, const double* vhat) {
+int launch_update(nsfr_gpu_ctx* ctx, int stage, bool entropy, const double* vhat, int ea, int eb) {
   UpdParams P{};
   P.vol = ctx->d_vol;
   P.facc = ctx->d_facc;
@@ -288,8 +297,10 @@ int launch_update(nsfr_gpu_ctx* ctx, int stage, bool entropy, const double* vhat
   P.stage = stage;
   P.pj = proj_params(ctx, nullptr, stage == 4);
   P.pj.vhat = nullptr;
+  P.pj.e_begin = ea;
+  P.pj.E = range_end(ctx, eb);
   if (int rc = set_attrs<N>(ctx)) return rc;
-  const int grid = (ctx->E + UpdCfg<N>::EPB - 1) / UpdCfg<N>::EPB;
+  const int grid = (P.pj.E - ea + UpdCfg<N>::EPB - 1) / UpdCfg<N>::EPB;
   ev_begin(ctx, 3);
   if (ctx->chi_pi_identity && stage > 0)
     k_update<N, true, true><<<grid, UpdCfg<N>::THREADS, UpdCfg<N>::SMEM, ctx->st>>>(
@@ -317,12 +328,17 @@ int launch_update(nsfr_gpu_ctx* ctx, int stage, bool entropy, const double* vhat
   ctx->msg = "unsupported p";                  \
   return NSFR_E_DIM
 
-int project(nsfr_gpu_ctx* ctx, const double* u, bool lam) { NSFR_DISPATCH(launch_project, (ctx, u, lam)); }
+int project(nsfr_gpu_ctx* ctx, const double* u, bool lam, int ea = 0, int eb = -1) {
+  NSFR_DISPATCH(launch_project, (ctx, u, lam, ea, eb));
+}
 // km: 0 the residual, 1 / 2 kinetic-energy diagnostic rows (kernel_residual.cuh)
-int residual(nsfr_gpu_ctx* ctx, int km = 0) { NSFR_DISPATCH(launch_residual, (ctx, km)); }
+int residual(nsfr_gpu_ctx* ctx, int km = 0, int ea = 0, int eb = -1) {
+  NSFR_DISPATCH(launch_residual, (ctx, km, ea, eb));
+}
 // entropy: stage-0 diagnostic -vhat . R, with vhat = v_hat (default) or the given coefficients
-int update(nsfr_gpu_ctx* ctx, int stage, bool entropy, const double* vhat = nullptr) {
-  NSFR_DISPATCH(launch_update, (ctx, stage, entropy, vhat));
+int update(nsfr_gpu_ctx* ctx, int stage, bool entropy, const double* vhat = nullptr, int ea = 0,
+           int eb = -1) {
+  NSFR_DISPATCH(launch_update, (ctx, stage, entropy, vhat, ea, eb));
 }
 
 // ---- conservative DG (kernel_dg.cuh) ------------------------------------------
@@ -613,8 +629,60 @@ int setup_kernel_smem(nsfr_gpu_ctx* ctx, size_t bytes, const void* fn) {
   return NSFR_OK;
 }
 
-// u_hat <-> u_q (k_convert) of elements [e0, e1): to_quad applies chi^3, else Pi^3
+// lam_out: instead of writing out, lambda_max of chi^3 in into d_step->lam_out_bits
+template <int N>
+int launch_convert_lines(nsfr_gpu_ctx* ctx, const double* in, double* out, bool to_quad, int e0, int e1,
+                         bool lam_out) {
+  using Cfg = ConvCfg<N>;
+  const unsigned bit = 1u << (ctx->s.device & 31);
+  static std::atomic<unsigned> done{0};
+  if (!(done.load() & bit)) {
+    CK(cudaFuncSetAttribute(k_convert_lines<N>, cudaFuncAttributeMaxDynamicSharedMemorySize, Cfg::SMEM));
+    CK(cudaFuncSetAttribute(k_convert_lines<N, true>, cudaFuncAttributeMaxDynamicSharedMemorySize,
+                            Cfg::SMEM));
+    done.fetch_or(bit);
+  }
+  ConvOps<N> o{};
+  for (int i = 0; i < N * N; ++i) o.A[i] = to_quad ? ctx->htab.interp[i] : ctx->htab.proj[i];
+  const int grid = (e1 - e0 + Cfg::EPB - 1) / Cfg::EPB;
+  if (lam_out)
+    k_convert_lines<N, true><<<grid, Cfg::THREADS, Cfg::SMEM, ctx->st>>>(o, in, nullptr, e0, e1, ctx->s.gamma,
+                                                                         &ctx->d_step->lam_out_bits);
+  else
+    k_convert_lines<N><<<grid, Cfg::THREADS, Cfg::SMEM, ctx->st>>>(o, in, out, e0, e1);
+  ++ctx->launches;
+  CK(cudaGetLastError());
+  return NSFR_OK;
+}
+
+// adaptive_dt's lambda_max of chi^3 u_hat over [e0, e1) (u_hat on the device,
+// e.g. a state on its way to the host) into d_step->lam_out_bits
+int lam_of_uhat(nsfr_gpu_ctx* ctx, const double* uhat, int e0, int e1) {
+  if (e1 <= e0) return NSFR_OK;
+  switch (ctx->NQ == ctx->N ? ctx->N : 0) {
+    case 3: return launch_convert_lines<3>(ctx, uhat, nullptr, true, e0, e1, true);
+    case 4: return launch_convert_lines<4>(ctx, uhat, nullptr, true, e0, e1, true);
+    case 5: return launch_convert_lines<5>(ctx, uhat, nullptr, true, e0, e1, true);
+    case 6: return launch_convert_lines<6>(ctx, uhat, nullptr, true, e0, e1, true);
+    case 7: return launch_convert_lines<7>(ctx, uhat, nullptr, true, e0, e1, true);
+  }
+  ctx->msg = "adaptive dt of the output: overintegrated DG is not supported";
+  return NSFR_E_DIM;
+}
+
+// u_hat <-> u_q of elements [e0, e1): to_quad applies chi^3, else Pi^3
+// (line-pass kernel for n_q = n_p; the generic k_convert for overintegrated DG)
 int convert_range(nsfr_gpu_ctx* ctx, const double* in, double* out, bool to_quad, int e0, int e1) {
+  if (e1 <= e0) return NSFR_OK;
+  if (ctx->NQ == ctx->N) {
+    switch (ctx->N) {
+      case 3: return launch_convert_lines<3>(ctx, in, out, to_quad, e0, e1, false);
+      case 4: return launch_convert_lines<4>(ctx, in, out, to_quad, e0, e1, false);
+      case 5: return launch_convert_lines<5>(ctx, in, out, to_quad, e0, e1, false);
+      case 6: return launch_convert_lines<6>(ctx, in, out, to_quad, e0, e1, false);
+      case 7: return launch_convert_lines<7>(ctx, in, out, to_quad, e0, e1, false);
+    }
+  }
   const size_t smem = sizeof(double) * 4 * std::max(nsol(ctx), nquad(ctx));
   const size_t in_per = NS * (to_quad ? nsol(ctx) : nquad(ctx)), out_per = NS * (to_quad ? nquad(ctx) : nsol(ctx));
   k_convert<<<e1 - e0, 128, smem, ctx->st>>>(ctx->d_tab, in + e0 * in_per, out + e0 * out_per, e1 - e0,
@@ -736,7 +804,8 @@ int nsfr_gpu_create(const nsfr_gpu_setup* setup, nsfr_gpu_ctx** out) {
     return fail(NSFR_E_CUDA);
   }
   if (cudaStreamCreateWithFlags(&ctx->st, cudaStreamNonBlocking) != cudaSuccess ||
-      cudaStreamCreateWithFlags(&ctx->st_copy, cudaStreamNonBlocking) != cudaSuccess) {
+      cudaStreamCreateWithFlags(&ctx->st_copy, cudaStreamNonBlocking) != cudaSuccess ||
+      cudaStreamCreateWithFlags(&ctx->st_d2h, cudaStreamNonBlocking) != cudaSuccess) {
     ctx->msg = "cudaStreamCreate failed (no CUDA device?)";
     return fail(NSFR_E_CUDA);
   }
@@ -863,6 +932,7 @@ int nsfr_gpu_destroy(nsfr_gpu_ctx* ctx) {
   if (ctx->h_err) cudaFreeHost(ctx->h_err);
   for (auto e : ctx->chunk_ev) cudaEventDestroy(e);
   if (ctx->st_copy) cudaStreamDestroy(ctx->st_copy);
+  if (ctx->st_d2h) cudaStreamDestroy(ctx->st_d2h);
   if (ctx->st) cudaStreamDestroy(ctx->st);
   delete ctx;
   return NSFR_OK;
@@ -1103,6 +1173,161 @@ int nsfr_gpu_advance(nsfr_gpu_ctx* ctx, int nsteps, double cfl, double t_final, 
   if (int rc = sync_check(ctx)) return rc;
   if (t_out) *t_out = ctx->h_step->t;
   return NSFR_OK;
+}
+
+// ---- streamed host step (rk4 step on host buffers, copies overlapped) --------
+// set_state(u_in); rk4 step; get_state(u_out) as ONE pipeline over contiguous
+// element chunks (>= one z-plane each, so a chunk's face neighbours lie in the
+// cyclically adjacent chunks). Per chunk the work is 9 layers: L0 = upload +
+// chi^3 + K1, L(2s-1) = K2 of stage s, L(2s) = K3 of stage s (s = 1..4), then
+// Pi^3 + download. Layer L of chunk c needs layer L-1 of c-1, c, c+1 (K2 reads
+// the neighbours' traces; K3 overwrites them, so it also waits for the
+// neighbours' K2). Chunks are visited outward from chunk 0 in cyclic distance
+// r, layer L at wave r + L: every dependency was enqueued earlier on the one
+// compute stream, the uploads run ahead on st_copy and the downloads trail on
+// st_d2h, both directions of the PCIe link busy while the SMs compute. The
+// upload lands in (and the download leaves from) the chunk's RK accumulator,
+// dead outside stages 1-4 of that chunk. Adaptive dt needs lambda_max of the
+// whole state before any K3: layers 0-1 form the first sweep, then dt, then
+// layers 2-8 a second sweep.
+namespace {
+
+int streamed_chunks(const nsfr_gpu_ctx* ctx, std::vector<int>& bounds) {
+  const long long plane = static_cast<long long>(ctx->m) * ctx->m;
+  const long long min_sz = plane + 8;  // >= one plane after rounding down to 8
+  const char* env = std::getenv("NSFR_STREAM_CHUNKS");
+  const long long cap = env ? std::max(1, std::atoi(env)) : 128;
+  int nch = static_cast<int>(std::min<long long>(cap, ctx->E / min_sz));
+  nch = std::max(nch, 1);
+  bounds.resize(nch + 1);
+  for (int c = 0; c <= nch; ++c)
+    bounds[c] = c == nch ? ctx->E : static_cast<int>((static_cast<long long>(ctx->E) * c / nch) & ~7LL);
+  return nch;
+}
+
+}  // namespace
+
+// dt_next (adaptive_dt of u_out): from the chunks' u_hat as they leave
+int finish_dt_next(nsfr_gpu_ctx* ctx, double* dt_next) {
+  if (ctx->comm)
+    NK(ncclAllReduce(&ctx->d_step->lam_out_bits, &ctx->d_step->lam_out_bits, 1, ncclUint64, ncclMax,
+                     ctx->comm, ctx->st));
+  k_step_next<<<1, 1, 0, ctx->st>>>(ctx->d_step);
+  ++ctx->launches;
+  CK(cudaGetLastError());
+  if (int rc = sync_check(ctx)) return rc;
+  *dt_next = ctx->h_step->dt_next;
+  return NSFR_OK;
+}
+
+int nsfr_gpu_rk4_step_host(nsfr_gpu_ctx* ctx, const double* u_in, double* u_out, double dt,
+                           double cfl, double t_final, double* dt_used, double* dt_next) {
+  const bool fixed = dt > 0.0;
+  const bool streamable = !ctx->dg && ctx->nranks == 1 && !ctx->comm && !ctx->d_halo_lo;
+  if (!streamable) {  // slabs / DG: the same GPU path, transfers not overlapped
+    if (int rc = nsfr_gpu_set_state(ctx, u_in)) return rc;
+    double used = dt;
+    if (fixed) {
+      if (dt_next)  // cfl / t_final of the adaptive_dt that follows
+        if (int rc = set_step_params(ctx, cfl, t_final)) return rc;
+      if (int rc = nsfr_gpu_rk4_step_dt(ctx, dt)) return rc;
+    } else if (int rc = nsfr_gpu_rk4_step(ctx, cfl, t_final, &used)) {
+      return rc;
+    }
+    if (dt_used) *dt_used = used;
+    if (int rc = nsfr_gpu_get_state(ctx, u_out)) return rc;
+    if (!dt_next) return NSFR_OK;
+    // get_state left u_hat of the whole slab in d_vol (NSFR); DG carries u_hat
+    CK(cudaMemsetAsync(&ctx->d_step->lam_out_bits, 0, sizeof(unsigned long long), ctx->st));
+    if (int rc = lam_of_uhat(ctx, ctx->dg ? ctx->d_un : ctx->d_vol, 0, ctx->E)) return rc;
+    return finish_dt_next(ctx, dt_next);
+  }
+  std::vector<int> b;
+  const int nch = streamed_chunks(ctx, b);
+  if (int rc = ensure_chunk_events(ctx, 2 * nch)) return rc;
+  if (!fixed || dt_next)
+    if (int rc = set_step_params(ctx, cfl, t_final)) return rc;
+  if (fixed) CK(cudaMemcpyAsync(&ctx->d_step->dt, &dt, sizeof dt, cudaMemcpyHostToDevice, ctx->st));
+  CK(cudaStreamSynchronize(ctx->st));  // device buffers free, step parameters in place
+  ctx->proj_valid = false;
+  k_step_begin<<<1, 1, 0, ctx->st>>>(ctx->d_step);  // clears lambda
+  ++ctx->launches;
+  const size_t per = nsol(ctx) * NS;
+  const bool nocopy = std::getenv("NSFR_STREAM_NOCOPY") != nullptr;  // probe: the compute schedule alone
+  const int D = nch / 2;  // largest cyclic distance from chunk 0
+  auto at_dist = [&](int r, int* cs) {
+    if (r == 0) { cs[0] = 0; return 1; }
+    cs[0] = r;
+    if (nch - r == r) return 1;
+    cs[1] = nch - r;
+    return 2;
+  };
+  // uploads, in the order the sweep consumes them
+  for (int r = 0; r <= D; ++r) {
+    int cs[2];
+    const int k = at_dist(r, cs);
+    for (int i = 0; i < k; ++i) {
+      const int c = cs[i], e0 = b[c], e1 = b[c + 1];
+      if (!nocopy)
+        CK(cudaMemcpyAsync(ctx->d_acc + e0 * per, u_in + e0 * per, sizeof(double) * per * (e1 - e0),
+                           cudaMemcpyHostToDevice, ctx->st_copy));
+      CK(cudaEventRecord(ctx->chunk_ev[c], ctx->st_copy));
+    }
+  }
+  auto layer = [&](int L, int c) -> int {
+    const int e0 = b[c], e1 = b[c + 1];
+    if (L == 0) {
+      CK(cudaStreamWaitEvent(ctx->st, ctx->chunk_ev[c], 0));
+      if (nocopy) {  // same conversion cost, the device state stays the input
+        if (int rc = convert_range(ctx, ctx->d_un, ctx->d_rhs, true, e0, e1)) return rc;
+      } else if (int rc = convert_range(ctx, ctx->d_acc, ctx->d_un, true, e0, e1)) {
+        return rc;
+      }
+      return project(ctx, ctx->d_un, !fixed, e0, e1);
+    }
+    const int stage = (L + 1) / 2;
+    if (L & 1) return residual(ctx, 0, e0, e1);
+    if (int rc = update(ctx, stage, false, nullptr, e0, e1)) return rc;
+    if (stage < 4) return NSFR_OK;
+    // u_{n+1} of this chunk is final: Pi^3 into the dead accumulator, download
+    if (int rc = convert_range(ctx, ctx->d_un, ctx->d_acc, false, e0, e1)) return rc;
+    CK(cudaEventRecord(ctx->chunk_ev[nch + c], ctx->st));
+    CK(cudaStreamWaitEvent(ctx->st_d2h, ctx->chunk_ev[nch + c], 0));
+    if (!nocopy)
+      CK(cudaMemcpyAsync(u_out + e0 * per, ctx->d_acc + e0 * per, sizeof(double) * per * (e1 - e0),
+                       cudaMemcpyDeviceToHost, ctx->st_d2h));
+    // adaptive_dt of what goes back, while it goes (reads the same buffer)
+    return dt_next ? lam_of_uhat(ctx, ctx->d_acc, e0, e1) : NSFR_OK;
+  };
+  auto sweep = [&](int La, int Lb) -> int {
+    for (int w = 0; w <= D + (Lb - La); ++w)
+      for (int L = La; L <= Lb; ++L) {
+        const int r = w - (L - La);
+        if (r < 0 || r > D) continue;
+        int cs[2];
+        const int k = at_dist(r, cs);
+        for (int i = 0; i < k; ++i)
+          if (int rc = layer(L, cs[i])) return rc;
+      }
+    return NSFR_OK;
+  };
+  if (fixed) {
+    if (int rc = sweep(0, 8)) return rc;
+  } else {
+    if (int rc = sweep(0, 1)) return rc;
+    k_step_dt<<<1, 1, 0, ctx->st>>>(ctx->d_step);  // reads and clears lambda
+    ++ctx->launches;
+    if (int rc = sweep(2, 8)) return rc;
+  }
+  k_step_end<<<1, 1, 0, ctx->st>>>(ctx->d_step);
+  ++ctx->launches;
+  CK(cudaGetLastError());
+  CK(cudaStreamSynchronize(ctx->st_d2h));
+  CK(cudaStreamSynchronize(ctx->st_copy));
+  if (int rc = sync_check(ctx)) return rc;
+  ctx->proj_valid = true;  // K3 of stage 4 left the projection (and lambda) of u_{n+1}
+  if (dt_used) *dt_used = ctx->h_step->dt;
+  return dt_next ? finish_dt_next(ctx, dt_next) : NSFR_OK;
 }
 
 int nsfr_gpu_l2_error(nsfr_gpu_ctx* ctx, int kind, double out2[2]) {

@@ -473,12 +473,18 @@ struct StepState {
   double t, dt, t_final, cfl, dx;
   unsigned long long lam_bits;
   int active;
+  unsigned long long lam_out_bits;  // streamed step: lambda_max of the state handed back
+  double dt_next;                   // adaptive_dt of that state
 };
 
-__global__ void k_step_begin(StepState* S) { S->lam_bits = 0ull; }
+__global__ void k_step_begin(StepState* S) {
+  S->lam_bits = 0ull;
+  S->lam_out_bits = 0ull;
+}
 
-__global__ void k_step_dt(StepState* S) {
-  const double lam = __longlong_as_double(static_cast<long long>(S->lam_bits));
+// adaptive_dt: cfl dx / lambda_max, clipped to t_final - t
+__device__ __forceinline__ double step_dt_of(const StepState* S, unsigned long long bits) {
+  const double lam = __longlong_as_double(static_cast<long long>(bits));
   double dt = lam > 0.0 ? S->cfl * S->dx / lam : S->cfl * S->dx;
   if (S->t_final > 0.0) {
     if (S->t >= S->t_final)
@@ -486,10 +492,17 @@ __global__ void k_step_dt(StepState* S) {
     else
       dt = fmin(dt, S->t_final - S->t);
   }
-  S->dt = dt;
+  return dt;
+}
+
+__global__ void k_step_dt(StepState* S) {
+  S->dt = step_dt_of(S, S->lam_bits);
   S->lam_bits = 0ull;  // K3 of the last stage accumulates the next step's lambda
 }
 
 __global__ void k_step_end(StepState* S) { S->t += S->dt; }
+
+// after k_step_end: the dt the next step would take from the output state
+__global__ void k_step_next(StepState* S) { S->dt_next = step_dt_of(S, S->lam_out_bits); }
 
 }  // namespace nsfr_b200

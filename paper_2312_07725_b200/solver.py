@@ -125,6 +125,7 @@ def load_library() -> C.CDLL:
         "nsfr_gpu_rk4_step": (C.c_int, [V, C.c_double, C.c_double, P]),
         "nsfr_gpu_advance": (C.c_int, [V, C.c_int, C.c_double, C.c_double, P]),
         "nsfr_gpu_rk4_step_dt": (C.c_int, [V, C.c_double]),
+        "nsfr_gpu_rk4_step_host": (C.c_int, [V, P, P, C.c_double, C.c_double, C.c_double, P, P]),
         "nsfr_gpu_max_wavespeed": (C.c_int, [V, P]),
         "nsfr_gpu_l2_error": (C.c_int, [V, C.c_int, P]),
         "nsfr_gpu_entropy_change": (C.c_int, [V, P]),
@@ -382,6 +383,22 @@ class GpuSolver:
 
     def rk4_step_dt(self, dt: float):
         self._check(self.lib.nsfr_gpu_rk4_step_dt(self.ctx, dt))
+
+    def rk4_step_host(self, u_in: np.ndarray, u_out: np.ndarray | None = None, dt: float = 0.0,
+                      cfl: float = 0.1, t_final: float = 0.0) -> tuple[np.ndarray, float, float]:
+        """rk4_step(field, dt) on host state: upload u_in, one RK4
+        step (dt if dt > 0, else adaptive_dt(u_in, cfl) clipped to t_final),
+        download into u_out (may be u_in; pinned buffers let the copies overlap
+        the compute). Returns (u_out, dt used, adaptive_dt(u_out, cfl) clipped to
+        t_final): feeding the last back as dt is the reference's
+        `dt = adaptive_dt(u); u = rk4_step(u, dt)` loop without a barrier."""
+        for a in (u_in,) + ((u_out,) if u_out is not None else ()):
+            assert a.shape == self.state_shape and a.dtype == np.float64 and a.flags.c_contiguous
+        out = np.zeros(self.state_shape) if u_out is None else u_out
+        used, nxt = np.zeros(1), np.zeros(1)
+        self._check(self.lib.nsfr_gpu_rk4_step_host(self.ctx, _ptr(u_in), _ptr(out), dt, cfl, t_final,
+                                                    _ptr(used), _ptr(nxt)))
+        return out, float(used[0]), float(nxt[0])
 
     def advance(self, nsteps: int, cfl: float = 0.1, t_final: float = 0.0) -> float:
         t = np.zeros(1)
