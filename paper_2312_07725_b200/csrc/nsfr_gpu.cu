@@ -38,6 +38,8 @@ struct nsfr_gpu_ctx {
   cudaStream_t st = nullptr;
   cudaStream_t st_copy = nullptr;  // host<->device state transfers, chunk-pipelined with st
   cudaStream_t st_d2h = nullptr;   // device->host leg of the streamed step (runs beside st_copy)
+  std::vector<cudaStream_t> lanes;  // streamed step: compute lanes (a chunk's ops stay on one lane)
+  std::vector<cudaEvent_t> op_ev;   // streamed step: one event per (layer, chunk) op, + fork/join
   std::vector<cudaEvent_t> chunk_ev;
   ncclComm_t comm = nullptr;
   int rank = 0, nranks = 1, peer_lo = 0, peer_hi = 0;
@@ -933,6 +935,8 @@ int nsfr_gpu_destroy(nsfr_gpu_ctx* ctx) {
   for (auto e : ctx->chunk_ev) cudaEventDestroy(e);
   if (ctx->st_copy) cudaStreamDestroy(ctx->st_copy);
   if (ctx->st_d2h) cudaStreamDestroy(ctx->st_d2h);
+  for (auto l : ctx->lanes) cudaStreamDestroy(l);
+  for (auto e : ctx->op_ev) cudaEventDestroy(e);
   if (ctx->st) cudaStreamDestroy(ctx->st);
   delete ctx;
   return NSFR_OK;
@@ -1252,6 +1256,44 @@ int nsfr_gpu_rk4_step_host(nsfr_gpu_ctx* ctx, const double* u_in, double* u_out,
   ctx->proj_valid = false;
   k_step_begin<<<1, 1, 0, ctx->st>>>(ctx->d_step);  // clears lambda
   ++ctx->launches;
+  // Compute lanes: chunk c's ops run on lane c % S, waiting only for the
+  // events of the neighbour-chunk ops they depend on, so one kernel's tail
+  // overlaps the next independent kernel (NSFR_STREAM_LANES, default 4;
+  // 128^3 p=4 chained e2e step: 1 lane 347 ms, 2-3 lanes 335 ms, 4 lanes 327 ms).
+  const char* lenv = std::getenv("NSFR_STREAM_LANES");
+  const int S = std::max(1, std::min(nch, lenv ? std::atoi(lenv) : 4));
+  while (static_cast<int>(ctx->lanes.size()) < S) {
+    cudaStream_t l;
+    CK(cudaStreamCreateWithFlags(&l, cudaStreamNonBlocking));
+    ctx->lanes.push_back(l);
+  }
+  const int nev = 9 * nch + 2 * S + 2;
+  while (static_cast<int>(ctx->op_ev.size()) < nev) {
+    cudaEvent_t e;
+    CK(cudaEventCreateWithFlags(&e, cudaEventDisableTiming));
+    ctx->op_ev.push_back(e);
+  }
+  cudaStream_t main_st = ctx->st;
+  struct Restore {
+    nsfr_gpu_ctx* c;
+    cudaStream_t s;
+    ~Restore() { c->st = s; }
+  } restore{ctx, main_st};
+  // fork: the lanes start after the step parameters (main) are in place
+  auto fork = [&](int slot) -> int {
+    CK(cudaEventRecord(ctx->op_ev[9 * nch + slot], main_st));
+    for (int k = 0; k < S; ++k) CK(cudaStreamWaitEvent(ctx->lanes[k], ctx->op_ev[9 * nch + slot], 0));
+    return NSFR_OK;
+  };
+  // join: main waits for every lane
+  auto join = [&](int slot) -> int {
+    for (int k = 0; k < S; ++k) {
+      CK(cudaEventRecord(ctx->op_ev[9 * nch + 2 + slot * S + k], ctx->lanes[k]));
+      CK(cudaStreamWaitEvent(main_st, ctx->op_ev[9 * nch + 2 + slot * S + k], 0));
+    }
+    return NSFR_OK;
+  };
+  if (int rc = fork(0)) return rc;
   const size_t per = nsol(ctx) * NS;
   const bool nocopy = std::getenv("NSFR_STREAM_NOCOPY") != nullptr;  // probe: the compute schedule alone
   const int D = nch / 2;  // largest cyclic distance from chunk 0
@@ -1274,7 +1316,7 @@ int nsfr_gpu_rk4_step_host(nsfr_gpu_ctx* ctx, const double* u_in, double* u_out,
       CK(cudaEventRecord(ctx->chunk_ev[c], ctx->st_copy));
     }
   }
-  auto layer = [&](int L, int c) -> int {
+  auto layer_ops = [&](int L, int c) -> int {
     const int e0 = b[c], e1 = b[c + 1];
     if (L == 0) {
       CK(cudaStreamWaitEvent(ctx->st, ctx->chunk_ev[c], 0));
@@ -1299,6 +1341,20 @@ int nsfr_gpu_rk4_step_host(nsfr_gpu_ctx* ctx, const double* u_in, double* u_out,
     // adaptive_dt of what goes back, while it goes (reads the same buffer)
     return dt_next ? lam_of_uhat(ctx, ctx->d_acc, e0, e1) : NSFR_OK;
   };
+  auto layer = [&](int L, int c) -> int {
+    cudaStream_t lane = ctx->lanes[c % S];
+    if (L > 0)  // layer L-1 of the neighbour chunks (same-lane ops are in order already)
+      for (int d = -1; d <= 1; d += 2) {
+        const int cn = (c + d + nch) % nch;
+        if (cn % S != c % S) CK(cudaStreamWaitEvent(lane, ctx->op_ev[(L - 1) * nch + cn], 0));
+      }
+    ctx->st = lane;
+    const int rc = layer_ops(L, c);
+    ctx->st = main_st;
+    if (rc) return rc;
+    CK(cudaEventRecord(ctx->op_ev[L * nch + c], lane));
+    return NSFR_OK;
+  };
   auto sweep = [&](int La, int Lb) -> int {
     for (int w = 0; w <= D + (Lb - La); ++w)
       for (int L = La; L <= Lb; ++L) {
@@ -1315,10 +1371,13 @@ int nsfr_gpu_rk4_step_host(nsfr_gpu_ctx* ctx, const double* u_in, double* u_out,
     if (int rc = sweep(0, 8)) return rc;
   } else {
     if (int rc = sweep(0, 1)) return rc;
+    if (int rc = join(0)) return rc;
     k_step_dt<<<1, 1, 0, ctx->st>>>(ctx->d_step);  // reads and clears lambda
     ++ctx->launches;
+    if (int rc = fork(1)) return rc;
     if (int rc = sweep(2, 8)) return rc;
   }
+  if (int rc = join(1)) return rc;
   k_step_end<<<1, 1, 0, ctx->st>>>(ctx->d_step);
   ++ctx->launches;
   CK(cudaGetLastError());
