@@ -38,6 +38,7 @@ class GpuSolver {
     s.tables = &t; s.jac_vol = jac_.data(); s.cof_vol = cof_.data();
     s.nranks = 1;
     check(nsfr_gpu_create(&s, &ctx_));
+    dx_ = (s.x_right - s.x_left) / (s.m * (s.p + 1));
   }
   ~GpuSolver() { nsfr_gpu_destroy(ctx_); }
 
@@ -48,12 +49,23 @@ class GpuSolver {
     check(nsfr_gpu_rhs(ctx_, dudt.data(), &ds));
     return ds;
   }
-  double rk4_step(std::span<double> u, double cfl, double t_final) {
-    double dt = 0.0;
+  // rk4_step(field, dt) on the caller's host field: upload,
+  // step and download pipelined on the device. Returns adaptive_dt(u, cfl)
+  // of the new field, so the reference loop
+  //   dt = adaptive_dt(u, cfl); while (...) dt = rk4_step(u, dt, cfl, t_final);
+  // runs without a global reduction inside the step. dt <= 0: take
+  // adaptive_dt of the incoming field first.
+  double rk4_step(std::span<double> u, double dt, double cfl, double t_final = 0.0) {
+    double used = 0.0, next = 0.0;
+    check(nsfr_gpu_rk4_step_host(ctx_, u.data(), u.data(), dt, cfl, t_final, &used, &next));
+    return next;
+  }
+  // adaptive_dt(field, cfl) of a host field
+  double adaptive_dt(std::span<const double> u, double cfl) {
+    double lam = 0.0;
     check(nsfr_gpu_set_state(ctx_, u.data()));
-    check(nsfr_gpu_rk4_step(ctx_, cfl, t_final, &dt));
-    check(nsfr_gpu_get_state(ctx_, u.data()));
-    return dt;
+    check(nsfr_gpu_max_wavespeed(ctx_, &lam));
+    return lam > 0.0 ? cfl * dx_ / lam : cfl * dx_;
   }
   std::array<double, 2> l2_error(int case_kind) {
     std::array<double, 2> e{};
@@ -75,6 +87,7 @@ class GpuSolver {
     }
   }
   nsfr_gpu_ctx* ctx_ = nullptr;
+  double dx_ = 0.0;  // l/(M(p+1))
   std::vector<double> jac_, cof_;
 };
 
