@@ -198,15 +198,17 @@ __device__ __forceinline__ void proj_core(const ProjParams& P, const ProjOps<N>&
     double* dst = P.traces + ((size_t)e * 6 + f) * 5 * N2 + k;
 #pragma unroll
     for (int s = 0; s < NS; ++s) dst[s * N2] = uu[s];
-    // boundary planes also go to the halo send buffers
-    const int mm = P.m * P.m, kl = e / mm, plane = e - kl * mm;
-    if (P.send_lo && f == 4 && kl == 0) {
+    // boundary planes also go to the halo send buffers (z faces of slab contexts only)
+    if ((P.send_lo && f == 4) || (P.send_hi && f == 5)) {
+      const int mm = P.m * P.m, kl = e / mm, plane = e - kl * mm;
+      if (f == 4 && kl == 0) {
 #pragma unroll
-      for (int s = 0; s < NS; ++s) P.send_lo[((size_t)plane * 5 + s) * N2 + k] = uu[s];
-    }
-    if (P.send_hi && f == 5 && kl == P.nz - 1) {
+        for (int s = 0; s < NS; ++s) P.send_lo[((size_t)plane * 5 + s) * N2 + k] = uu[s];
+      }
+      if (f == 5 && kl == P.nz - 1) {
 #pragma unroll
-      for (int s = 0; s < NS; ++s) P.send_hi[((size_t)plane * 5 + s) * N2 + k] = uu[s];
+        for (int s = 0; s < NS; ++s) P.send_hi[((size_t)plane * 5 + s) * N2 + k] = uu[s];
+      }
     }
   }
   PHASE_MARK(13);

@@ -275,6 +275,7 @@ __device__ __forceinline__ void upd_batch(const UpdParams& P, const UpdOps<N>& O
     for (int a = 0; a < N; ++a) x[a] = src[a * N2];
     const size_t gb = (size_t)e0 * VS + (size_t)bsi * N3 + l;
     double* nxt = R0 + bsi * N3 + l;
+    double kv[N];
 #pragma unroll
     for (int c = 0; c < N; ++c) {
       double z = 0.0;
@@ -284,29 +285,38 @@ __device__ __forceinline__ void upd_batch(const UpdParams& P, const UpdOps<N>& O
 #pragma unroll
         for (int a = 0; a < N; ++a) z = fma(T.fr[c * N + a], x[a], z);
       }
-      const double kv = -z;
-      const size_t gi = gb + c * N2;
-      switch (P.stage) {
-        case 0: P.out[gi] = kv; break;
-        case 1:
-          P.acc[gi] = kv;
-          nxt[c * N2] = fma(hdt, kv, pre_un[j][c]);
-          break;
-        case 2:
-          P.acc[gi] = fma(2.0, kv, pre_acc[j][c]);
-          nxt[c * N2] = fma(hdt, kv, pre_un[j][c]);
-          break;
-        case 3:
-          P.acc[gi] = fma(2.0, kv, pre_acc[j][c]);
-          nxt[c * N2] = fma(dt, kv, pre_un[j][c]);
-          break;
-        default: {
-          const double a4 = pre_acc[j][c] + kv;
-          const double u1 = fma(sdt, a4, pre_un[j][c]);
-          P.un[gi] = u1;
+      kv[c] = -z;
+    }
+    // one (warp-uniform) stage dispatch per line, not per node
+    switch (P.stage) {
+      case 0:
+#pragma unroll
+        for (int c = 0; c < N; ++c) P.out[gb + c * N2] = kv[c];
+        break;
+      case 1:
+#pragma unroll
+        for (int c = 0; c < N; ++c) {
+          P.acc[gb + c * N2] = kv[c];
+          nxt[c * N2] = fma(hdt, kv[c], pre_un[j][c]);
+        }
+        break;
+      case 2:
+      case 3: {
+        const double cdt = P.stage == 2 ? hdt : dt;
+#pragma unroll
+        for (int c = 0; c < N; ++c) {
+          P.acc[gb + c * N2] = fma(2.0, kv[c], pre_acc[j][c]);
+          nxt[c * N2] = fma(cdt, kv[c], pre_un[j][c]);
+        }
+        break;
+      }
+      default:
+#pragma unroll
+        for (int c = 0; c < N; ++c) {
+          const double u1 = fma(sdt, pre_acc[j][c] + kv[c], pre_un[j][c]);
+          P.un[gb + c * N2] = u1;
           nxt[c * N2] = u1;
         }
-      }
     }
   }
   if (P.stage == 0) return;
