@@ -202,8 +202,7 @@ __global__ void __launch_bounds__(256) k_dg_states(DgStateParams P, DgOps<NP, NQ
         atomicOr(P.err, ERR_STATE);
         continue;
       }
-      const double vx = uu[1] / uu[0], vy = uu[2] / uu[0], vz = uu[3] / uu[0];
-      lam = fmax(lam, sqrt(vx * vx + vy * vy + vz * vz) + sqrt(g * d_pressure(g, uu) / uu[0]));
+      lam = fmax(lam, d_node_wavespeed(g, uu));
     }
     for (int o = 16; o > 0; o >>= 1) lam = fmax(lam, __shfl_xor_sync(0xffffffffu, lam, o));
     if ((tid & 31) == 0 && lam > 0.0) atomicMax(P.lam, dbl_bits(lam));
