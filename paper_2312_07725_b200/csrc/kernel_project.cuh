@@ -142,17 +142,20 @@ __device__ __forceinline__ void proj_core(const ProjParams& P, const ProjOps<N>&
     double uu[NS], vv[NS];
 #pragma unroll
     for (int s = 0; s < NS; ++s) uu[s] = A[(b * 5 + s) * N3 + q];
-    if (!d_entropy_vars(g, uu, vv)) {
+    // primitives once (1/rho, 1/p): the entropy variables and K2's bundle share them
+    const PrimX px = d_primx(g, uu);
+    if (!d_admissible(g, uu)) {
       atomicOr(P.err, ERR_STATE);
 #pragma unroll
       for (int s = 0; s < NS; ++s) vv[s] = (s == 4) ? -1.0 : 0.0;
-    } else if (P.lam) {
-      lam = fmax(lam, d_node_wavespeed(g, uu));
+    } else {
+      d_entropy_vars_x(g, uu, px, vv);
+      if (P.lam) lam = fmax(lam, d_node_wavespeed(g, uu));
     }
 #pragma unroll
     for (int s = 0; s < NS; ++s) V[(b * 5 + s) * N3 + q] = vv[s];
     // half-scaled primitive bundle for K2's pair fluxes (prim(), euler.cpp:109-115)
-    const PrimH ph = to_half(g - 1.0, d_primx(g, uu));
+    const PrimH ph = to_half(g - 1.0, px);
     double* dst = P.ut_vol + (size_t)(e0 + b) * 6 * N3 + q;
     dst[0 * N3] = ph.hr;
     dst[1 * N3] = ph.hu;
