@@ -1227,8 +1227,11 @@ int finish_dt_next(nsfr_gpu_ctx* ctx, double* dt_next) {
 int nsfr_gpu_rk4_step_host(nsfr_gpu_ctx* ctx, const double* u_in, double* u_out, double dt,
                            double cfl, double t_final, double* dt_used, double* dt_next) {
   const bool fixed = dt > 0.0;
-  const bool streamable = !ctx->dg && ctx->nranks == 1 && !ctx->comm && !ctx->d_halo_lo;
-  if (!streamable) {  // slabs / DG: the same GPU path, transfers not overlapped
+  // seg: a z-slab (or a 1-rank NCCL loopback) whose end planes take NCCL halos
+  // instead of wrapping locally; external-halo contexts and DG do not stream
+  const bool seg = ctx->d_halo_lo != nullptr;
+  const bool streamable = !ctx->dg && (seg ? ctx->comm != nullptr : ctx->nranks == 1);
+  if (!streamable) {  // external halos / DG: the same GPU path, transfers not overlapped
     if (int rc = nsfr_gpu_set_state(ctx, u_in)) return rc;
     double used = dt;
     if (fixed) {
@@ -1267,7 +1270,7 @@ int nsfr_gpu_rk4_step_host(nsfr_gpu_ctx* ctx, const double* u_in, double* u_out,
     CK(cudaStreamCreateWithFlags(&l, cudaStreamNonBlocking));
     ctx->lanes.push_back(l);
   }
-  const int nev = 9 * nch + 2 * S + 2;
+  const int nev = 9 * nch + 2 * S + 2 + 5;
   while (static_cast<int>(ctx->op_ev.size()) < nev) {
     cudaEvent_t e;
     CK(cudaEventCreateWithFlags(&e, cudaEventDisableTiming));
@@ -1296,14 +1299,34 @@ int nsfr_gpu_rk4_step_host(nsfr_gpu_ctx* ctx, const double* u_in, double* u_out,
   if (int rc = fork(0)) return rc;
   const size_t per = nsol(ctx) * NS;
   const bool nocopy = std::getenv("NSFR_STREAM_NOCOPY") != nullptr;  // probe: the compute schedule alone
-  const int D = nch / 2;  // largest cyclic distance from chunk 0
+  // Periodic box: chunks visited outward from chunk 0 in cyclic distance.
+  // Slab: a segment whose two end chunks take halo planes, visited outward
+  // from its middle chunk c0; before K2 of stage s reaches an end chunk, the
+  // stage's grouped send/recv runs on the main stream once both end chunks
+  // have projected (their K1 / K3 pack the send planes).
+  const int c0 = seg ? nch / 2 : 0;
+  const int D = seg ? std::max(c0, nch - 1 - c0) : nch / 2;
   auto at_dist = [&](int r, int* cs) {
+    if (seg) {
+      int k = 0;
+      if (c0 - r >= 0) cs[k++] = c0 - r;
+      if (r > 0 && c0 + r < nch) cs[k++] = c0 + r;
+      return k;
+    }
     if (r == 0) { cs[0] = 0; return 1; }
     cs[0] = r;
     if (nch - r == r) return 1;
     cs[1] = nch - r;
     return 2;
   };
+  auto nbr = [&](int c, int d) {  // -1: a slab end (its neighbour is the halo)
+    const int cn = c + d;
+    if (seg) return (cn < 0 || cn >= nch) ? -1 : cn;
+    return (cn + nch) % nch;
+  };
+  std::vector<char> done(9 * nch, 0);
+  bool exchanged[5] = {false, false, false, false, false};
+  const int ex_ev0 = 9 * nch + 2 * S + 2;
   // uploads, in the order the sweep consumes them
   for (int r = 0; r <= D; ++r) {
     int cs[2];
@@ -1345,14 +1368,35 @@ int nsfr_gpu_rk4_step_host(nsfr_gpu_ctx* ctx, const double* u_in, double* u_out,
     cudaStream_t lane = ctx->lanes[c % S];
     if (L > 0)  // layer L-1 of the neighbour chunks (same-lane ops are in order already)
       for (int d = -1; d <= 1; d += 2) {
-        const int cn = (c + d + nch) % nch;
-        if (cn % S != c % S) CK(cudaStreamWaitEvent(lane, ctx->op_ev[(L - 1) * nch + cn], 0));
+        const int cn = nbr(c, d);
+        if (cn < 0 || cn % S == c % S) continue;
+        if (!done[(L - 1) * nch + cn]) {
+          ctx->msg = "streamed step: schedule out of order";
+          return NSFR_E_DIM;
+        }
+        CK(cudaStreamWaitEvent(lane, ctx->op_ev[(L - 1) * nch + cn], 0));
       }
+    if (seg && (L & 1) && (c == 0 || c == nch - 1)) {  // K2 of stage s at a slab end: halos first
+      const int st = (L + 1) / 2;
+      if (!exchanged[st]) {
+        if (!done[(L - 1) * nch] || !done[(L - 1) * nch + nch - 1]) {
+          ctx->msg = "streamed step: halo exchange before the end chunks projected";
+          return NSFR_E_DIM;
+        }
+        CK(cudaStreamWaitEvent(main_st, ctx->op_ev[(L - 1) * nch], 0));
+        CK(cudaStreamWaitEvent(main_st, ctx->op_ev[(L - 1) * nch + nch - 1], 0));
+        if (int rc = exchange(ctx)) return rc;  // on ctx->st == main_st
+        CK(cudaEventRecord(ctx->op_ev[ex_ev0 + st], main_st));
+        exchanged[st] = true;
+      }
+      CK(cudaStreamWaitEvent(lane, ctx->op_ev[ex_ev0 + st], 0));
+    }
     ctx->st = lane;
     const int rc = layer_ops(L, c);
     ctx->st = main_st;
     if (rc) return rc;
     CK(cudaEventRecord(ctx->op_ev[L * nch + c], lane));
+    done[L * nch + c] = 1;
     return NSFR_OK;
   };
   auto sweep = [&](int La, int Lb) -> int {
@@ -1372,6 +1416,9 @@ int nsfr_gpu_rk4_step_host(nsfr_gpu_ctx* ctx, const double* u_in, double* u_out,
   } else {
     if (int rc = sweep(0, 1)) return rc;
     if (int rc = join(0)) return rc;
+    if (ctx->comm)
+      NK(ncclAllReduce(&ctx->d_step->lam_bits, &ctx->d_step->lam_bits, 1, ncclUint64, ncclMax, ctx->comm,
+                       ctx->st));
     k_step_dt<<<1, 1, 0, ctx->st>>>(ctx->d_step);  // reads and clears lambda
     ++ctx->launches;
     if (int rc = fork(1)) return rc;

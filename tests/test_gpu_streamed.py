@@ -124,3 +124,30 @@ def test_dt_next_chain_equals_adaptive_steps(scheme, m):
         if dt == 0.0:
             break
     assert a.time == t_final
+
+
+@pytest.mark.parametrize("m,fixed", [(8, True), (8, False), (5, False)])
+def test_streamed_step_slab_with_nccl_halos(m, fixed):
+    """The slab form of the pipeline (end chunks fed by NCCL halo planes, one
+    grouped send/recv per stage once both end chunks projected) on a 1-rank
+    NCCL loopback communicator (its halo is the periodic wrap): bitwise the
+    periodic context's plain calls."""
+    pkg = P()
+    p = 4
+    cfg = pkg.SolverConfig(p=p, m=m, c1d=C_PLUS[p])
+    a = pkg.GpuSolver(cfg, nccl_id=pkg.nccl_unique_id())
+    b = pkg.GpuSolver(cfg)
+    a.init_case()
+    b.init_case()
+    u = perturbed(b, seed=3)
+    ub = u.copy()
+    dt = 0.1 * (10.0 / (m * (p + 1))) / 2.5 if fixed else 0.0
+    for _ in range(2):
+        _, used, nxt = a.rk4_step_host(u, u, dt=dt, cfl=0.1)
+        b.set_state(ub)
+        want = b.rk4_step_dt(dt) if fixed else b.rk4_step(0.1)
+        b.get_state(out=ub)
+        np.testing.assert_array_equal(u, ub)
+        assert a.time == b.time
+        if not fixed:
+            assert used == want
