@@ -148,29 +148,66 @@ __device__ __forceinline__ void res_prefetch(const ResParams& P, int e0, int tid
 // KM (kinetic-energy diagnostics; every two-point flux minus the pressure work):
 //   0 the residual; 1 volume rows only (S6); 2 all rows (S6-S8) without Roe.
 
+// Shared-memory carve-up of one batch: ACCV [EPB][3][5][N3] direction
+// accumulators, PRIM [EPB][6][N3] half-scaled primitives, COF [EPB][9][N3] 0.5 C.
+template <int N>
+struct ResSmem {
+  static constexpr int N3 = N * N * N, EPB = ResCfg<N>::EPB, AS = 15 * N3;
+  double *ACCV, *PRIM, *COF;
+  __device__ __forceinline__ explicit ResSmem(double* sm)
+      : ACCV(sm), PRIM(sm + EPB * AS), COF(sm + EPB * AS + EPB * 6 * N3) {}
+};
+
+// the staging blocks of batch e0 (pure copies: node primitives of u~ and 0.5 C)
+template <int N>
+__device__ __forceinline__ void res_stage_blocks(const ResParams& P, const ResSmem<N>& S, int e0, int nb,
+                                                 StageBlock (&blk)[2]) {
+  constexpr int N3 = N * N * N;
+  blk[0] = {S.PRIM, P.ut_vol + (size_t)e0 * 6 * N3, nb * 6 * N3};
+  blk[1] = {S.COF, P.cof + (size_t)e0 * 9 * N3, nb * 9 * N3};
+}
+
+template <int N, int KM>
+__device__ __forceinline__ void res_lines(const ResParams& P, const ResOps<N>& O, int e0, int nb,
+                                          const ResSmem<N>& S);
+template <int N>
+__device__ __forceinline__ void res_writeout(const ResParams& P, int e0, int nb, const double* ACCV);
+
 template <int N, int KM>
 __device__ __forceinline__ void res_batch(const ResParams& P, const ResOps<N>& O, int e0, double* sm) {
   using Cfg = ResCfg<N>;
-  constexpr int N2 = Cfg::N2, N3 = Cfg::N3, EPB = Cfg::EPB, LINES = Cfg::LINES;
-  constexpr int AS = 15 * N3;     // element stride of ACCV
-  double* ACCV = sm;                    // [EPB][3][5][N3]
-  double* PRIM = ACCV + EPB * AS;       // [EPB][6][N3] half-scaled primitives
-  double* COF = PRIM + EPB * 6 * N3;    // [EPB][9][N3] 0.5 C
-  const int tid = threadIdx.x, nthr = blockDim.x;
+  constexpr int EPB = Cfg::EPB;
+  const ResSmem<N> S(sm);
   const int nb = min(EPB, P.E - e0);
-  const double g = P.gamma, gm1 = g - 1.0;
   PHASE_START();
-  // stage element data (pure copies, TMA bulk): node primitives of u~ and 0.5 C
   __shared__ unsigned long long bar;
   {
-    const StageBlock blk[2] = {{PRIM, P.ut_vol + (size_t)e0 * 6 * N3, nb * 6 * N3},
-                               {COF, P.cof + (size_t)e0 * 9 * N3, nb * 9 * N3}};
+    StageBlock blk[2];
+    res_stage_blocks<N>(P, S, e0, nb, blk);
     stage_issue<2>(blk, &bar);
   }
   __syncthreads();
   stage_wait(&bar);
   __syncthreads();
   PHASE_MARK(0);
+  res_lines<N, KM>(P, O, e0, nb, S);
+  __syncthreads();
+  PHASE_MARK(1);
+  res_writeout<N>(P, e0, nb, S.ACCV);
+  PHASE_MARK(2);
+}
+
+template <int N, int KM>
+__device__ __forceinline__ void res_lines(const ResParams& P, const ResOps<N>& O, int e0, int nb,
+                                          const ResSmem<N>& S) {
+  using Cfg = ResCfg<N>;
+  constexpr int N2 = Cfg::N2, N3 = Cfg::N3, LINES = Cfg::LINES;
+  constexpr int AS = 15 * N3;     // element stride of ACCV
+  double* ACCV = S.ACCV;
+  const double* PRIM = S.PRIM;
+  const double* COF = S.COF;
+  const int tid = threadIdx.x;
+  const double g = P.gamma, gm1 = g - 1.0;
 
   // ---- line phase: one thread owns one 1D line (dir, t1, t2) ----
   double fout0[NS], fout1[NS];  // face rows of the two faces this line pierces (registers)
@@ -286,15 +323,17 @@ __device__ __forceinline__ void res_batch(const ResParams& P, const ResOps<N>& O
       fa[(s * 2 + 1) * N2] = fout1[s];
     }
   }
-  __syncthreads();
-  PHASE_MARK(1);
-  // volume rows: sum of the three direction accumulators
-  for (int it = tid; it < nb * 5 * N3; it += nthr) {
+}
+
+// volume rows: sum of the three direction accumulators
+template <int N>
+__device__ __forceinline__ void res_writeout(const ResParams& P, int e0, int nb, const double* ACCV) {
+  constexpr int N3 = N * N * N, AS = 15 * N3;
+  for (int it = threadIdx.x; it < nb * 5 * N3; it += blockDim.x) {
     const int b = it / (5 * N3), r = it - b * 5 * N3;
     const double* a0 = ACCV + b * AS;
     P.vol[(size_t)e0 * 5 * N3 + it] = a0[r] + a0[5 * N3 + r] + a0[10 * N3 + r];
   }
-  PHASE_MARK(2);
 }
 
 // One batch per CTA (CTAs retire at staggered times, so their staging and
