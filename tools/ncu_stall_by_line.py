@@ -17,7 +17,7 @@ fname, hdr, tot = "?", None, 0.0
 for row in csv.reader(out.splitlines()):
     if not row:
         continue
-    if row[0] == "File Name":
+    if row[0] in ("File Name", "File Path"):
         fname = row[1].split("/")[-1]
         continue
     if row[0] == "Line No":
