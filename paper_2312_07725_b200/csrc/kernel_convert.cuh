@@ -13,6 +13,7 @@ namespace nsfr_b200 {
 template <int N>
 struct ConvOps {
   double A[N * N];  // chi (to_quad) or Pi, row-major N x N
+  double B[N * N];  // MODE 2: chi, applied after A to what A wrote out
 };
 
 template <int N>
@@ -23,30 +24,15 @@ struct ConvCfg {
   static constexpr int SMEM = EPB * 5 * N3 * 8;
 };
 
-// elements [e_begin, e_end): one CTA per EPB elements; each thread owns whole
-// lines, so a pass updates its lines in place (no other thread touches them).
-// LAM: no output; lambda_max = max(|u| + a) over the admissible nodes of the
-// converted state into *lam (atomicMax on the bits; u_q = chi^3 u_hat, the
-// node set and formula of K1, so adaptive_dt of a state about to leave the
-// device equals what K1 finds when it comes back).
-template <int N, bool LAM = false>
-__global__ void __launch_bounds__(ConvCfg<N>::THREADS)
-    k_convert_lines(ConvOps<N> O, const double* __restrict__ in, double* __restrict__ out, int e_begin,
-                    int e_end, double gamma = 0.0, unsigned long long* lam = nullptr) {
+// The three passes of op over the staged block S (in place); the zeta pass
+// also writes its results to out when WRITE (consecutive threads, consecutive
+// nodes), and keeps them in S when KEEP.
+template <int N, bool WRITE, bool KEEP>
+__device__ __forceinline__ void conv_passes(const double (&op)[N * N], double* S, double* __restrict__ out,
+                                            int e0, int nb) {
   using Cfg = ConvCfg<N>;
-  constexpr int N2 = Cfg::N2, N3 = Cfg::N3, EPB = Cfg::EPB, LINES = Cfg::LINES;
-  extern __shared__ __align__(128) double S[];
-  const int e0 = e_begin + blockIdx.x * EPB;
-  const int nb = min(EPB, e_end - e0);
+  constexpr int N2 = Cfg::N2, N3 = Cfg::N3, LINES = Cfg::LINES;
   const int tid = threadIdx.x, nthr = blockDim.x;
-  __shared__ unsigned long long bar;
-  {
-    const StageBlock blk[1] = {{S, in + (size_t)e0 * 5 * N3, nb * 5 * N3}};
-    stage_issue<1>(blk, &bar);
-  }
-  __syncthreads();
-  stage_wait(&bar);
-  __syncthreads();
 #pragma unroll
   for (int D = 0; D < 3; ++D) {
     const int stride = D == 0 ? 1 : (D == 1 ? N : N2);
@@ -62,14 +48,49 @@ __global__ void __launch_bounds__(ConvCfg<N>::THREADS)
       for (int row = 0; row < N; ++row) {
         double acc = 0.0;
 #pragma unroll
-        for (int a = 0; a < N; ++a) acc = fma(O.A[row * N + a], v[a], acc);
-        if (D < 2 || LAM)
-          x[row * stride] = acc;
-        else  // zeta lines: consecutive threads write consecutive nodes
-          out[((size_t)(e0 + b) * 5 + s) * N3 + base + row * N2] = acc;
+        for (int a = 0; a < N; ++a) acc = fma(op[row * N + a], v[a], acc);
+        if (D < 2 || KEEP) x[row * stride] = acc;
+        if (D == 2 && WRITE) out[((size_t)(e0 + b) * 5 + s) * N3 + base + row * N2] = acc;
       }
     }
-    if (D < 2 || LAM) __syncthreads();
+    if (D < 2 || KEEP) __syncthreads();
+  }
+}
+
+// elements [e_begin, e_end): one CTA per EPB elements; each thread owns whole
+// lines, so a pass updates its lines in place (no other thread touches them).
+// MODE 0: out = A^3 in. MODE 1 (LAM): no output; lambda_max = max(|u| + a)
+// over the admissible nodes of A^3 in (A = chi: u_q = chi^3 u_hat, the node set
+// and formula of K1, so adaptive_dt of a state about to leave the device
+// equals what K1 finds when it comes back) into *lam (atomicMax on the bits).
+// MODE 2: out = A^3 in (A = Pi) and lambda_max of B^3 out (B = chi) from the
+// same bytes, in one pass over HBM.
+template <int N, int MODE = 0>
+__global__ void __launch_bounds__(ConvCfg<N>::THREADS)
+    k_convert_lines(ConvOps<N> O, const double* __restrict__ in, double* __restrict__ out, int e_begin,
+                    int e_end, double gamma = 0.0, unsigned long long* lam = nullptr) {
+  using Cfg = ConvCfg<N>;
+  constexpr int N3 = Cfg::N3, EPB = Cfg::EPB;
+  constexpr bool LAM = MODE != 0;
+  extern __shared__ __align__(128) double S[];
+  const int e0 = e_begin + blockIdx.x * EPB;
+  const int nb = min(EPB, e_end - e0);
+  const int tid = threadIdx.x, nthr = blockDim.x;
+  __shared__ unsigned long long bar;
+  {
+    const StageBlock blk[1] = {{S, in + (size_t)e0 * 5 * N3, nb * 5 * N3}};
+    stage_issue<1>(blk, &bar);
+  }
+  __syncthreads();
+  stage_wait(&bar);
+  __syncthreads();
+  if constexpr (MODE == 0) {
+    conv_passes<N, true, false>(O.A, S, out, e0, nb);
+  } else if constexpr (MODE == 1) {
+    conv_passes<N, false, true>(O.A, S, out, e0, nb);
+  } else {
+    conv_passes<N, true, true>(O.A, S, out, e0, nb);
+    conv_passes<N, false, true>(O.B, S, out, e0, nb);
   }
   if (LAM) {
     double lm = 0.0;

@@ -631,42 +631,50 @@ int setup_kernel_smem(nsfr_gpu_ctx* ctx, size_t bytes, const void* fn) {
   return NSFR_OK;
 }
 
-// lam_out: instead of writing out, lambda_max of chi^3 in into d_step->lam_out_bits
+// mode 0: out = (chi or Pi)^3 in; 1: lambda_max of chi^3 in into
+// d_step->lam_out_bits (no output); 2: out = Pi^3 in and lambda_max of chi^3 out
 template <int N>
 int launch_convert_lines(nsfr_gpu_ctx* ctx, const double* in, double* out, bool to_quad, int e0, int e1,
-                         bool lam_out) {
+                         int mode) {
   using Cfg = ConvCfg<N>;
   const unsigned bit = 1u << (ctx->s.device & 31);
   static std::atomic<unsigned> done{0};
   if (!(done.load() & bit)) {
-    CK(cudaFuncSetAttribute(k_convert_lines<N>, cudaFuncAttributeMaxDynamicSharedMemorySize, Cfg::SMEM));
-    CK(cudaFuncSetAttribute(k_convert_lines<N, true>, cudaFuncAttributeMaxDynamicSharedMemorySize,
-                            Cfg::SMEM));
+    CK(cudaFuncSetAttribute(k_convert_lines<N, 0>, cudaFuncAttributeMaxDynamicSharedMemorySize, Cfg::SMEM));
+    CK(cudaFuncSetAttribute(k_convert_lines<N, 1>, cudaFuncAttributeMaxDynamicSharedMemorySize, Cfg::SMEM));
+    CK(cudaFuncSetAttribute(k_convert_lines<N, 2>, cudaFuncAttributeMaxDynamicSharedMemorySize, Cfg::SMEM));
     done.fetch_or(bit);
   }
   ConvOps<N> o{};
-  for (int i = 0; i < N * N; ++i) o.A[i] = to_quad ? ctx->htab.interp[i] : ctx->htab.proj[i];
+  for (int i = 0; i < N * N; ++i) {
+    o.A[i] = to_quad ? ctx->htab.interp[i] : ctx->htab.proj[i];
+    o.B[i] = ctx->htab.interp[i];
+  }
   const int grid = (e1 - e0 + Cfg::EPB - 1) / Cfg::EPB;
-  if (lam_out)
-    k_convert_lines<N, true><<<grid, Cfg::THREADS, Cfg::SMEM, ctx->st>>>(o, in, nullptr, e0, e1, ctx->s.gamma,
-                                                                         &ctx->d_step->lam_out_bits);
+  unsigned long long* lam = &ctx->d_step->lam_out_bits;
+  if (mode == 1)
+    k_convert_lines<N, 1><<<grid, Cfg::THREADS, Cfg::SMEM, ctx->st>>>(o, in, nullptr, e0, e1, ctx->s.gamma, lam);
+  else if (mode == 2)
+    k_convert_lines<N, 2><<<grid, Cfg::THREADS, Cfg::SMEM, ctx->st>>>(o, in, out, e0, e1, ctx->s.gamma, lam);
   else
-    k_convert_lines<N><<<grid, Cfg::THREADS, Cfg::SMEM, ctx->st>>>(o, in, out, e0, e1);
+    k_convert_lines<N, 0><<<grid, Cfg::THREADS, Cfg::SMEM, ctx->st>>>(o, in, out, e0, e1);
   ++ctx->launches;
   CK(cudaGetLastError());
   return NSFR_OK;
 }
 
 // adaptive_dt's lambda_max of chi^3 u_hat over [e0, e1) (u_hat on the device,
-// e.g. a state on its way to the host) into d_step->lam_out_bits
-int lam_of_uhat(nsfr_gpu_ctx* ctx, const double* uhat, int e0, int e1) {
+// e.g. a state on its way to the host) into d_step->lam_out_bits; with
+// from_q, u_hat = Pi^3 u_q is formed from `in` on the way into `out` first
+int lam_of_uhat(nsfr_gpu_ctx* ctx, const double* in, int e0, int e1, double* out = nullptr) {
   if (e1 <= e0) return NSFR_OK;
+  const int mode = out ? 2 : 1;
   switch (ctx->NQ == ctx->N ? ctx->N : 0) {
-    case 3: return launch_convert_lines<3>(ctx, uhat, nullptr, true, e0, e1, true);
-    case 4: return launch_convert_lines<4>(ctx, uhat, nullptr, true, e0, e1, true);
-    case 5: return launch_convert_lines<5>(ctx, uhat, nullptr, true, e0, e1, true);
-    case 6: return launch_convert_lines<6>(ctx, uhat, nullptr, true, e0, e1, true);
-    case 7: return launch_convert_lines<7>(ctx, uhat, nullptr, true, e0, e1, true);
+    case 3: return launch_convert_lines<3>(ctx, in, out, mode == 1, e0, e1, mode);
+    case 4: return launch_convert_lines<4>(ctx, in, out, mode == 1, e0, e1, mode);
+    case 5: return launch_convert_lines<5>(ctx, in, out, mode == 1, e0, e1, mode);
+    case 6: return launch_convert_lines<6>(ctx, in, out, mode == 1, e0, e1, mode);
+    case 7: return launch_convert_lines<7>(ctx, in, out, mode == 1, e0, e1, mode);
   }
   ctx->msg = "adaptive dt of the output: overintegrated DG is not supported";
   return NSFR_E_DIM;
@@ -678,11 +686,11 @@ int convert_range(nsfr_gpu_ctx* ctx, const double* in, double* out, bool to_quad
   if (e1 <= e0) return NSFR_OK;
   if (ctx->NQ == ctx->N) {
     switch (ctx->N) {
-      case 3: return launch_convert_lines<3>(ctx, in, out, to_quad, e0, e1, false);
-      case 4: return launch_convert_lines<4>(ctx, in, out, to_quad, e0, e1, false);
-      case 5: return launch_convert_lines<5>(ctx, in, out, to_quad, e0, e1, false);
-      case 6: return launch_convert_lines<6>(ctx, in, out, to_quad, e0, e1, false);
-      case 7: return launch_convert_lines<7>(ctx, in, out, to_quad, e0, e1, false);
+      case 3: return launch_convert_lines<3>(ctx, in, out, to_quad, e0, e1, 0);
+      case 4: return launch_convert_lines<4>(ctx, in, out, to_quad, e0, e1, 0);
+      case 5: return launch_convert_lines<5>(ctx, in, out, to_quad, e0, e1, 0);
+      case 6: return launch_convert_lines<6>(ctx, in, out, to_quad, e0, e1, 0);
+      case 7: return launch_convert_lines<7>(ctx, in, out, to_quad, e0, e1, 0);
     }
   }
   const size_t smem = sizeof(double) * 4 * std::max(nsol(ctx), nquad(ctx));
@@ -1354,15 +1362,19 @@ int nsfr_gpu_rk4_step_host(nsfr_gpu_ctx* ctx, const double* u_in, double* u_out,
     if (L & 1) return residual(ctx, 0, e0, e1);
     if (int rc = update(ctx, stage, false, nullptr, e0, e1)) return rc;
     if (stage < 4) return NSFR_OK;
-    // u_{n+1} of this chunk is final: Pi^3 into the dead accumulator, download
-    if (int rc = convert_range(ctx, ctx->d_un, ctx->d_acc, false, e0, e1)) return rc;
+    // u_{n+1} of this chunk is final: Pi^3 into the dead accumulator (and
+    // adaptive_dt's lambda of exactly those bytes, same pass), download
+    if (dt_next) {
+      if (int rc = lam_of_uhat(ctx, ctx->d_un, e0, e1, ctx->d_acc)) return rc;
+    } else if (int rc = convert_range(ctx, ctx->d_un, ctx->d_acc, false, e0, e1)) {
+      return rc;
+    }
     CK(cudaEventRecord(ctx->chunk_ev[nch + c], ctx->st));
     CK(cudaStreamWaitEvent(ctx->st_d2h, ctx->chunk_ev[nch + c], 0));
     if (!nocopy)
       CK(cudaMemcpyAsync(u_out + e0 * per, ctx->d_acc + e0 * per, sizeof(double) * per * (e1 - e0),
                        cudaMemcpyDeviceToHost, ctx->st_d2h));
-    // adaptive_dt of what goes back, while it goes (reads the same buffer)
-    return dt_next ? lam_of_uhat(ctx, ctx->d_acc, e0, e1) : NSFR_OK;
+    return NSFR_OK;
   };
   auto layer = [&](int L, int c) -> int {
     cudaStream_t lane = ctx->lanes[c % S];
