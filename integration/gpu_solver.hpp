@@ -76,7 +76,7 @@ class GpuSolver {
  private:
   void check(int rc) {
     if (rc == NSFR_OK) return;
-    const std::string what = nsfr_gpu_last_error(ctx_);
+    const std::string what = ctx_ ? nsfr_gpu_last_error(ctx_) : nsfr_gpu_create_error();
     double t = 0.0;
     switch (rc) {
       case NSFR_E_DIM: throw DimensionError(what);
