@@ -38,6 +38,8 @@ struct nsfr_gpu_ctx {
   cudaStream_t st = nullptr;
   cudaStream_t st_copy = nullptr;  // host<->device state transfers, chunk-pipelined with st
   cudaStream_t st_d2h = nullptr;   // device->host leg of the streamed step (runs beside st_copy)
+  cudaStream_t st_comm = nullptr;   // halo exchange overlapped with K2 on the interior planes
+  cudaEvent_t ev_fork = nullptr, ev_halo = nullptr;
   std::vector<cudaStream_t> lanes;  // streamed step: compute lanes (a chunk's ops stay on one lane)
   std::vector<cudaEvent_t> op_ev;   // streamed step: one event per (layer, chunk) op, + fork/join
   std::vector<cudaEvent_t> chunk_ev;
@@ -535,11 +537,48 @@ int enqueue_step_dg(nsfr_gpu_ctx* ctx, bool fixed_dt) {
   return NSFR_OK;
 }
 
+// One stage's halo exchange and K2: with NCCL and at least
+// three planes, the grouped send/recv runs on st_comm while K2 covers the
+// interior planes, whose faces need no halo; the two end planes follow once
+// the halo has landed. Element-local arithmetic: bitwise the serial order.
+// NSFR_NO_HALO_OVERLAP=1 keeps exchange -> K2 on one stream.
+bool halo_overlap(const nsfr_gpu_ctx* ctx) {
+  return ctx->comm && !ctx->dg && ctx->nz >= 3 && !std::getenv("NSFR_NO_HALO_OVERLAP");
+}
+
+int exchange_residual(nsfr_gpu_ctx* ctx) {
+  if (!halo_overlap(ctx)) {
+    if (int rc = exchange(ctx)) return rc;
+    return residual(ctx);
+  }
+  if (!ctx->st_comm) {
+    CK(cudaStreamCreateWithFlags(&ctx->st_comm, cudaStreamNonBlocking));
+    CK(cudaEventCreateWithFlags(&ctx->ev_fork, cudaEventDisableTiming));
+    CK(cudaEventCreateWithFlags(&ctx->ev_halo, cudaEventDisableTiming));
+  }
+  const int plane = ctx->m * ctx->m;
+  cudaStream_t main_st = ctx->st;
+  CK(cudaEventRecord(ctx->ev_fork, main_st));  // the send planes are packed
+  CK(cudaStreamWaitEvent(ctx->st_comm, ctx->ev_fork, 0));
+  ctx->st = ctx->st_comm;
+  const int rc_x = exchange(ctx);
+  ctx->st = main_st;
+  if (rc_x) return rc_x;
+  CK(cudaEventRecord(ctx->ev_halo, ctx->st_comm));
+  if (int rc = residual(ctx, 0, plane, ctx->E - plane)) return rc;
+  CK(cudaStreamWaitEvent(main_st, ctx->ev_halo, 0));
+  if (int rc = residual(ctx, 0, 0, plane)) return rc;
+  return residual(ctx, 0, ctx->E - plane, ctx->E);
+}
+
 // Enqueue one RK4 step (no host sync), graph-capturable: needs the projection
 // of d_un in place (ensure_projected) and leaves the projection of u_{n+1}.
 // fixed_dt: dt already in d_step.
 constexpr long long kLaunchesPerStep = 1 + 4 * 2 + 1;
-long long launches_per_step(const nsfr_gpu_ctx* ctx) { return ctx->dg ? 1 + 1 + 1 + 4 + 3 + 1 : kLaunchesPerStep; }
+long long launches_per_step(const nsfr_gpu_ctx* ctx) {
+  if (ctx->dg) return 1 + 1 + 1 + 4 + 3 + 1;
+  return halo_overlap(ctx) ? kLaunchesPerStep + 4 * 2 : kLaunchesPerStep;  // K2 in three ranges
+}
 int enqueue_step(nsfr_gpu_ctx* ctx, bool fixed_dt) {
   if (ctx->dg) return enqueue_step_dg(ctx, fixed_dt);
   if (!fixed_dt) {
@@ -552,8 +591,7 @@ int enqueue_step(nsfr_gpu_ctx* ctx, bool fixed_dt) {
   }
   ++ctx->launches;
   for (int stage = 1; stage <= 4; ++stage) {
-    if (int rc = exchange(ctx)) return rc;
-    if (int rc = residual(ctx)) return rc;
+    if (int rc = exchange_residual(ctx)) return rc;
     if (int rc = update(ctx, stage, false)) return rc;
   }
   k_step_end<<<1, 1, 0, ctx->st>>>(ctx->d_step);
@@ -944,6 +982,9 @@ int nsfr_gpu_destroy(nsfr_gpu_ctx* ctx) {
   if (ctx->st_copy) cudaStreamDestroy(ctx->st_copy);
   if (ctx->st_d2h) cudaStreamDestroy(ctx->st_d2h);
   for (auto l : ctx->lanes) cudaStreamDestroy(l);
+  if (ctx->st_comm) cudaStreamDestroy(ctx->st_comm);
+  if (ctx->ev_fork) cudaEventDestroy(ctx->ev_fork);
+  if (ctx->ev_halo) cudaEventDestroy(ctx->ev_halo);
   for (auto e : ctx->op_ev) cudaEventDestroy(e);
   if (ctx->st) cudaStreamDestroy(ctx->st);
   delete ctx;
