@@ -20,10 +20,10 @@ for k in $KERNELS; do
   skip=4
   [ "$k" = "k_project" ] && skip=0
   timeout 900 ncu --set full --import-source on --clock-control none -k regex:$k -s $skip -c 1 \
-    -o /tmp/full_$k -f python bench.py --steps 1 --warmup 3 --no-cpu-baseline > $OUT/ncu_$k.log 2>&1
+    -o /tmp/full_$k -f $CMD > $OUT/ncu_$k.log 2>&1
   echo "$k rc=$?"
   python tools/ncu_report.py /tmp/full_$k.ncu-rep "ncu --set full: $k at the bench workload" \
-    "ncu --set full --import-source on --clock-control none -k regex:$k -s $skip -c 1 python bench.py --steps 1 --warmup 3 --no-cpu-baseline" \
+    "ncu --set full --import-source on --clock-control none -k regex:$k -s $skip -c 1 $CMD" \
     $OUT/$k.md > /dev/null 2>&1
   python tools/ncu_ops_by_line.py /tmp/full_$k.ncu-rep 40 > $OUT/${k}_ops_by_line.txt 2>&1
   for r in barrier wait short_sb long_sb mio lg; do
