@@ -1273,8 +1273,8 @@ int finish_dt_next(nsfr_gpu_ctx* ctx, double* dt_next) {
   return NSFR_OK;
 }
 
-int nsfr_gpu_rk4_step_host(nsfr_gpu_ctx* ctx, const double* u_in, double* u_out, double dt,
-                           double cfl, double t_final, double* dt_used, double* dt_next) {
+static int rk4_step_host_impl(nsfr_gpu_ctx* ctx, const double* u_in, double* u_out, double dt,
+                              double cfl, double t_final, double* dt_used, double* dt_next) {
   const bool fixed = dt > 0.0;
   // seg: a z-slab (or a 1-rank NCCL loopback) whose end planes take NCCL halos
   // instead of wrapping locally; external-halo contexts and DG do not stream
@@ -1487,6 +1487,24 @@ int nsfr_gpu_rk4_step_host(nsfr_gpu_ctx* ctx, const double* u_in, double* u_out,
   ctx->proj_valid = true;  // K3 of stage 4 left the projection (and lambda) of u_{n+1}
   if (dt_used) *dt_used = ctx->h_step->dt;
   return dt_next ? finish_dt_next(ctx, dt_next) : NSFR_OK;
+}
+
+int nsfr_gpu_rk4_step_host(nsfr_gpu_ctx* ctx, const double* u_in, double* u_out, double dt,
+                           double cfl, double t_final, double* dt_used, double* dt_next) {
+  if (!ctx) return NSFR_E_DIM;
+  if (!u_in || !u_out) {
+    ctx->msg = "rk4_step_host: null state buffer";
+    return NSFR_E_DIM;
+  }
+  const int rc = rk4_step_host_impl(ctx, u_in, u_out, dt, cfl, t_final, dt_used, dt_next);
+  if (rc) {  // a failure mid-pipeline: let every stream drain before the context is reused
+    for (auto l : ctx->lanes) cudaStreamSynchronize(l);
+    if (ctx->st_copy) cudaStreamSynchronize(ctx->st_copy);
+    if (ctx->st_d2h) cudaStreamSynchronize(ctx->st_d2h);
+    cudaStreamSynchronize(ctx->st);
+    ctx->proj_valid = false;
+  }
+  return rc;
 }
 
 int nsfr_gpu_l2_error(nsfr_gpu_ctx* ctx, int kind, double out2[2]) {

@@ -96,6 +96,14 @@ def test_streamed_step_inadmissible_raises():
     u.reshape(u.shape[0], 5, -1)[7, 0, :] = -1.0  # negative density in one element
     with pytest.raises(pkg.StepFailureError):
         a.rk4_step_host(u, dt=1e-3)
+    # the context stays usable after the failed pipeline
+    a.init_case()
+    b = pkg.GpuSolver(pkg.SolverConfig(p=3, m=4))
+    b.init_case()
+    u0 = b.get_state()
+    got, _, _ = a.rk4_step_host(u0, dt=1e-3)
+    b.rk4_step_dt(1e-3)
+    np.testing.assert_array_equal(got, b.get_state())
 
 
 @pytest.mark.parametrize("scheme,m", [("nsfr", 8), ("nsfr", 5), ("dg", 4)])
