@@ -102,6 +102,7 @@ def test_streamed_step_inadmissible_raises():
     b.init_case()
     u0 = b.get_state()
     got, _, _ = a.rk4_step_host(u0, dt=1e-3)
+    b.set_state(u0)
     b.rk4_step_dt(1e-3)
     np.testing.assert_array_equal(got, b.get_state())
 
