@@ -210,7 +210,6 @@ __device__ __forceinline__ void res_lines(const ResParams& P, const ResOps<N>& O
   const double g = P.gamma, gm1 = g - 1.0;
 
   // ---- line phase: one thread owns one 1D line (dir, t1, t2) ----
-  double fout0[NS], fout1[NS];  // face rows of the two faces this line pierces (registers)
   const int lb = tid / LINES;
   const int ll = tid - lb * LINES;
   const int ldir = ll / N2, lrem = ll - ldir * N2;
@@ -304,23 +303,11 @@ __device__ __forceinline__ void res_lines(const ResParams& P, const ResOps<N>& O
         for (int s = 0; s < NS; ++s) fn[s] -= d[s];
       }
       const double cc = wt * jg;
-      if (side == 0) {
+      // this face's row leaves registers now (facc[e][dir][s][side][k]): nothing
+      // of side 0 stays live through side 1
+      double* fa = P.facc + ((size_t)e * 3 + dir) * 10 * N2 + k + side * N2;
 #pragma unroll
-        for (int s = 0; s < NS; ++s) fout0[s] = fma(cc, fn[s], ff[s]);
-      } else {
-#pragma unroll
-        for (int s = 0; s < NS; ++s) fout1[s] = fma(cc, fn[s], ff[s]);
-      }
-    }
-  }
-  // face rows straight from registers: facc[e][dir][s][side][k]
-  if (KM != 1 && lb < nb) {
-    const int k = (lrem % N) + N * (lrem / N);
-    double* fa = P.facc + ((size_t)(e0 + lb) * 3 + ldir) * 10 * N2 + k;
-#pragma unroll
-    for (int s = 0; s < NS; ++s) {
-      fa[(s * 2 + 0) * N2] = fout0[s];
-      fa[(s * 2 + 1) * N2] = fout1[s];
+      for (int s = 0; s < NS; ++s) fa[s * 2 * N2] = fma(cc, fn[s], ff[s]);
     }
   }
 }
