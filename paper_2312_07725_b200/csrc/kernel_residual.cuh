@@ -236,15 +236,15 @@ __device__ __forceinline__ void res_lines(const ResParams& P, const ResOps<N>& O
       const int f = 2 * dir + side;
       const double sign = side ? 1.0 : -1.0;
       const int k = t1 + N * t2;
-      double uf[NS], un[NS];
+      // Through the hybrid loop only the two traces, the face's half-scaled
+      // bundle and its halved cofactor column stay live (the primitives are
+      // recomputed after it), which keeps the flux chains out of local memory.
       const double* tr = P.traces + ((size_t)e * 6 + f) * 5 * N2 + k;
-#pragma unroll
-      for (int s = 0; s < NS; ++s) uf[s] = tr[s * N2];
+      const double* nt = nullptr;
       {  // neighbour across face f (geometry.hpp:24-29), its face f^1, same node k
         const int mm = P.m;
         int i = e % mm, j = (e / mm) % mm, kl = e / (mm * mm);
         const int step = side ? 1 : -1;
-        const double* nt = nullptr;
         if (dir == 0) i = (i + step + mm) % mm;
         if (dir == 1) j = (j + step + mm) % mm;
         if (dir == 2) {
@@ -256,22 +256,31 @@ __device__ __forceinline__ void res_lines(const ResParams& P, const ResOps<N>& O
           }
         }
         if (!nt) nt = P.traces + (((size_t)(i + mm * (j + mm * kl))) * 6 + (f ^ 1)) * 5 * N2 + k;
-#pragma unroll
-        for (int s = 0; s < NS; ++s) un[s] = nt[s * N2];
       }
-      const PrimX pf = d_primx(g, uf);
-      const PrimH pfh = to_half(gm1, pf);
-      // own face cofactor column C_f[:,dir] = sum_a bound_flux(side,a) C_a (geometry.cpp:218-226)
-      double cf0 = 0.0, cf1 = 0.0, cf2 = 0.0;
+      double uf[NS], un[NS];  // loaded now: their latency hides behind the hybrid loop
 #pragma unroll
-      for (int a = 0; a < N; ++a) {
-        const int ia = lbase + a * stride;
-        const double w = O.bflux[side * N + a];
-        cf0 = fma(w, 2.0 * Ch[(0 + dir) * N3 + ia], cf0);
-        cf1 = fma(w, 2.0 * Ch[(3 + dir) * N3 + ia], cf1);
-        cf2 = fma(w, 2.0 * Ch[(6 + dir) * N3 + ia], cf2);
+      for (int s = 0; s < NS; ++s) {
+        uf[s] = tr[s * N2];
+        un[s] = nt[s * N2];
       }
-      const double ch0 = 0.5 * cf0, ch1 = 0.5 * cf1, ch2 = 0.5 * cf2;
+      const PrimH pfh = to_half(gm1, d_primx(g, uf));
+      // own face cofactor column C_f[:,dir] = sum_a bound_flux(side,a) C_a (geometry.cpp:218-226),
+      // kept halved (ch = C_f/2; doubling it back is exact)
+      double ch0, ch1, ch2;
+      {
+        double cf0 = 0.0, cf1 = 0.0, cf2 = 0.0;
+#pragma unroll
+        for (int a = 0; a < N; ++a) {
+          const int ia = lbase + a * stride;
+          const double w = O.bflux[side * N + a];
+          cf0 = fma(w, 2.0 * Ch[(0 + dir) * N3 + ia], cf0);
+          cf1 = fma(w, 2.0 * Ch[(3 + dir) * N3 + ia], cf1);
+          cf2 = fma(w, 2.0 * Ch[(6 + dir) * N3 + ia], cf2);
+        }
+        ch0 = 0.5 * cf0;
+        ch1 = 0.5 * cf1;
+        ch2 = 0.5 * cf2;
+      }
       double ff[NS] = {0.0, 0.0, 0.0, 0.0, 0.0};
 #pragma unroll 1
       for (int a = 0; a < N; ++a) {
@@ -289,10 +298,11 @@ __device__ __forceinline__ void res_lines(const ResParams& P, const ResOps<N>& O
         }
       }
       // S8 f*.n with the own unit normal and J^Gamma (geometry.cpp:227-236)
-      const double v0 = sign * cf0, v1 = sign * cf1, v2 = sign * cf2;
+      const double v0 = sign * (2.0 * ch0), v1 = sign * (2.0 * ch1), v2 = sign * (2.0 * ch2);
       const double jg = sqrt(v0 * v0 + v1 * v1 + v2 * v2);
       const double ijg = 1.0 / jg;
       const double nrm[3] = {v0 * ijg, v1 * ijg, v2 * ijg};
+      const PrimX pf = d_primx(g, uf);  // recomputed rather than kept through the loop
       const PrimX pn = d_primx(g, un);
       double fn[NS];
       d_flux_h<(KM != 0)>(pfh, to_half(gm1, pn), nrm[0], nrm[1], nrm[2], fn, amask);
