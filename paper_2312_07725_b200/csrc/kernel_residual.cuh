@@ -105,7 +105,11 @@ struct ResCfg {
 #ifdef NSFR_RES_MINB
   static constexpr int MINB = NSFR_RES_MINB;
 #else
-  static constexpr int MINB = SMEM <= 56 * 1024 ? 4 : (SMEM <= 75 * 1024 ? 3 : (SMEM <= 112 * 1024 ? 2 : 1));
+  // what shared memory allows, except p <= 3: 2 CTAs/SM with the registers the
+  // fully unrolled pair loops want beat 3-4 CTAs with spills (measured K2:
+  // p=3 -6.2%, p=2 -12%; p=4 keeps 3: 2 is +23%)
+  static constexpr int MINB_S = SMEM <= 56 * 1024 ? 4 : (SMEM <= 75 * 1024 ? 3 : (SMEM <= 112 * 1024 ? 2 : 1));
+  static constexpr int MINB = N <= 4 && MINB_S > 2 ? 2 : MINB_S;
 #endif
 };
 
