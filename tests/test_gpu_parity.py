@@ -483,3 +483,29 @@ def test_nccl_loopback_matches_plain(scheme):
     np.testing.assert_array_equal(b.get_state_q(), a.get_state_q())
     np.testing.assert_array_equal(b.l2_error(), a.l2_error())
     np.testing.assert_array_equal(b.conserved_totals(), a.conserved_totals())
+
+
+@pytest.mark.parametrize("p,m,nranks", [(3, 5, 2), (2, 7, 3)])
+def test_partition_independence_with_mixed_series(p, m, nranks):
+    """A state rough enough that some pairs take the short log-mean series and
+    others the long one, on slabs whose batches do not line up with the whole
+    box's (m^2 not a multiple of the elements per CTA): the residual is still
+    bitwise the whole box's, because each pair's series choice is its own."""
+    pkg = P()
+    kw = dict(p=p, m=m)
+    whole = pkg.GpuSolver(gpu_cfg(**kw))
+    whole.init_case()
+    u = whole.get_state()
+    rng = np.random.default_rng(7)
+    u = u * (1 + 0.03 * rng.uniform(-1, 1, u.shape))  # pair gaps straddle the 2% switch
+    whole.set_state(u)
+    ranks = [pkg.GpuSolver(gpu_cfg(rank=r, nranks=nranks, **kw)) for r in range(nranks)]
+    off = 0
+    for g in ranks:
+        n = g.state_shape[0]
+        g.set_state(u[off:off + n])
+        off += n
+        g.project()
+    _swap(ranks)
+    rhs = np.concatenate([g.residual() for g in ranks])
+    np.testing.assert_array_equal(rhs, whole.rhs())
