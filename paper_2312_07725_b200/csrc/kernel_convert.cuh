@@ -57,6 +57,24 @@ __device__ __forceinline__ void conv_passes(const double (&op)[N * N], double* S
   }
 }
 
+// lambda_max = max(|u| + a) over the admissible nodes of the [nb][5][N3]
+// block S (synchronised by the caller) into *lam (atomicMax on the bits);
+// every thread of the CTA calls it
+template <int N>
+__device__ __forceinline__ void conv_lambda(const double* S, int nb, double gamma, unsigned long long* lam) {
+  constexpr int N3 = N * N * N;
+  double lm = 0.0;
+  for (int it = threadIdx.x; it < nb * N3; it += blockDim.x) {
+    const int b = it / N3, q = it - b * N3;
+    double uu[NS];
+#pragma unroll
+    for (int s = 0; s < NS; ++s) uu[s] = S[(b * 5 + s) * N3 + q];
+    if (d_admissible(gamma, uu)) lm = fmax(lm, d_node_wavespeed(gamma, uu));
+  }
+  for (int o = 16; o > 0; o >>= 1) lm = fmax(lm, __shfl_xor_sync(0xffffffffu, lm, o));
+  if ((threadIdx.x & 31) == 0 && lm > 0.0) atomicMax(lam, dbl_bits(lm));
+}
+
 // elements [e_begin, e_end): one CTA per EPB elements; each thread owns whole
 // lines, so a pass updates its lines in place (no other thread touches them).
 // MODE 0: out = A^3 in. MODE 1 (LAM): no output; lambda_max = max(|u| + a)
@@ -92,18 +110,7 @@ __global__ void __launch_bounds__(ConvCfg<N>::THREADS)
     conv_passes<N, true, true>(O.A, S, out, e0, nb);
     conv_passes<N, false, true>(O.B, S, out, e0, nb);
   }
-  if (LAM) {
-    double lm = 0.0;
-    for (int it = tid; it < nb * N3; it += nthr) {
-      const int b = it / N3, q = it - b * N3;
-      double uu[NS];
-#pragma unroll
-      for (int s = 0; s < NS; ++s) uu[s] = S[(b * 5 + s) * N3 + q];
-      if (d_admissible(gamma, uu)) lm = fmax(lm, d_node_wavespeed(gamma, uu));
-    }
-    for (int o = 16; o > 0; o >>= 1) lm = fmax(lm, __shfl_xor_sync(0xffffffffu, lm, o));
-    if ((tid & 31) == 0 && lm > 0.0) atomicMax(lam, dbl_bits(lm));
-  }
+  if (LAM) conv_lambda<N>(S, nb, gamma, lam);
 }
 
 }  // namespace nsfr_b200

@@ -17,6 +17,7 @@
 // Stage 0 is a plain residual (dU/dt into `out`, optional -v_hat . R); stages
 // 1-3 accumulate acc and project u_{s+1}; stage 4 writes u_{n+1} and projects it.
 #pragma once
+#include "kernel_convert.cuh"
 #include "kernel_project.cuh"
 #include "physics.cuh"
 
@@ -34,6 +35,8 @@ struct UpdParams {
   const double* dt;    // device scalar
   int stage;
   ProjParams pj;       // projection of u_{s+1} (pj.u unused); pj.err, pj.E shared
+  double* uhat_out;    // OUT (stage 4 of the streamed host step): Pi^3 u_{n+1} instead of the projection
+  unsigned long long* lam_out;  // OUT: adaptive_dt's lambda_max of chi^3 of that u_hat, or nullptr
 };
 
 template <int N>
@@ -50,6 +53,7 @@ template <int N>
 struct UpdOps {
   TailOps<N> t;
   ProjOps<N> p;
+  double chi[N * N];     // chi (OUT: lambda of the outgoing state)
 };
 
 template <int N>
@@ -153,7 +157,7 @@ __device__ __forceinline__ void upd_prefetch(const UpdParams& P, int e0, int tid
 // change): IDM: M = Pi~^T chi^T = I as well, so lift + first half of the WA
 // inverse reduce to the pointwise face injection and 1/(w J) (same fma order);
 // IDF: the RK stages also skip the final three (chi Pi~) passes.
-template <int N, bool IDM, bool IDF>
+template <int N, bool IDM, bool IDF, bool OUT>
 __device__ __forceinline__ void upd_batch(const UpdParams& P, const UpdOps<N>& O, int e0, double* sm) {
   using Cfg = UpdCfg<N>;
   constexpr int N2 = Cfg::N2, N3 = Cfg::N3, EPB = Cfg::EPB;
@@ -330,18 +334,29 @@ __device__ __forceinline__ void upd_batch(const UpdParams& P, const UpdOps<N>& O
   if (P.stage == 0) return;
   __syncthreads();
   PHASE_MARK(10);
+  if constexpr (OUT) {
+    // the state leaves for the host: u_hat = Pi^3 u_{n+1} (kernel_convert's
+    // passes, same bits as k_convert_lines) and adaptive_dt's lambda of it,
+    // instead of a projection the next (uploaded) state would replace
+    conv_passes<N, true, true>(O.p.proj, R0, P.uhat_out, e0, nb);
+    if (P.lam_out) {
+      conv_passes<N, false, true>(O.chi, R0, nullptr, e0, nb);
+      conv_lambda<N>(R0, nb, P.pj.gamma, P.lam_out);
+    }
+    return;
+  }
   proj_core<N>(P.pj, O.p, e0, nb, R0, R1, R2, R3);
 }
 
 // One batch per CTA with look-ahead L2 prefetch (see k_residual).
-template <int N, bool IDM = false, bool IDF = false>
+template <int N, bool IDM = false, bool IDF = false, bool OUT = false>
 __global__ void __launch_bounds__(UpdCfg<N>::THREADS, UpdCfg<N>::MINB)
     k_update(UpdParams P, UpdOps<N> O, int ahead) {
   extern __shared__ __align__(128) double sm[];
   constexpr int EPB = UpdCfg<N>::EPB;
   const long long pe = P.pj.e_begin + (static_cast<long long>(blockIdx.x) + ahead) * EPB;
   if (pe < P.pj.E) upd_prefetch<N>(P, static_cast<int>(pe), threadIdx.x);
-  upd_batch<N, IDM, IDF>(P, O, P.pj.e_begin + blockIdx.x * EPB, sm);
+  upd_batch<N, IDM, IDF, OUT>(P, O, P.pj.e_begin + blockIdx.x * EPB, sm);
 }
 
 }  // namespace nsfr_b200

@@ -108,6 +108,10 @@ int set_attrs(nsfr_gpu_ctx* ctx) {
                             UpdCfg<N>::SMEM));
     CK(cudaFuncSetAttribute(k_update<N, true, true>, cudaFuncAttributeMaxDynamicSharedMemorySize,
                             UpdCfg<N>::SMEM));
+    CK(cudaFuncSetAttribute(k_update<N, false, false, true>, cudaFuncAttributeMaxDynamicSharedMemorySize,
+                            UpdCfg<N>::SMEM));
+    CK(cudaFuncSetAttribute(k_update<N, true, true, true>, cudaFuncAttributeMaxDynamicSharedMemorySize,
+                            UpdCfg<N>::SMEM));
     AttrsDone<N>::mask.fetch_or(bit);
   }
   int sms = 0, bp = 0, br = 0, bu = 0;
@@ -181,6 +185,7 @@ template <int N>
 UpdOps<N> upd_ops(const nsfr_gpu_ctx* ctx, int stage) {
   const DevTables& t = ctx->htab;
   UpdOps<N> u{};
+  for (int i = 0; i < N * N; ++i) u.chi[i] = t.interp[i];
   TailOps<N>& o = u.t;
   for (int a = 0; a < N; ++a)
     for (int i = 0; i < N; ++i) {
@@ -286,8 +291,11 @@ int launch_residual(nsfr_gpu_ctx* ctx, int km, int ea, int eb) {
 
 // stage 0: dU/dt (+ entropy change); stages 1-4: RK update and projection of
 // the next stage state (lambda_max after stage 4)
+// uhat_out (stage 4 only): write Pi^3 u_{n+1} there (and adaptive_dt's lambda
+// into lam_out when given) instead of projecting u_{n+1}
 template <int N>
-int launch_update(nsfr_gpu_ctx* ctx, int stage, bool entropy, const double* vhat, int ea, int eb) {
+int launch_update(nsfr_gpu_ctx* ctx, int stage, bool entropy, const double* vhat, int ea, int eb,
+                  double* uhat_out, unsigned long long* lam_out) {
   UpdParams P{};
   P.vol = ctx->d_vol;
   P.facc = ctx->d_facc;
@@ -303,10 +311,18 @@ int launch_update(nsfr_gpu_ctx* ctx, int stage, bool entropy, const double* vhat
   P.pj.vhat = nullptr;
   P.pj.e_begin = ea;
   P.pj.E = range_end(ctx, eb);
+  P.uhat_out = uhat_out;
+  P.lam_out = lam_out;
   if (int rc = set_attrs<N>(ctx)) return rc;
   const int grid = (P.pj.E - ea + UpdCfg<N>::EPB - 1) / UpdCfg<N>::EPB;
   ev_begin(ctx, 3);
-  if (ctx->chi_pi_identity && stage > 0)
+  if (uhat_out && ctx->chi_pi_identity)
+    k_update<N, true, true, true><<<grid, UpdCfg<N>::THREADS, UpdCfg<N>::SMEM, ctx->st>>>(
+        P, upd_ops<N>(ctx, stage), ctx->ahead_upd);
+  else if (uhat_out)
+    k_update<N, false, false, true><<<grid, UpdCfg<N>::THREADS, UpdCfg<N>::SMEM, ctx->st>>>(
+        P, upd_ops<N>(ctx, stage), ctx->ahead_upd);
+  else if (ctx->chi_pi_identity && stage > 0)
     k_update<N, true, true><<<grid, UpdCfg<N>::THREADS, UpdCfg<N>::SMEM, ctx->st>>>(
         P, upd_ops<N>(ctx, stage), ctx->ahead_upd);
   else if (ctx->chi_pi_identity && !entropy)
@@ -341,8 +357,8 @@ int residual(nsfr_gpu_ctx* ctx, int km = 0, int ea = 0, int eb = -1) {
 }
 // entropy: stage-0 diagnostic -vhat . R, with vhat = v_hat (default) or the given coefficients
 int update(nsfr_gpu_ctx* ctx, int stage, bool entropy, const double* vhat = nullptr, int ea = 0,
-           int eb = -1) {
-  NSFR_DISPATCH(launch_update, (ctx, stage, entropy, vhat, ea, eb));
+           int eb = -1, double* uhat_out = nullptr, unsigned long long* lam_out = nullptr) {
+  NSFR_DISPATCH(launch_update, (ctx, stage, entropy, vhat, ea, eb, uhat_out, lam_out));
 }
 
 // ---- conservative DG (kernel_dg.cuh) ------------------------------------------
@@ -1401,15 +1417,13 @@ static int rk4_step_host_impl(nsfr_gpu_ctx* ctx, const double* u_in, double* u_o
     }
     const int stage = (L + 1) / 2;
     if (L & 1) return residual(ctx, 0, e0, e1);
-    if (int rc = update(ctx, stage, false, nullptr, e0, e1)) return rc;
-    if (stage < 4) return NSFR_OK;
-    // u_{n+1} of this chunk is final: Pi^3 into the dead accumulator (and
-    // adaptive_dt's lambda of exactly those bytes, same pass), download
-    if (dt_next) {
-      if (int rc = lam_of_uhat(ctx, ctx->d_un, e0, e1, ctx->d_acc)) return rc;
-    } else if (int rc = convert_range(ctx, ctx->d_un, ctx->d_acc, false, e0, e1)) {
+    if (stage < 4) return update(ctx, stage, false, nullptr, e0, e1);
+    // stage 4: u_{n+1} of this chunk is final; K3 writes Pi^3 u_{n+1} into the
+    // dead accumulator (and adaptive_dt's lambda of exactly those bytes)
+    // instead of projecting it, then the download
+    if (int rc = update(ctx, 4, false, nullptr, e0, e1, ctx->d_acc,
+                        dt_next ? &ctx->d_step->lam_out_bits : nullptr))
       return rc;
-    }
     CK(cudaEventRecord(ctx->chunk_ev[nch + c], ctx->st));
     CK(cudaStreamWaitEvent(ctx->st_d2h, ctx->chunk_ev[nch + c], 0));
     if (!nocopy)
@@ -1484,7 +1498,7 @@ static int rk4_step_host_impl(nsfr_gpu_ctx* ctx, const double* u_in, double* u_o
   CK(cudaStreamSynchronize(ctx->st_d2h));
   CK(cudaStreamSynchronize(ctx->st_copy));
   if (int rc = sync_check(ctx)) return rc;
-  ctx->proj_valid = true;  // K3 of stage 4 left the projection (and lambda) of u_{n+1}
+  ctx->proj_valid = false;  // K3 of stage 4 wrote u_hat instead of projecting u_{n+1}
   if (dt_used) *dt_used = ctx->h_step->dt;
   return dt_next ? finish_dt_next(ctx, dt_next) : NSFR_OK;
 }
