@@ -11,6 +11,7 @@
 // apply_operator_dir sumfac.cpp:7-55). The 1D operators travel in the kernel
 // parameter (constant) bank, so each FMA takes its coefficient as an operand.
 #pragma once
+#include "kernel_convert.cuh"
 #include "physics.cuh"
 #include "setup_kernels.cuh"
 
@@ -28,6 +29,7 @@ struct ProjParams {
   int E, m, nz;          // E: end of the launched element range [e_begin, E) (the slab by default)
   double gamma;
   int e_begin;           // first element of the launched range (a multiple of 8)
+  double* uq_out;        // K1 from u_hat (streamed host step): u is u_hat, chi^3 u goes here
 };
 
 template <int N>
@@ -36,6 +38,7 @@ struct ProjOps {
   double bsol[2 * N];    // bound_sol rows at xi = -1, +1
   double bp[2 * N];      // bound_sol_side Pi: face trace rows applied to nodal v (chi Pi = I)
   double c35;            // gm1^(1/gm1) when gamma/(gamma-1) == 7/2 (closed-form u(v)), else 0
+  double chi[N * N];     // chi (nq x np): K1 from u_hat, K3's outgoing lambda
 };
 
 template <int N>
@@ -217,7 +220,7 @@ __device__ __forceinline__ void proj_core(const ProjParams& P, const ProjOps<N>&
   PHASE_MARK(13);
 }
 
-template <int N>
+template <int N, bool HAT>
 __device__ __forceinline__ void proj_batch(const ProjParams& P, const ProjOps<N>& O, int e0, double* sm) {
   using Cfg = ProjCfg<N>;
   constexpr int N3 = Cfg::N3, EPB = Cfg::EPB;
@@ -233,12 +236,15 @@ __device__ __forceinline__ void proj_batch(const ProjParams& P, const ProjOps<N>
   __syncthreads();
   stage_wait(&bar);
   __syncthreads();
+  // HAT: the block is u_hat (just uploaded): u_q = chi^3 u_hat in place, also
+  // to P.uq_out (kernel_convert's passes: the bits of k_convert_lines)
+  if constexpr (HAT) conv_passes<N, true, true>(O.chi, A, P.uq_out, e0, nb);
   proj_core<N>(P, O, e0, nb, A, B, V, V + EPB * 5 * N3);
 }
 
 // One batch per CTA; L2 prefetch of the input block of the CTA `ahead`
 // (= #resident CTAs) later (see k_residual).
-template <int N>
+template <int N, bool HAT = false>
 __global__ void __launch_bounds__(ProjCfg<N>::THREADS) k_project(ProjParams P, ProjOps<N> O, int ahead) {
   extern __shared__ __align__(128) double sm[];
   constexpr int EPB = ProjCfg<N>::EPB, N3 = N * N * N;
@@ -248,7 +254,7 @@ __global__ void __launch_bounds__(ProjCfg<N>::THREADS) k_project(ProjParams P, P
     const int e0 = P.e_begin + pb * EPB, nb = min(EPB, P.E - e0);
     l2_prefetch(P.u + (size_t)e0 * 5 * N3, (size_t)nb * 5 * N3 * sizeof(double));
   }
-  proj_batch<N>(P, O, P.e_begin + blockIdx.x * EPB, sm);
+  proj_batch<N, HAT>(P, O, P.e_begin + blockIdx.x * EPB, sm);
 }
 
 }  // namespace nsfr_b200

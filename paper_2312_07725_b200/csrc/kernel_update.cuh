@@ -52,8 +52,7 @@ struct TailOps {
 template <int N>
 struct UpdOps {
   TailOps<N> t;
-  ProjOps<N> p;
-  double chi[N * N];     // chi (OUT: lambda of the outgoing state)
+  ProjOps<N> p;          // p.chi: OUT's lambda of the outgoing state
 };
 
 template <int N>
@@ -340,7 +339,7 @@ __device__ __forceinline__ void upd_batch(const UpdParams& P, const UpdOps<N>& O
     // instead of a projection the next (uploaded) state would replace
     conv_passes<N, true, true>(O.p.proj, R0, P.uhat_out, e0, nb);
     if (P.lam_out) {
-      conv_passes<N, false, true>(O.chi, R0, nullptr, e0, nb);
+      conv_passes<N, false, true>(O.p.chi, R0, nullptr, e0, nb);
       conv_lambda<N>(R0, nb, P.pj.gamma, P.lam_out);
     }
     return;

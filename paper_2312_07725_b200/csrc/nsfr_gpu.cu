@@ -100,6 +100,7 @@ int set_attrs(nsfr_gpu_ctx* ctx) {
   const unsigned bit = 1u << (ctx->s.device & 31);
   if (!(AttrsDone<N>::mask.load() & bit)) {
     CK(cudaFuncSetAttribute(k_project<N>, cudaFuncAttributeMaxDynamicSharedMemorySize, ProjCfg<N>::SMEM));
+    CK(cudaFuncSetAttribute(k_project<N, true>, cudaFuncAttributeMaxDynamicSharedMemorySize, ProjCfg<N>::SMEM));
     CK(cudaFuncSetAttribute(k_residual<N>, cudaFuncAttributeMaxDynamicSharedMemorySize, ResCfg<N>::SMEM));
     CK(cudaFuncSetAttribute(k_residual<N, 1>, cudaFuncAttributeMaxDynamicSharedMemorySize, ResCfg<N>::SMEM));
     CK(cudaFuncSetAttribute(k_residual<N, 2>, cudaFuncAttributeMaxDynamicSharedMemorySize, ResCfg<N>::SMEM));
@@ -153,7 +154,10 @@ template <int N>
 ProjOps<N> proj_ops(const nsfr_gpu_ctx* ctx) {
   const DevTables& t = ctx->htab;
   ProjOps<N> o{};
-  for (int i = 0; i < N * N; ++i) o.proj[i] = t.proj[i];
+  for (int i = 0; i < N * N; ++i) {
+    o.proj[i] = t.proj[i];
+    o.chi[i] = t.interp[i];
+  }
   for (int i = 0; i < 2 * N; ++i) o.bsol[i] = t.bsol[i];
   for (int side = 0; side < 2; ++side)
     for (int a = 0; a < N; ++a) {  // (bound_sol Pi)[side][a]; Pi is np x nq
@@ -185,7 +189,6 @@ template <int N>
 UpdOps<N> upd_ops(const nsfr_gpu_ctx* ctx, int stage) {
   const DevTables& t = ctx->htab;
   UpdOps<N> u{};
-  for (int i = 0; i < N * N; ++i) u.chi[i] = t.interp[i];
   TailOps<N>& o = u.t;
   for (int a = 0; a < N; ++a)
     for (int i = 0; i < N; ++i) {
@@ -237,16 +240,22 @@ ProjParams proj_params(nsfr_gpu_ctx* ctx, const double* u, bool want_lam) {
 // multiple of 8 so every batch's TMA blocks stay 16-byte aligned.
 int range_end(const nsfr_gpu_ctx* ctx, int eb) { return eb < 0 ? ctx->E : eb; }
 
+// uq_out: u is u_hat; chi^3 u lands there and is projected (streamed upload)
 template <int N>
-int launch_project(nsfr_gpu_ctx* ctx, const double* u, bool want_lam, int ea, int eb) {
+int launch_project(nsfr_gpu_ctx* ctx, const double* u, bool want_lam, int ea, int eb, double* uq_out) {
   if (int rc = set_attrs<N>(ctx)) return rc;
   ProjParams P = proj_params(ctx, u, want_lam);
   P.e_begin = ea;
   P.E = range_end(ctx, eb);
+  P.uq_out = uq_out;
   const int grid = (P.E - ea + ProjCfg<N>::EPB - 1) / ProjCfg<N>::EPB;
   ev_begin(ctx, 1);
-  k_project<N><<<grid, ProjCfg<N>::THREADS, ProjCfg<N>::SMEM, ctx->st>>>(P, proj_ops<N>(ctx),
-                                                                         ctx->ahead_proj);
+  if (uq_out)
+    k_project<N, true><<<grid, ProjCfg<N>::THREADS, ProjCfg<N>::SMEM, ctx->st>>>(P, proj_ops<N>(ctx),
+                                                                               ctx->ahead_proj);
+  else
+    k_project<N><<<grid, ProjCfg<N>::THREADS, ProjCfg<N>::SMEM, ctx->st>>>(P, proj_ops<N>(ctx),
+                                                                           ctx->ahead_proj);
   ev_end(ctx);
   ++ctx->launches;
   CK(cudaGetLastError());
@@ -348,8 +357,8 @@ int launch_update(nsfr_gpu_ctx* ctx, int stage, bool entropy, const double* vhat
   ctx->msg = "unsupported p";                  \
   return NSFR_E_DIM
 
-int project(nsfr_gpu_ctx* ctx, const double* u, bool lam, int ea = 0, int eb = -1) {
-  NSFR_DISPATCH(launch_project, (ctx, u, lam, ea, eb));
+int project(nsfr_gpu_ctx* ctx, const double* u, bool lam, int ea = 0, int eb = -1, double* uq_out = nullptr) {
+  NSFR_DISPATCH(launch_project, (ctx, u, lam, ea, eb, uq_out));
 }
 // km: 0 the residual, 1 / 2 kinetic-energy diagnostic rows (kernel_residual.cuh)
 int residual(nsfr_gpu_ctx* ctx, int km = 0, int ea = 0, int eb = -1) {
@@ -1410,10 +1419,10 @@ static int rk4_step_host_impl(nsfr_gpu_ctx* ctx, const double* u_in, double* u_o
       CK(cudaStreamWaitEvent(ctx->st, ctx->chunk_ev[c], 0));
       if (nocopy) {  // same conversion cost, the device state stays the input
         if (int rc = convert_range(ctx, ctx->d_un, ctx->d_rhs, true, e0, e1)) return rc;
-      } else if (int rc = convert_range(ctx, ctx->d_acc, ctx->d_un, true, e0, e1)) {
-        return rc;
+        return project(ctx, ctx->d_un, !fixed, e0, e1);
       }
-      return project(ctx, ctx->d_un, !fixed, e0, e1);
+      // K1 straight from the uploaded u_hat: u_q = chi^3 u_hat into the state and projected
+      return project(ctx, ctx->d_acc, !fixed, e0, e1, ctx->d_un);
     }
     const int stage = (L + 1) / 2;
     if (L & 1) return residual(ctx, 0, e0, e1);
