@@ -93,7 +93,6 @@ __global__ void __launch_bounds__(ConvCfg<N>::THREADS)
   extern __shared__ __align__(128) double S[];
   const int e0 = e_begin + blockIdx.x * EPB;
   const int nb = min(EPB, e_end - e0);
-  const int tid = threadIdx.x, nthr = blockDim.x;
   __shared__ unsigned long long bar;
   {
     const StageBlock blk[1] = {{S, in + (size_t)e0 * 5 * N3, nb * 5 * N3}};
