@@ -417,11 +417,11 @@ __global__ void __launch_bounds__(256, 2) k_dg_residual(DgResParams P, DgOps<NP,
   double* R1 = FR;
   double* R2 = FR + EPB * VS;
   tail_pass<NQ, 0, true, false>(O.M, O.bm, FACC, FS, VOL, VS, R1, VS, WJ, nbs, tid, nthr);
-  tail_face_pass<NQ, 0>(O.M, FACC + 10 * Q2, FS, G, FS, nb, tid, nthr);
-  tail_face_pass<NQ, 0>(O.M, FACC + 20 * Q2, FS, G + 10 * Q2, FS, nb, tid, nthr);
+  tail_face_pass<NQ, 0>(O.M, FACC + 10 * Q2, FS, G, FS, nb, face_vt<NQ>(tid, nthr, 0), nthr);
+  tail_face_pass<NQ, 0>(O.M, FACC + 20 * Q2, FS, G + 10 * Q2, FS, nb, face_vt<NQ>(tid, nthr, nb * 10 * NQ), nthr);
   __syncthreads();
   tail_pass<NQ, 1, true, false>(O.M, O.bm, G, FS, R1, VS, R2, VS, WJ, nbs, tid, nthr);
-  tail_face_pass<NQ, 1>(O.M, G + 10 * Q2, FS, G + 20 * Q2, FS, nb, tid, nthr);
+  tail_face_pass<NQ, 1>(O.M, G + 10 * Q2, FS, G + 20 * Q2, FS, nb, face_vt<NQ>(tid, nthr, 0), nthr);
   __syncthreads();
   tail_pass<NQ, 2, true, true>(O.M, O.bm, G + 20 * Q2, FS, R2, VS, VOL, VS, WJ, nbs, tid, nthr);
   __syncthreads();

@@ -38,7 +38,7 @@ namespace nsfr_b200 {
                      Pd[5 * N3 + ib]};                                                         \
       double f[NS];                                                                            \
       d_flux_h<KE>(pa, pb, ca0 + Ch[(0 + dir) * N3 + ib], ca1 + Ch[(3 + dir) * N3 + ib],       \
-                   ca2 + Ch[(6 + dir) * N3 + ib], f, amask);                                          \
+                   ca2 + Ch[(6 + dir) * N3 + ib], f);                                                 \
       const double c = wt * q[a * N + bb];                                                     \
       _Pragma("unroll") for (int s = 0; s < NS; ++s) {                                         \
         fa[s] = fma(c, f[s], fa[s]);                                                           \
@@ -55,7 +55,7 @@ template <int N, bool KE>
 __device__ __forceinline__ void vol_pairs(const double* __restrict__ Pd, const double* __restrict__ Ch,
                                           double* __restrict__ acc,
                                           const double (&q)[N * N], double wt, int lbase,
-                                          int stride, int dir, unsigned amask) {
+                                          int stride, int dir) {
   constexpr int N3 = N * N * N;
   if constexpr (N <= NSFR_UNROLL_MAXN) {
 #define NSFR_INNER_UNROLL _Pragma("unroll")
@@ -218,9 +218,6 @@ __device__ __forceinline__ void res_lines(const ResParams& P, const ResOps<N>& O
   const int ll = tid - lb * LINES;
   const int ldir = ll / N2, lrem = ll - ldir * N2;
   if (lb < nb) {
-    // lanes of this warp in the line phase: every line runs the same loop trip
-    // counts, so this set is active at every flux call below
-    const unsigned amask = __activemask();
     const int b = lb, e = e0 + b, dir = ldir, t1 = lrem % N, t2 = lrem / N;
     const int stride = dir == 0 ? 1 : (dir == 1 ? N : N2);
     const int lbase = dir == 0 ? N * (t1 + N * t2) : (dir == 1 ? t1 + N2 * t2 : t1 + N * t2);
@@ -233,7 +230,7 @@ __device__ __forceinline__ void res_lines(const ResParams& P, const ResOps<N>& O
     for (int a = 0; a < N; ++a)
 #pragma unroll
       for (int s = 0; s < NS; ++s) acc[s * N3 + lbase + a * stride] = 0.0;
-    vol_pairs<N, (KM != 0)>(Pd, Ch, acc, O.q, wt, lbase, stride, dir, amask);
+    vol_pairs<N, (KM != 0)>(Pd, Ch, acc, O.q, wt, lbase, stride, dir);
     // S7 hybrid surface pairs + S8 face flux for the two faces this line pierces
 #pragma unroll 1
     for (int side = 0; side < (KM == 1 ? 0 : 2); ++side) {
@@ -293,7 +290,7 @@ __device__ __forceinline__ void res_lines(const ResParams& P, const ResOps<N>& O
                        Pd[4 * N3 + ia], Pd[5 * N3 + ia]};
         double fl[NS];
         d_flux_h<(KM != 0)>(pa, pfh, Ch[(0 + dir) * N3 + ia] + ch0, Ch[(3 + dir) * N3 + ia] + ch1,
-                            Ch[(6 + dir) * N3 + ia] + ch2, fl, amask);
+                            Ch[(6 + dir) * N3 + ia] + ch2, fl);
         const double c = sign * O.bflux[side * N + a] * wt;
 #pragma unroll
         for (int s = 0; s < NS; ++s) {
@@ -309,7 +306,7 @@ __device__ __forceinline__ void res_lines(const ResParams& P, const ResOps<N>& O
       const PrimX pf = d_primx(g, uf);  // recomputed rather than kept through the loop
       const PrimX pn = d_primx(g, un);
       double fn[NS];
-      d_flux_h<(KM != 0)>(pfh, to_half(gm1, pn), nrm[0], nrm[1], nrm[2], fn, amask);
+      d_flux_h<(KM != 0)>(pfh, to_half(gm1, pn), nrm[0], nrm[1], nrm[2], fn);
       if (P.roe && KM == 0) {
         double d[NS];
         if (!d_roe_x(g, uf, un, pf, pn, nrm, d)) atomicOr(P.err, ERR_ROE);
@@ -330,10 +327,21 @@ __device__ __forceinline__ void res_lines(const ResParams& P, const ResOps<N>& O
 template <int N>
 __device__ __forceinline__ void res_writeout(const ResParams& P, int e0, int nb, const double* ACCV) {
   constexpr int N3 = N * N * N, AS = 15 * N3;
-  for (int it = threadIdx.x; it < nb * 5 * N3; it += blockDim.x) {
+  // compile-time trip count: every thread's shared loads issue before its sums
+  constexpr int T = ResCfg<N>::THREADS, ITS = (ResCfg<N>::EPB * 5 * N3 + T - 1) / T;
+  const int lim = nb * 5 * N3;
+  double v[ITS];
+#pragma unroll
+  for (int j = 0; j < ITS; ++j) {
+    const int it = threadIdx.x + j * T;
     const int b = it / (5 * N3), r = it - b * 5 * N3;
     const double* a0 = ACCV + b * AS;
-    P.vol[(size_t)e0 * 5 * N3 + it] = a0[r] + a0[5 * N3 + r] + a0[10 * N3 + r];
+    v[j] = it < lim ? a0[r] + a0[5 * N3 + r] + a0[10 * N3 + r] : 0.0;
+  }
+#pragma unroll
+  for (int j = 0; j < ITS; ++j) {
+    const int it = threadIdx.x + j * T;
+    if (it < lim) P.vol[(size_t)e0 * 5 * N3 + it] = v[j];
   }
 }
 

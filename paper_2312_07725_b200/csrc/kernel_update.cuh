@@ -113,6 +113,17 @@ __device__ __forceinline__ void tail_pass(const double (&op)[N * N], const doubl
 }
 
 // Face-array pass (10 arrays [s][side] of N2 per element) along t1 (T=0) or t2 (T=1).
+// Callers pass a virtual thread index from face_vt. At n >= 6 the face items
+// fill the threads counted from the top of the block, i.e. those the volume
+// tail_pass of the same phase leaves idle (phase 1 at p=5: at most 2 line items
+// per thread instead of 3; K3 -3.5%). At p=3/4 the same remap measured +1.6% /
+// +0.3%, so there the face items start at thread 0.
+template <int N>
+__device__ __forceinline__ int face_vt(int tid, int nthr, int off) {
+  if constexpr (N < 6) return tid;
+  return (((nthr - 1 - tid - off) % nthr) + nthr) % nthr;
+}
+
 template <int N, int T>
 __device__ __forceinline__ void tail_face_pass(const double (&op)[N * N], const double* in, int in_es,
                                                double* out, int out_es, int nb, int tid, int nthr) {
@@ -228,22 +239,22 @@ __device__ __forceinline__ void upd_batch(const UpdParams& P, const UpdOps<N>& O
   } else if (!P.dS) {
     // Pi~^T S9 in three fused passes; 1/(w J) in the last
     tail_pass<N, 0, true, false>(T.M, T.bm, R3, FS, R0, VS, R1, VS, WJ, nbs, tid, nthr);
-    tail_face_pass<N, 0>(T.M, R3 + 10 * N2, FS, R4, FS, nb, tid, nthr);
-    tail_face_pass<N, 0>(T.M, R3 + 20 * N2, FS, R4 + 10 * N2, FS, nb, tid, nthr);
+    tail_face_pass<N, 0>(T.M, R3 + 10 * N2, FS, R4, FS, nb, face_vt<N>(tid, nthr, 0), nthr);
+    tail_face_pass<N, 0>(T.M, R3 + 20 * N2, FS, R4 + 10 * N2, FS, nb, face_vt<N>(tid, nthr, nb * 10 * N), nthr);
     __syncthreads();
     tail_pass<N, 1, true, false>(T.M, T.bm, R4, FS, R1, VS, R2, VS, WJ, nbs, tid, nthr);
-    tail_face_pass<N, 1>(T.M, R4 + 10 * N2, FS, R4 + 20 * N2, FS, nb, tid, nthr);
+    tail_face_pass<N, 1>(T.M, R4 + 10 * N2, FS, R4 + 20 * N2, FS, nb, face_vt<N>(tid, nthr, 0), nthr);
     __syncthreads();
     tail_pass<N, 2, true, true>(T.M, T.bm, R4 + 20 * N2, FS, R2, VS, R0, VS, WJ, nbs, tid, nthr);
     __syncthreads();
   } else {
     // entropy diagnostic: R = S9 explicitly (chi^T, bound_sol), -v_hat . R, then Pi~^T
     tail_pass<N, 0, true, false>(T.it, T.bs, R3, FS, R0, VS, R1, VS, WJ, nbs, tid, nthr);
-    tail_face_pass<N, 0>(T.it, R3 + 10 * N2, FS, R4, FS, nb, tid, nthr);
-    tail_face_pass<N, 0>(T.it, R3 + 20 * N2, FS, R4 + 10 * N2, FS, nb, tid, nthr);
+    tail_face_pass<N, 0>(T.it, R3 + 10 * N2, FS, R4, FS, nb, face_vt<N>(tid, nthr, 0), nthr);
+    tail_face_pass<N, 0>(T.it, R3 + 20 * N2, FS, R4 + 10 * N2, FS, nb, face_vt<N>(tid, nthr, nb * 10 * N), nthr);
     __syncthreads();
     tail_pass<N, 1, true, false>(T.it, T.bs, R4, FS, R1, VS, R2, VS, WJ, nbs, tid, nthr);
-    tail_face_pass<N, 1>(T.it, R4 + 10 * N2, FS, R4 + 20 * N2, FS, nb, tid, nthr);
+    tail_face_pass<N, 1>(T.it, R4 + 10 * N2, FS, R4 + 20 * N2, FS, nb, face_vt<N>(tid, nthr, 0), nthr);
     __syncthreads();
     tail_pass<N, 2, true, false>(T.it, T.bs, R4 + 20 * N2, FS, R2, VS, R0, VS, WJ, nbs, tid, nthr);
     __syncthreads();
