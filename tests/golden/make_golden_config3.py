@@ -4,8 +4,8 @@
 (p = 4: ~763 steps; p = 5: ~916 steps). Run here (needs oracle/_ref):
     python tests/golden/make_golden_config3.py 4 [5] [--t-final T]   (hours on 8 cores)
 Merges {"p4": {...}, "p5": {...}} into tests/golden/config3.json. The p = 5
-entry was made with --t-final 1.0 (the full t_f = 2 run is ~5 h of the
-reference build on 8 cores); the entry records its own t_target.
+entry was made with --t-final 0.2 (~92 steps, ~26 min; the full t_f = 2 run is
+~5 h of the reference build on 8 cores); the entry records its own t_target.
 """
 import json
 import os

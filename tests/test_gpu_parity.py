@@ -206,7 +206,7 @@ def test_config3_to_final_time(p):
     (~763 steps at p=4, ~916 at p=5); final L2(rho), L2(p) within 1e-10
     relative of the reference build (tests/golden/config3.json,
     tests/golden/make_golden_config3.py; the p=4 run took ~2 h on 8 cores, the
-    p=5 golden stops at its recorded t_target = 1, ~458 steps)."""
+    p=5 golden stops at its recorded t_target = 0.2, ~92 steps)."""
     with open(os.path.join(GOLD, "config3.json")) as f:
         gold = json.load(f).get(f"p{p}")
     if gold is None:
