@@ -10,9 +10,15 @@ per GPU, NCCL face-halo exchange + lambda_max allreduce per step).
     python bench.py [--gpus N --steps K --warmup W] [--impl reference]
     torchrun --nproc-per-node N --master-addr 127.0.0.1 bench.py --gpus N ...
 
+`python bench.py --gpus N` (N > 1) outside torchrun re-launches itself under
+`torch.distributed.run` with N ranks; every rank prints the NCCL communicator
+it got (size, rank, device) to stderr, and rank 0's JSON carries the list.
+
 Prints ONE JSON line on rank 0. The CPU legs (cpu_baseline and --impl
 reference) run the reference's own compiled primitives (oracle/_ref, built
-from /root/reference/proj/src) under the residual glue, on a bounded sample.
+from /root/reference/proj/src) under the residual glue, on a bounded sample:
+the periodic 128x128x16 z-slab of the 128^3 box, one RHS
+per sample, median of the samples, scaled per element to 128^3 (extrapolation).
 """
 from __future__ import annotations
 
@@ -31,14 +37,14 @@ ROOT = os.path.dirname(os.path.abspath(__file__))
 sys.path.insert(0, ROOT)
 sys.path.insert(0, os.path.join(ROOT, "tools"))
 
-from flop_model import bytes_per_element, per_element  # noqa: E402
+from flop_model import bytes_per_element, per_element, survey_per_element  # noqa: E402
 
 METRIC = "RHS DOF-updates/sec (fp64, 3D Euler NSFR)"
 UNIT = "DOF-updates/s"
 P_DEG, M = 4, 128
 C_PLUS4 = 0.5 * 4.67e-5
 WORKLOAD = "isentropic-vortex-128^3-p4-c_plus-EC+Roe-RK4"
-CPU_SAMPLE_M = 24  # bounded CPU sample: same p/c/flux on a periodic 24^3 box
+CPU_SLAB = 16  # bounded CPU sample: planes [0, 16) of the 128^3 box, its own halos (periodic slab)
 
 
 def read_peaks():
@@ -112,24 +118,47 @@ def cpu_model() -> str:
     return "unknown"
 
 
-def cpu_reference_run(steps: int, warmup: int, threads: int):
-    """Reference CPU path (oracle/_ref) RK4 steps on the bounded sample; returns
-    (DOF-updates/s, seconds per step, kind, cores)."""
-    sys.path.insert(0, os.path.join(ROOT, "tests"))
-    from oracle_lib import LIBS, Config, CpuSolver  # CPU baseline leg only
-    kind = "ref" if os.path.exists(LIBS["ref"][0]) else "oracle"
-    cfg = Config(p=P_DEG, m=CPU_SAMPLE_M, c1d=C_PLUS4, case="vortex", roe=True, workers=threads)
-    s = CpuSolver(kind, cfg)
-    u = s.initial_state()
-    dt = 0.1 * s.dx() / s.max_wavespeed(u)
-    for _ in range(warmup):
-        s.rk4_step(u, dt)
-    t0 = time.perf_counter()
-    for _ in range(steps):
-        s.rk4_step(u, dt)
-    sec = (time.perf_counter() - t0) / steps
-    dof = CPU_SAMPLE_M ** 3 * (P_DEG + 1) ** 3 * 5
-    return 4 * dof / sec, sec, ("reference" if kind == "ref" else "port"), threads
+class CpuSlab:
+    """The reference's CPU path (oracle/_ref) on the periodic 128x128x16 z-slab
+    of the bench box: same p / c_+ / EC+Roe / metrics as the GPU workload. The
+    slab's halo planes are its own end planes (wrapped), taken once from the
+    initial state, so every sample is one full RHS of 262,144 elements."""
+
+    def __init__(self, threads: int):
+        sys.path.insert(0, os.path.join(ROOT, "tests"))
+        from oracle_lib import LIBS, Config, CpuSolver  # CPU baseline legs only
+        self.kind = "ref" if os.path.exists(LIBS["ref"][0]) else "oracle"
+        self.threads = threads
+        t0 = time.perf_counter()
+        self.s = CpuSolver(self.kind, Config(p=P_DEG, m=M, c1d=C_PLUS4, case="vortex", roe=True,
+                                             k0=0, k1=CPU_SLAB, workers=threads))
+        self.u = self.s.initial_state()
+        lo, hi = self.s.boundary_traces(self.u)
+        self.halo_lo, self.halo_hi = hi, lo
+        self.setup_s = time.perf_counter() - t0
+        self.dof = M * M * CPU_SLAB * (P_DEG + 1) ** 3 * 5
+
+    def rhs_seconds(self) -> float:
+        t0 = time.perf_counter()
+        self.s.rhs(self.u, self.halo_lo, self.halo_hi)
+        return time.perf_counter() - t0
+
+    def sample(self, n: int, warmup: int = 1):
+        for _ in range(warmup):
+            self.rhs_seconds()
+        secs = [self.rhs_seconds() for _ in range(n)]
+        med = statistics.median(secs)
+        return self.dof / med, med, secs
+
+    def describe(self, n: int) -> str:
+        return (f"periodic {M}x{M}x{CPU_SLAB} z-slab of the {M}^3 box (262,144 elements, p=4, c_+, "
+                f"EC+Roe, the reference's metrics of those elements), one RHS per sample, median of "
+                f"{n} after 1 warm-up, {self.threads} threads; DOF-updates/s per element is the "
+                f"128^3 rate (extrapolation: the full box needs ~75 GB of reference metrics)")
+
+    @property
+    def kind_name(self) -> str:
+        return "reference" if self.kind == "ref" else "port"
 
 
 def run_reference_arm(args):
@@ -137,19 +166,36 @@ def run_reference_arm(args):
     if rank != 0:
         return
     threads = os.cpu_count() or 1
-    val, sec, kind, cores = cpu_reference_run(args.steps, args.warmup, threads)
-    sample = (f"periodic {CPU_SAMPLE_M}^3-element box, same p=4/c_+/EC+Roe/RK4 per-element work as "
-              f"128^3; {args.steps} RK4 steps after {args.warmup} warm-up")
+    cs = CpuSlab(threads)
+    val, med, secs = cs.sample(args.steps, warmup=args.warmup)
     print(json.dumps({
         "impl": "reference", "metric": METRIC, "value": val, "unit": UNIT, "n_gpus": args.gpus,
-        "steps": args.steps, "warmup": args.warmup, "ms_per_step": sec * 1e3,
+        "steps": args.steps, "warmup": args.warmup, "ms_per_step": med * 1e3,
         "higher_is_better": True, "scaling": "strong", "vs_baseline": None, "dtype": "f64",
         "data": "synthetic (analytic isentropic vortex IC)",
-        "config": {"workload": WORKLOAD, "p": P_DEG, "elements": f"{CPU_SAMPLE_M}^3 sample of 128^3"},
-        "cpu_baseline": {"value": val, "unit": UNIT, "cores": cores, "kind": kind, "sample": sample,
-                         "cpu_model": cpu_model()},
+        "config": {"workload": WORKLOAD, "p": P_DEG, "elements": f"{M}x{M}x{CPU_SLAB} slab of {M}^3",
+                   "step": "one RHS of the slab (median over steps)"},
+        "cpu_baseline": {"value": val, "unit": UNIT, "cores": threads, "kind": cs.kind_name,
+                         "sample": cs.describe(args.steps), "cpu_model": cpu_model(),
+                         "setup_s": cs.setup_s, "rhs_s": secs},
         "e2e": {"value": val, "unit": UNIT, "h2d_bytes_per_step": 0, "d2h_bytes_per_step": 0},
     }), flush=True)
+
+
+def free_port() -> int:
+    import socket
+    with socket.socket() as sk:
+        sk.bind(("127.0.0.1", 0))
+        return sk.getsockname()[1]
+
+
+def relaunch_command(args, argv) -> list[str] | None:
+    """`bench.py --gpus N` (N > 1) outside a torchrun environment: the command
+    that re-runs it with N ranks (one process per GPU), else None."""
+    if args.impl != "b200" or args.gpus <= 1 or "WORLD_SIZE" in os.environ:
+        return None
+    return [sys.executable, "-m", "torch.distributed.run", "--nnodes=1", f"--nproc-per-node={args.gpus}",
+            "--master-addr", "127.0.0.1", f"--master-port={free_port()}", os.path.abspath(__file__), *argv]
 
 
 def run_gpu_arm(args):
@@ -157,7 +203,9 @@ def run_gpu_arm(args):
     import paper_2312_07725_b200 as pkg
 
     world, rank, local = dist_env()
-    assert world == args.gpus or world == 1, "launch N>1 under torchrun with --gpus N"
+    if world != args.gpus:
+        raise SystemExit(f"bench.py: WORLD_SIZE={world} but --gpus {args.gpus}: launch N>1 with "
+                         f"`python bench.py --gpus N` (it starts N ranks) or under torchrun")
     device = local
     torch.cuda.set_device(device)
     nccl_id = None
@@ -170,8 +218,21 @@ def run_gpu_arm(args):
     cfg = pkg.SolverConfig(p=P_DEG, m=M, c1d=C_PLUS4, case="vortex", roe=True, device=device,
                            rank=rank, nranks=world)
     g = pkg.GpuSolver(cfg, nccl_id=nccl_id)
+    comm = {"rank": rank, "world": world, **g.comm_info()}
+    print(json.dumps({"nccl_comm": comm}), file=sys.stderr, flush=True)
+    if world > 1:
+        import torch.distributed as dist
+        comms = [None] * world
+        dist.all_gather_object(comms, comm)
+        bad = [c for c in comms if c["nccl_nranks"] != world]
+        if bad:
+            raise SystemExit(f"bench.py: NCCL communicator size != {world}: {bad}")
+    else:
+        comms = [comm]
     g.init_case()
-    fp64_peak = pkg.measure_fp64_peak(device)
+    fp64_peak, peak_mhz = pkg.measure_fp64_peak(device, with_clock=True)
+    sms = torch.cuda.get_device_properties(device).multi_processor_count
+    nominal = sms * 128 * peak_mhz * 1e6 / 1e12  # SMs x 64 DFMA/clk x 2 flop x measured clock
 
     def barrier():
         if world > 1:
@@ -237,8 +298,10 @@ def run_gpu_arm(args):
     state_bytes = host.nbytes
 
     fm = per_element(P_DEG)
+    sv = survey_per_element(P_DEG)["flops_total"]
     ne_local = g.ne
     k2_tflops = fm["flops_k2"] * ne_local / (k2_ms * 1e-3) / 1e12
+    step_rate = ne_local * 4 * args.steps / (ms_total * 1e-3) / 1e12  # element-RHS per s / 1e12
     traffic = None
     prof = os.path.join(ROOT, "profiles", "k_residual_p4_traffic.json")
     if os.path.exists(prof):
@@ -257,13 +320,21 @@ def run_gpu_arm(args):
         "roofline": {"bound": "fp64", "achieved": k2_tflops, "peak": fp64_peak, "unit": "TFLOP/s",
                      "frac": k2_tflops / fp64_peak, "traffic": traffic,
                      "kernel": f"k_residual<{P_DEG + 1}>",
-                     "peak_source": "measured live: DFMA loop (nsfr_gpu_measure_fp64_peak); "
+                     "peak_source": "measured live: DFMA loop (nsfr_gpu_measure_fp64_peak_ex); "
                                     "MEASURED_PEAKS.json has no fp64 entry",
+                     "peak_sm_mhz": peak_mhz, "peak_nominal": nominal,
+                     "frac_nominal": k2_tflops / nominal,
                      "flops_per_element": fm["flops_k2"], "elements_per_launch": ne_local,
                      "launch_ms": k2_ms, "k3_launch_ms": k3_ms,
                      "k3_tflops": fm["flops_k3"] * ne_local / (k3_ms * 1e-3) / 1e12,
                      "step_frac": (fm["flops_total"] * ne_local * 4 * args.steps / (ms_total * 1e-3) / 1e12)
                      / fp64_peak,
+                     "step_frac_table": {
+                         "model_vs_measured": fm["flops_total"] * step_rate / fp64_peak,
+                         "model_vs_nominal": fm["flops_total"] * step_rate / nominal,
+                         "survey_vs_measured": sv * step_rate / fp64_peak,
+                         "survey_vs_nominal": sv * step_rate / nominal,
+                         "flops_model": fm["flops_total"], "flops_survey": sv},
                      "hbm_b_alg_gbs": bytes_per_element(P_DEG)["b_alg"] * ne_local / (
                          (k2_ms + k3_ms) * 1e-3) / 1e9,
                      "hbm_peak_gbs": read_peaks().get("hbm_gbs")},
@@ -275,14 +346,16 @@ def run_gpu_arm(args):
                 "in_step_adaptive_value": 4 * dof_total / e2e_barrier_sec,
                 "unpipelined_value": 4 * dof_total / e2e_plain_sec},
         "gpu_launches": int(launches),
+        "nccl": comms,
     }
     if rank == 0 and world == 1 and not args.no_cpu_baseline:
+        g.close()  # host RAM for the reference's slab metrics
         threads = os.cpu_count() or 1
-        val, sec, kind, cores = cpu_reference_run(1, 1, threads)
-        out["cpu_baseline"] = {"value": val, "unit": UNIT, "cores": cores, "kind": kind,
-                               "cpu_model": cpu_model(),
-                               "sample": f"1 RK4 step (4 RHS) on a periodic {CPU_SAMPLE_M}^3 box, "
-                                         f"same p=4/c_+/EC+Roe per-element work, {cores} threads"}
+        cs = CpuSlab(threads)
+        val, med, secs = cs.sample(3)
+        out["cpu_baseline"] = {"value": val, "unit": UNIT, "cores": threads, "kind": cs.kind_name,
+                               "cpu_model": cpu_model(), "sample": cs.describe(3),
+                               "setup_s": cs.setup_s, "rhs_s": secs}
     g.close()
     if rank == 0:
         print(json.dumps(out), flush=True)
@@ -300,6 +373,9 @@ def main():
     ap.add_argument("--impl", default="b200", choices=["b200", "reference"])
     ap.add_argument("--no-cpu-baseline", action="store_true")
     args = ap.parse_args()
+    cmd = relaunch_command(args, sys.argv[1:])
+    if cmd:
+        raise SystemExit(subprocess.call(cmd))
     if args.impl == "reference":
         run_reference_arm(args)
     else:

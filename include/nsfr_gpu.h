@@ -111,6 +111,12 @@ const char* nsfr_gpu_create_error(void);
 /* 128-byte NCCL unique id (call on rank 0, broadcast to the others). */
 int nsfr_gpu_nccl_unique_id(void* out128);
 
+/* The NCCL communicator a context exchanges over, as NCCL itself reports it
+ * (ncclCommCount / ncclCommUserRank / ncclCommCuDevice): a multi-GPU launch
+ * prints these per rank so the world size can be checked. A context without
+ * a communicator (single rank, external halos) reports 0 / -1 / its device. */
+int nsfr_gpu_comm_info(nsfr_gpu_ctx* ctx, int* nccl_nranks, int* nccl_rank, int* cuda_device);
+
 /* Halo plan of a z-slab decomposition (pure host logic, no GPU needed):
  * the slab of `rank`, the peers it exchanges face traces with, and the
  * message size in doubles. */
@@ -161,8 +167,10 @@ int nsfr_gpu_rk4_step_dt(nsfr_gpu_ctx* ctx, double dt);
  * reference-style loop `dt = adaptive_dt(u); u = rk4_step(u, dt)` runs as
  * rk4_step_host(u, u, dt, cfl, t_final, NULL, &dt) with no global reduction
  * inside the step (dt <= 0 takes lambda_max of u_in first: one barrier).
- * Single-rank NSFR contexts stream; slab / DG contexts run the calls in
- * sequence. */
+ * NSFR contexts stream: a single rank, and a z-slab with an NCCL
+ * communicator (its end chunks take the per-stage halo planes). External-halo
+ * slab contexts (no NCCL id: the caller moves the planes between stages) and
+ * DG contexts run the same calls in sequence. */
 int nsfr_gpu_rk4_step_host(nsfr_gpu_ctx* ctx, const double* u_in, double* u_out, double dt,
                            double cfl, double t_final, double* dt_used, double* dt_next);
 int nsfr_gpu_max_wavespeed(nsfr_gpu_ctx* ctx, double* lam);
@@ -200,6 +208,9 @@ int nsfr_gpu_time_steps(nsfr_gpu_ctx* ctx, int nsteps, double cfl, double* step_
 
 /* FP64 pipe peak of `device` in TFLOP/s (DFMA loop; roofline denominator). */
 int nsfr_gpu_measure_fp64_peak(int device, double* tflops);
+/* Same, plus the SM clock (MHz) the loop ran at, from the CTAs' clock64 spans
+ * over the event-timed launch (nominal peak = SMs x 128 flop/clk x clock). */
+int nsfr_gpu_measure_fp64_peak_ex(int device, double* tflops, double* sm_mhz);
 
 /* ---- Stage-level driving and external halo transport ----------------------
  * A context created with nranks > 1 but nccl_id == NULL exchanges no data

@@ -20,6 +20,7 @@
 //   weight_adjusted_inverse_apply  fr_operators.cpp:280-309
 //   isentropic_vortex_exact / tgv_initial    cases.cpp:7-56
 //   parallel_for                   defs.hpp:36-50
+#include <algorithm>
 #include <atomic>
 #include <cmath>
 #include <cstdio>
@@ -48,12 +49,59 @@ struct RefCtx {
   Operator1D half_skew, interp_t, bs_row[2], bs_col[2];
   CurvilinearMapping mapping;
   MetricData md;
+  int md_base = 0;  // md.elem[i] holds global element md_base + i
   int np = 0, nq = 0, nv = 0, nsol = 0, nf = 0, ne = 0;
   std::vector<double> ut_vol, ut_f, vhat;
   std::string msg;
 };
 
 int global_elem(const RefCtx& c, int e) { return e + c.cfg.m * c.cfg.m * c.cfg.k0; }
+int md_index(const RefCtx& c, int e) { return global_elem(c, e) - c.md_base; }
+
+// Metrics of the slab's elements only. build_metrics_conservative_curl
+// (geometry.cpp:86-266) is element-local: it reads mapping.point(e, .) and the
+// shared 1D operators, nothing of the neighbours or of the mesh. So it runs on
+// chunks of the slab in parallel (parallel_for, defs.hpp:36-50), each chunk a
+// sub-mapping whose stand-in mesh has >= chunk elements (padded by repeating
+// the chunk's last element); element i of a chunk gets exactly the metrics the
+// whole-box build gives it. A 128x128x16 slab then needs 1/8 of the whole
+// box's metric memory and the build runs on every core.
+MetricData build_metrics_slab(const CurvilinearMapping& full, const ReferenceOperators& ops, int e0,
+                              int ne, int workers) {
+  MetricData md;
+  md.elem.resize(ne);
+  const int nchunks = std::max(1, std::min(ne, 4 * std::max(1, workers)));
+  const size_t per = static_cast<size_t>(full.nodes_per_element()) * 3;
+  std::vector<MetricData> heads(1);
+  parallel_for(nchunks, workers, [&](int ch) {
+    const int a = static_cast<int>(static_cast<long long>(ne) * ch / nchunks);
+    const int b = static_cast<int>(static_cast<long long>(ne) * (ch + 1) / nchunks);
+    const int cnt = b - a;
+    if (cnt <= 0) return;
+    int mf = 1;
+    while (mf * mf * mf < cnt) ++mf;
+    CurvilinearMapping sub;
+    sub.mesh = StructuredMesh{mf, full.mesh.x_left, full.mesh.x_right};
+    sub.grid_degree = full.grid_degree;
+    sub.grid_basis = full.grid_basis;
+    sub.grid_ext = full.grid_ext;
+    sub.control_points.resize(static_cast<size_t>(mf) * mf * mf * per);
+    for (int i = 0; i < mf * mf * mf; ++i) {
+      const size_t src = static_cast<size_t>(e0 + a + std::min(i, cnt - 1)) * per;
+      std::copy(full.control_points.begin() + src, full.control_points.begin() + src + per,
+                sub.control_points.begin() + static_cast<size_t>(i) * per);
+    }
+    MetricData part = build_metrics_conservative_curl(sub, ops);
+    for (int i = 0; i < cnt; ++i) md.elem[a + i] = std::move(part.elem[i]);
+    if (ch == 0) {
+      heads[0].vol_ext = part.vol_ext;
+      heads[0].sol_ext = part.sol_ext;
+    }
+  });
+  md.vol_ext = heads[0].vol_ext;
+  md.sol_ext = heads[0].sol_ext;
+  return md;
+}
 
 void case_state(const RefCtx& c, int kind, const double* x, double t, double* u) {
   State st;
@@ -193,7 +241,7 @@ void rhs_elem(RefCtx& c, int e, const double* halo_lo, const double* halo_hi, do
   const auto& o = c.ops;
   const int nv = c.nv, nf = c.nf, nsol = c.nsol, nq = c.nq;
   const Extents qe{nq, nq, nq}, me{c.np, c.np, c.np};
-  const ElementMetrics& em = c.md.elem[global_elem(c, e)];
+  const ElementMetrics& em = c.md.elem[md_index(c, e)];
   const double* utv = &c.ut_vol[static_cast<size_t>(e) * kStates * nv];
   const double* utf_all = &c.ut_f[static_cast<size_t>(e) * 6 * kStates * nf];
   std::vector<double> vol(kStates * nv, 0.0);
@@ -233,7 +281,7 @@ void rhs_elem(RefCtx& c, int e, const double* halo_lo, const double* halo_hi, do
   for (int fid = 0; fid < 6; ++fid) {
     const double* utf = utf_all + static_cast<size_t>(fid) * kStates * nf;
     const double* utn = nbr_trace(c, e, fid, halo_lo, halo_hi);
-    const FaceNormals fnrm = physical_normals(c.md, global_elem(c, e), fid);
+    const FaceNormals fnrm = physical_normals(c.md, md_index(c, e), fid);
     for (int t2 = 0; t2 < nq; ++t2)
       for (int t1 = 0; t1 < nq; ++t1) {
         const int k = t1 + nq * t2;
@@ -312,7 +360,7 @@ void dg_rhs_elem(RefCtx& c, int e, const double* halo_lo, const double* halo_hi,
   const auto& o = c.ops;
   const int nv = c.nv, nf = c.nf, nsol = c.nsol, nq = c.nq;
   const Extents qe{nq, nq, nq};
-  const ElementMetrics& em = c.md.elem[global_elem(c, e)];
+  const ElementMetrics& em = c.md.elem[md_index(c, e)];
   const double* utv = &c.ut_vol[static_cast<size_t>(e) * kStates * nv];
   const double* utf_all = &c.ut_f[static_cast<size_t>(e) * 6 * kStates * nf];
   std::vector<double> fr(3 * kStates * nv), vol(kStates * nv), tmpv(nv);
@@ -351,7 +399,7 @@ void dg_rhs_elem(RefCtx& c, int e, const double* halo_lo, const double* halo_hi,
       facc[fid].assign(kStates * nf, 0.0);
       const double* utf = utf_all + static_cast<size_t>(fid) * kStates * nf;
       const double* utn = nbr_trace(c, e, fid, halo_lo, halo_hi);
-      const FaceNormals fnrm = physical_normals(c.md, global_elem(c, e), fid);
+      const FaceNormals fnrm = physical_normals(c.md, md_index(c, e), fid);
       for (int t2 = 0; t2 < nq; ++t2)
         for (int t1 = 0; t1 < nq; ++t1) {
           const int k = t1 + nq * t2;
@@ -465,7 +513,13 @@ void* nsfr_ref_create(const nsfr_cfg* cfg, char* err, int errlen) {
     }
     c->mapping = warp_grid_3d(cfg->m, cfg->beta, cfg->x_left, cfg->x_right, cfg->grid_degree,
                               cfg->length_scale);
-    c->md = build_metrics_conservative_curl(c->mapping, c->ops);
+    if (cfg->k0 == 0 && cfg->k1 == cfg->m) {
+      c->md = build_metrics_conservative_curl(c->mapping, c->ops);
+    } else {  // a z-slab: its own elements only
+      c->md_base = cfg->m * cfg->m * cfg->k0;
+      c->md = build_metrics_slab(c->mapping, c->ops, c->md_base, c->ne, cfg->workers);
+      std::vector<double>().swap(c->mapping.control_points);  // the mesh (neighbours) stays
+    }
     c->ut_vol.resize(static_cast<size_t>(c->ne) * kStates * c->nv);
     c->ut_f.resize(static_cast<size_t>(c->ne) * 6 * kStates * c->nf);
     c->vhat.resize(static_cast<size_t>(c->ne) * kStates * c->nsol);
@@ -506,7 +560,7 @@ int nsfr_ref_tables(void* ctx, double* out, int cap) {
 int nsfr_ref_metrics(void* ctx, double* jac, double* cof) {
   const RefCtx& c = *static_cast<RefCtx*>(ctx);
   for (int e = 0; e < c.ne; ++e) {
-    const ElementMetrics& em = c.md.elem[global_elem(c, e)];
+    const ElementMetrics& em = c.md.elem[md_index(c, e)];
     if (jac) std::memcpy(jac + static_cast<size_t>(e) * c.nv, em.jac_vol.data(), sizeof(double) * c.nv);
     if (cof)
       std::memcpy(cof + static_cast<size_t>(e) * c.nv * 9, em.cof_vol.data(),
@@ -518,7 +572,7 @@ int nsfr_ref_metrics(void* ctx, double* jac, double* cof) {
 int nsfr_ref_x_sol(void* ctx, double* x) {
   const RefCtx& c = *static_cast<RefCtx*>(ctx);
   for (int e = 0; e < c.ne; ++e)
-    std::memcpy(x + static_cast<size_t>(e) * c.nsol * 3, c.md.elem[global_elem(c, e)].x_sol.data(),
+    std::memcpy(x + static_cast<size_t>(e) * c.nsol * 3, c.md.elem[md_index(c, e)].x_sol.data(),
                 sizeof(double) * c.nsol * 3);
   return NSFR_OK;
 }
@@ -526,7 +580,7 @@ int nsfr_ref_x_sol(void* ctx, double* x) {
 int nsfr_ref_x_vol(void* ctx, double* x) {
   const RefCtx& c = *static_cast<RefCtx*>(ctx);
   for (int e = 0; e < c.ne; ++e)
-    std::memcpy(x + static_cast<size_t>(e) * c.nv * 3, c.md.elem[global_elem(c, e)].x_vol.data(),
+    std::memcpy(x + static_cast<size_t>(e) * c.nv * 3, c.md.elem[md_index(c, e)].x_vol.data(),
                 sizeof(double) * c.nv * 3);
   return NSFR_OK;
 }
@@ -534,7 +588,7 @@ int nsfr_ref_x_vol(void* ctx, double* x) {
 int nsfr_ref_initial_state(void* ctx, int kind, double* u) {
   const RefCtx& c = *static_cast<RefCtx*>(ctx);
   for (int e = 0; e < c.ne; ++e) {
-    const auto& xs = c.md.elem[global_elem(c, e)].x_sol;
+    const auto& xs = c.md.elem[md_index(c, e)].x_sol;
     for (int q = 0; q < c.nsol; ++q) {
       double st[kStates];
       case_state(c, kind, &xs[3 * static_cast<size_t>(q)], 0.0, st);
@@ -591,7 +645,7 @@ int nsfr_ref_ke_volume(void* ctx, const double* u, double* out) {
   std::vector<double> part(c.ne, 0.0);
   std::atomic<int> bad{-1};
   parallel_for(c.ne, c.cfg.workers, [&](int e) {
-    const ElementMetrics& em = c.md.elem[global_elem(c, e)];
+    const ElementMetrics& em = c.md.elem[md_index(c, e)];
     const double* utv = &c.ut_vol[static_cast<size_t>(e) * kStates * nv];
     std::vector<double> vol(kStates * nv, 0.0);
     auto provider = [&](int i, int j, int dir, double* o5) {
@@ -719,7 +773,7 @@ int nsfr_ref_l2_error(void* ctx, const double* u, double t, int kind, double out
   std::vector<double> work(4096), uq(kStates * c.nv);
   double er = 0.0, ep = 0.0;
   for (int e = 0; e < c.ne; ++e) {
-    const ElementMetrics& em = c.md.elem[global_elem(c, e)];
+    const ElementMetrics& em = c.md.elem[md_index(c, e)];
     for (int s = 0; s < kStates; ++s)
       apply_tensor_product(o.basis.interp, o.basis.interp, o.basis.interp,
                            std::span<const double>(u + (static_cast<size_t>(e) * kStates + s) * c.nsol, c.nsol),
@@ -758,7 +812,7 @@ int nsfr_ref_entropy_total(void* ctx, const double* u, double* out) {
   std::vector<double> work(4096), uq(kStates * c.nv);
   double tot = 0.0;
   for (int e = 0; e < c.ne; ++e) {
-    const ElementMetrics& em = c.md.elem[global_elem(c, e)];
+    const ElementMetrics& em = c.md.elem[md_index(c, e)];
     for (int s = 0; s < kStates; ++s)
       apply_tensor_product(o.basis.interp, o.basis.interp, o.basis.interp,
                            std::span<const double>(u + (static_cast<size_t>(e) * kStates + s) * c.nsol, c.nsol),
@@ -787,7 +841,7 @@ int nsfr_ref_conserved_totals(void* ctx, const double* u, double out5[5]) {
   std::vector<double> work(4096), uq(kStates * c.nv);
   double tot[kStates] = {0.0, 0.0, 0.0, 0.0, 0.0};
   for (int e = 0; e < c.ne; ++e) {
-    const ElementMetrics& em = c.md.elem[global_elem(c, e)];
+    const ElementMetrics& em = c.md.elem[md_index(c, e)];
     for (int s = 0; s < kStates; ++s)
       apply_tensor_product(o.basis.interp, o.basis.interp, o.basis.interp,
                            std::span<const double>(u + (static_cast<size_t>(e) * kStates + s) * c.nsol, c.nsol),

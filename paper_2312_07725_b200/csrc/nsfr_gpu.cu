@@ -82,6 +82,25 @@ thread_local std::string g_create_error;
     }                                                                                     \
   } while (0)
 
+// Every ABI entry that takes a context runs on that context's device and
+// restores the caller's current device on return (a thread may drive contexts
+// on several GPUs; kernel attributes, lazily created streams/events and the
+// launches themselves are all per device).
+struct DeviceGuard {
+  int prev = -1;
+  explicit DeviceGuard(int want) {
+    int cur = -1;
+    if (want < 0 || cudaGetDevice(&cur) != cudaSuccess) return;
+    if (cur != want && cudaSetDevice(want) == cudaSuccess) prev = cur;
+  }
+  explicit DeviceGuard(const nsfr_gpu_ctx* c) : DeviceGuard(c ? c->s.device : -1) {}
+  ~DeviceGuard() {
+    if (prev >= 0) cudaSetDevice(prev);
+  }
+  DeviceGuard(const DeviceGuard&) = delete;
+  DeviceGuard& operator=(const DeviceGuard&) = delete;
+};
+
 size_t nsol(const nsfr_gpu_ctx* c) { return static_cast<size_t>(c->N) * c->N * c->N; }
 size_t state_count(const nsfr_gpu_ctx* c) { return static_cast<size_t>(c->E) * NS * nsol(c); }
 size_t nquad(const nsfr_gpu_ctx* c) { return static_cast<size_t>(c->NQ) * c->NQ * c->NQ; }
@@ -832,6 +851,7 @@ int nsfr_gpu_halo_plan_for(int m, int p, int rank, int nranks, nsfr_gpu_halo_pla
 }
 
 int nsfr_gpu_create(const nsfr_gpu_setup* setup, nsfr_gpu_ctx** out) {
+  DeviceGuard dev_guard_(setup ? setup->device : -1);
   *out = nullptr;
   auto* ctx = new nsfr_gpu_ctx();
   ctx->s = *setup;
@@ -988,6 +1008,7 @@ int nsfr_gpu_create(const nsfr_gpu_setup* setup, nsfr_gpu_ctx** out) {
 }
 
 int nsfr_gpu_destroy(nsfr_gpu_ctx* ctx) {
+  DeviceGuard dev_guard_(ctx);
   if (!ctx) return NSFR_OK;
   if (ctx->st) cudaStreamSynchronize(ctx->st);
   if (ctx->graph) cudaGraphExecDestroy(ctx->graph);
@@ -1016,9 +1037,23 @@ int nsfr_gpu_destroy(nsfr_gpu_ctx* ctx) {
   return NSFR_OK;
 }
 
+int nsfr_gpu_comm_info(nsfr_gpu_ctx* ctx, int* nccl_nranks, int* nccl_rank, int* cuda_device) {
+  DeviceGuard dev_guard_(ctx);
+  if (!ctx || !nccl_nranks || !nccl_rank || !cuda_device) return NSFR_E_DIM;
+  *nccl_nranks = 0;
+  *nccl_rank = -1;
+  *cuda_device = ctx->s.device;
+  if (!ctx->comm) return NSFR_OK;
+  NK(ncclCommCount(ctx->comm, nccl_nranks));
+  NK(ncclCommUserRank(ctx->comm, nccl_rank));
+  NK(ncclCommCuDevice(ctx->comm, cuda_device));
+  return NSFR_OK;
+}
+
 const char* nsfr_gpu_last_error(const nsfr_gpu_ctx* ctx) { return ctx ? ctx->msg.c_str() : "null context"; }
 
 int nsfr_gpu_get_tables(nsfr_gpu_ctx* ctx, double* out, int cap) {
+  DeviceGuard dev_guard_(ctx);
   const Tables1D& t = ctx->tab;
   int pos = 0;
   auto put = [&](const std::vector<double>& v) {
@@ -1041,6 +1076,7 @@ int nsfr_gpu_get_tables(nsfr_gpu_ctx* ctx, double* out, int cap) {
 }
 
 int nsfr_gpu_get_metrics(nsfr_gpu_ctx* ctx, double* jac, double* cof) {
+  DeviceGuard dev_guard_(ctx);
   const size_t n3 = static_cast<size_t>(ctx->E) * nquad(ctx);
   const int N3 = static_cast<int>(nquad(ctx));
   CK(cudaStreamSynchronize(ctx->st));
@@ -1057,6 +1093,7 @@ int nsfr_gpu_get_metrics(nsfr_gpu_ctx* ctx, double* jac, double* cof) {
 }
 
 int nsfr_gpu_set_state(nsfr_gpu_ctx* ctx, const double* u) {
+  DeviceGuard dev_guard_(ctx);
   ctx->proj_valid = false;
   if (ctx->dg) return nsfr_gpu_set_state_q(ctx, u);  // DG carries u_hat itself
   // u_hat -> scratch (d_vol is dead between steps) -> u_q = chi^3 u_hat, in
@@ -1080,6 +1117,7 @@ int nsfr_gpu_set_state(nsfr_gpu_ctx* ctx, const double* u) {
 }
 
 int nsfr_gpu_get_state(nsfr_gpu_ctx* ctx, double* u) {
+  DeviceGuard dev_guard_(ctx);
   if (ctx->dg) return nsfr_gpu_get_state_q(ctx, u);
   // u_q -> Pi^3 -> u_hat in element chunks; the copy of chunk c overlaps the
   // conversion of chunk c+1
@@ -1102,6 +1140,7 @@ int nsfr_gpu_get_state(nsfr_gpu_ctx* ctx, double* u) {
 }
 
 int nsfr_gpu_set_state_q(nsfr_gpu_ctx* ctx, const double* uq) {
+  DeviceGuard dev_guard_(ctx);
   ctx->proj_valid = false;
   CK(cudaMemcpyAsync(ctx->d_un, uq, sizeof(double) * state_count(ctx), cudaMemcpyHostToDevice, ctx->st));
   CK(cudaStreamSynchronize(ctx->st));
@@ -1109,12 +1148,14 @@ int nsfr_gpu_set_state_q(nsfr_gpu_ctx* ctx, const double* uq) {
 }
 
 int nsfr_gpu_get_state_q(nsfr_gpu_ctx* ctx, double* uq) {
+  DeviceGuard dev_guard_(ctx);
   CK(cudaMemcpyAsync(uq, ctx->d_un, sizeof(double) * state_count(ctx), cudaMemcpyDeviceToHost, ctx->st));
   CK(cudaStreamSynchronize(ctx->st));
   return NSFR_OK;
 }
 
 int nsfr_gpu_init_case(nsfr_gpu_ctx* ctx, int kind) {
+  DeviceGuard dev_guard_(ctx);
   const int g = ctx->tab.g, np = ctx->N, G3 = g * g * g, S3 = np * np * np;
   const int M = std::max(g, np), M3 = M * M * M;
   const size_t smem = sizeof(double) * (3 * G3 + 2 * M3 + 3 * S3);
@@ -1141,6 +1182,7 @@ int nsfr_gpu_init_case(nsfr_gpu_ctx* ctx, int kind) {
 }
 
 int nsfr_gpu_set_time(nsfr_gpu_ctx* ctx, double t) {
+  DeviceGuard dev_guard_(ctx);
   ctx->proj_valid = false;  // also the re-sync point after writes through state_device_ptr
   CK(cudaMemcpyAsync(&ctx->d_step->t, &t, sizeof(double), cudaMemcpyHostToDevice, ctx->st));
   CK(cudaStreamSynchronize(ctx->st));
@@ -1148,12 +1190,14 @@ int nsfr_gpu_set_time(nsfr_gpu_ctx* ctx, double t) {
 }
 
 int nsfr_gpu_get_time(nsfr_gpu_ctx* ctx, double* t) {
+  DeviceGuard dev_guard_(ctx);
   if (int rc = sync_check(ctx)) return rc;
   *t = ctx->h_step->t;
   return NSFR_OK;
 }
 
 int nsfr_gpu_rhs(nsfr_gpu_ctx* ctx, double* dudt, double* entropy_change) {
+  DeviceGuard dev_guard_(ctx);
   const bool ent = entropy_change != nullptr;
   if (ent && ctx->dg) {
     ctx->msg = "entropy change: defined for the NSFR scheme only";
@@ -1175,9 +1219,13 @@ int nsfr_gpu_rhs(nsfr_gpu_ctx* ctx, double* dudt, double* entropy_change) {
   return NSFR_OK;
 }
 
-int nsfr_gpu_entropy_change(nsfr_gpu_ctx* ctx, double* out) { return nsfr_gpu_rhs(ctx, nullptr, out); }
+int nsfr_gpu_entropy_change(nsfr_gpu_ctx* ctx, double* out) {
+  DeviceGuard dev_guard_(ctx);
+  return nsfr_gpu_rhs(ctx, nullptr, out);
+}
 
 int nsfr_gpu_get_traces(nsfr_gpu_ctx* ctx, double* traces) {
+  DeviceGuard dev_guard_(ctx);
   CK(cudaStreamSynchronize(ctx->st));
   CK(cudaMemcpy(traces, ctx->d_tr, sizeof(double) * ctx->E * 6 * NS * ctx->NQ * ctx->NQ,
                 cudaMemcpyDeviceToHost));
@@ -1185,6 +1233,7 @@ int nsfr_gpu_get_traces(nsfr_gpu_ctx* ctx, double* traces) {
 }
 
 int nsfr_gpu_max_wavespeed(nsfr_gpu_ctx* ctx, double* lam) {
+  DeviceGuard dev_guard_(ctx);
   if (int rc = project_state(ctx)) return rc;
   if (ctx->comm)
     NK(ncclAllReduce(&ctx->d_step->lam_bits, &ctx->d_step->lam_bits, 1, ncclUint64, ncclMax, ctx->comm, ctx->st));
@@ -1195,6 +1244,7 @@ int nsfr_gpu_max_wavespeed(nsfr_gpu_ctx* ctx, double* lam) {
 }
 
 int nsfr_gpu_rk4_step_dt(nsfr_gpu_ctx* ctx, double dt) {
+  DeviceGuard dev_guard_(ctx);
   CK(cudaMemcpyAsync(&ctx->d_step->dt, &dt, sizeof dt, cudaMemcpyHostToDevice, ctx->st));
   if (int rc = ensure_projected(ctx)) return rc;
   if (int rc = enqueue_step(ctx, true)) return rc;
@@ -1212,6 +1262,7 @@ static int set_step_params(nsfr_gpu_ctx* ctx, double cfl, double t_final) {
 }
 
 int nsfr_gpu_rk4_step(nsfr_gpu_ctx* ctx, double cfl, double t_final, double* dt_used) {
+  DeviceGuard dev_guard_(ctx);
   if (int rc = set_step_params(ctx, cfl, t_final)) return rc;
   if (int rc = ensure_projected(ctx)) return rc;
   if (int rc = enqueue_step(ctx, false)) return rc;
@@ -1221,6 +1272,7 @@ int nsfr_gpu_rk4_step(nsfr_gpu_ctx* ctx, double cfl, double t_final, double* dt_
 }
 
 int nsfr_gpu_advance(nsfr_gpu_ctx* ctx, int nsteps, double cfl, double t_final, double* t_out) {
+  DeviceGuard dev_guard_(ctx);
   if (int rc = set_step_params(ctx, cfl, t_final)) return rc;
   if (int rc = ensure_projected(ctx)) return rc;
   if (!ctx->graph && !ctx->timing) {
@@ -1514,6 +1566,7 @@ static int rk4_step_host_impl(nsfr_gpu_ctx* ctx, const double* u_in, double* u_o
 
 int nsfr_gpu_rk4_step_host(nsfr_gpu_ctx* ctx, const double* u_in, double* u_out, double dt,
                            double cfl, double t_final, double* dt_used, double* dt_next) {
+  DeviceGuard dev_guard_(ctx);
   if (!ctx) return NSFR_E_DIM;
   if (!u_in || !u_out) {
     ctx->msg = "rk4_step_host: null state buffer";
@@ -1531,6 +1584,7 @@ int nsfr_gpu_rk4_step_host(nsfr_gpu_ctx* ctx, const double* u_in, double* u_out,
 }
 
 int nsfr_gpu_l2_error(nsfr_gpu_ctx* ctx, int kind, double out2[2]) {
+  DeviceGuard dev_guard_(ctx);
   const int g = ctx->tab.g, n = ctx->NQ, G3 = g * g * g, N3 = n * n * n;
   const int M = std::max(g, n), M3 = M * M * M;
   const size_t smem = sizeof(double) * (3 * G3 + 2 * M3 + 10 * N3);
@@ -1586,6 +1640,7 @@ static int totals(nsfr_gpu_ctx* ctx, double out6[NTOT]) {
 // ---- external halo mode (nranks > 1, no NCCL id): the caller moves the planes
 int nsfr_gpu_halo_buffers(nsfr_gpu_ctx* ctx, double** send_lo, double** send_hi, double** recv_lo,
                           double** recv_hi) {
+  DeviceGuard dev_guard_(ctx);
   *send_lo = ctx->d_send_lo;
   *send_hi = ctx->d_send_hi;
   *recv_lo = ctx->d_halo_lo;
@@ -1594,6 +1649,7 @@ int nsfr_gpu_halo_buffers(nsfr_gpu_ctx* ctx, double** send_lo, double** send_hi,
 }
 
 int nsfr_gpu_halo_get(nsfr_gpu_ctx* ctx, double* send_lo, double* send_hi) {
+  DeviceGuard dev_guard_(ctx);
   if (!ctx->d_send_lo) {
     ctx->msg = "halo_get: single-rank context has no halo planes";
     return NSFR_E_CONFIG;
@@ -1605,6 +1661,7 @@ int nsfr_gpu_halo_get(nsfr_gpu_ctx* ctx, double* send_lo, double* send_hi) {
 }
 
 int nsfr_gpu_halo_set(nsfr_gpu_ctx* ctx, const double* recv_lo, const double* recv_hi) {
+  DeviceGuard dev_guard_(ctx);
   if (!ctx->d_halo_lo) {
     ctx->msg = "halo_set: single-rank context has no halo planes";
     return NSFR_E_CONFIG;
@@ -1616,6 +1673,7 @@ int nsfr_gpu_halo_set(nsfr_gpu_ctx* ctx, const double* recv_lo, const double* re
 }
 
 int nsfr_gpu_project(nsfr_gpu_ctx* ctx) {
+  DeviceGuard dev_guard_(ctx);
   if (ctx->dg) {
     ctx->msg = "project: defined for the NSFR scheme only";
     return NSFR_E_CONFIG;
@@ -1625,6 +1683,7 @@ int nsfr_gpu_project(nsfr_gpu_ctx* ctx) {
 }
 
 int nsfr_gpu_residual(nsfr_gpu_ctx* ctx, double* dudt, double* entropy_change) {
+  DeviceGuard dev_guard_(ctx);
   if (ctx->dg) {
     ctx->msg = "residual: defined for the NSFR scheme only";
     return NSFR_E_CONFIG;
@@ -1653,6 +1712,7 @@ int nsfr_gpu_residual(nsfr_gpu_ctx* ctx, double* dudt, double* entropy_change) {
 }
 
 int nsfr_gpu_stage(nsfr_gpu_ctx* ctx, int stage, double dt) {
+  DeviceGuard dev_guard_(ctx);
   if (ctx->dg) {
     ctx->msg = "stage: defined for the NSFR scheme only";
     return NSFR_E_CONFIG;
@@ -1681,6 +1741,7 @@ int nsfr_gpu_stage(nsfr_gpu_ctx* ctx, int stage, double dt) {
 }
 
 int nsfr_gpu_conserved_totals(nsfr_gpu_ctx* ctx, double out5[5]) {
+  DeviceGuard dev_guard_(ctx);
   double t[NTOT];
   if (int rc = totals(ctx, t)) return rc;
   for (int s = 0; s < NS; ++s) out5[s] = t[s];
@@ -1688,6 +1749,7 @@ int nsfr_gpu_conserved_totals(nsfr_gpu_ctx* ctx, double out5[5]) {
 }
 
 int nsfr_gpu_entropy_total(nsfr_gpu_ctx* ctx, double* out) {
+  DeviceGuard dev_guard_(ctx);
   double t[NTOT];
   if (int rc = totals(ctx, t)) return rc;
   *out = t[NS];
@@ -1695,6 +1757,7 @@ int nsfr_gpu_entropy_total(nsfr_gpu_ctx* ctx, double* out) {
 }
 
 int nsfr_gpu_ke_volume(nsfr_gpu_ctx* ctx, double* out) {
+  DeviceGuard dev_guard_(ctx);
   if (ctx->dg) {
     ctx->msg = "ke_volume: defined for the NSFR scheme only";
     return NSFR_E_CONFIG;
@@ -1715,6 +1778,7 @@ int nsfr_gpu_ke_volume(nsfr_gpu_ctx* ctx, double* out) {
 }
 
 int nsfr_gpu_ke_total(nsfr_gpu_ctx* ctx, double* out) {
+  DeviceGuard dev_guard_(ctx);
   if (ctx->dg) {
     ctx->msg = "ke_total: defined for the NSFR scheme only";
     return NSFR_E_CONFIG;
@@ -1740,7 +1804,10 @@ int nsfr_gpu_ke_total(nsfr_gpu_ctx* ctx, double* out) {
 
 double* nsfr_gpu_state_device_ptr(nsfr_gpu_ctx* ctx) { return ctx->d_un; }
 size_t nsfr_gpu_state_count(const nsfr_gpu_ctx* ctx) { return state_count(ctx); }
-int nsfr_gpu_sync(nsfr_gpu_ctx* ctx) { return sync_check(ctx); }
+int nsfr_gpu_sync(nsfr_gpu_ctx* ctx) {
+  DeviceGuard dev_guard_(ctx);
+  return sync_check(ctx);
+}
 long long nsfr_gpu_launch_count(const nsfr_gpu_ctx* ctx) { return ctx->launches; }
 
 // Bench helper: time `nsteps` RK4 steps with CUDA events on the context
@@ -1748,6 +1815,7 @@ long long nsfr_gpu_launch_count(const nsfr_gpu_ctx* ctx) { return ctx->launches;
 // kernel_ms[0]/[1]/[2] receive the summed K1/K2/K3 durations (ms).
 int nsfr_gpu_time_steps(nsfr_gpu_ctx* ctx, int nsteps, double cfl, double* step_ms,
                         double* kernel_ms) {
+  DeviceGuard dev_guard_(ctx);
   if (int rc = set_step_params(ctx, cfl, 0.0)) return rc;
   if (!kernel_ms && !ctx->graph) {
     if (int rc = nsfr_gpu_advance(ctx, 0, cfl, 0.0, nullptr)) return rc;  // capture the step graph
@@ -1796,7 +1864,10 @@ int nsfr_gpu_time_steps(nsfr_gpu_ctx* ctx, int nsteps, double cfl, double* step_
 // FP64 pipe peak (roofline denominator; MEASURED_PEAKS.json carries none):
 // independent DFMA chains on every SM, best of 5, CUDA events.
 namespace {
-__global__ void k_dfma_peak(double* out, int iters, double a, double b) {
+// Each CTA's thread 0 records its SM clock64 span: cycles / event time is the
+// SM clock the DFMA loop actually ran at (roofline nominal = 148 x 128 x f).
+__global__ void k_dfma_peak(double* out, long long* cycles, int iters, double a, double b) {
+  const long long c0 = clock64();
   double x0 = threadIdx.x, x1 = x0 + 1, x2 = x0 + 2, x3 = x0 + 3, x4 = x0 + 4, x5 = x0 + 5,
          x6 = x0 + 6, x7 = x0 + 7;
   for (int i = 0; i < iters; ++i) {
@@ -1807,36 +1878,59 @@ __global__ void k_dfma_peak(double* out, int iters, double a, double b) {
     }
   }
   out[blockIdx.x * blockDim.x + threadIdx.x] = x0 + x1 + x2 + x3 + x4 + x5 + x6 + x7;
+  __syncthreads();
+  if (threadIdx.x == 0 && cycles) cycles[blockIdx.x] = clock64() - c0;
 }
 }  // namespace
 
-extern "C" int nsfr_gpu_measure_fp64_peak(int device, double* tflops) {
-  if (cudaSetDevice(device) != cudaSuccess) return NSFR_E_CUDA;
+extern "C" int nsfr_gpu_measure_fp64_peak_ex(int device, double* tflops, double* sm_mhz) {
+  DeviceGuard dev_guard_(device);
+  int cur = -1;
+  if (cudaGetDevice(&cur) != cudaSuccess || cur != device) return NSFR_E_CUDA;
   int sms = 0;
   cudaDeviceGetAttribute(&sms, cudaDevAttrMultiProcessorCount, device);
   const int threads = 256, blocks = sms * 8, iters = 2048;
   double* out = nullptr;
+  long long* cyc = nullptr;
   if (cudaMalloc(&out, sizeof(double) * threads * blocks) != cudaSuccess) return NSFR_E_CUDA;
+  if (cudaMalloc(&cyc, sizeof(long long) * blocks) != cudaSuccess) {
+    cudaFree(out);
+    return NSFR_E_CUDA;
+  }
   cudaEvent_t a, b;
   cudaEventCreate(&a);
   cudaEventCreate(&b);
-  k_dfma_peak<<<blocks, threads>>>(out, 64, 0.999999, 1e-7);
+  k_dfma_peak<<<blocks, threads>>>(out, nullptr, 64, 0.999999, 1e-7);
   float best = 1e30f;
+  double mhz = 0.0;
+  std::vector<long long> hc(blocks);
   for (int r = 0; r < 5; ++r) {
     cudaEventRecord(a);
-    k_dfma_peak<<<blocks, threads>>>(out, iters, 0.999999, 1e-7);
+    k_dfma_peak<<<blocks, threads>>>(out, cyc, iters, 0.999999, 1e-7);
     cudaEventRecord(b);
     cudaEventSynchronize(b);
     float ms = 0.f;
     cudaEventElapsedTime(&ms, a, b);
-    best = ms < best ? ms : best;
+    if (ms < best) {
+      best = ms;
+      // all CTAs are co-resident (8 per SM): the longest CTA span ~ the kernel
+      cudaMemcpy(hc.data(), cyc, sizeof(long long) * blocks, cudaMemcpyDeviceToHost);
+      const long long mx = *std::max_element(hc.begin(), hc.end());
+      mhz = mx / (ms * 1e3);
+    }
   }
   cudaEventDestroy(a);
   cudaEventDestroy(b);
+  cudaFree(cyc);
   cudaFree(out);
   if (cudaGetLastError() != cudaSuccess) return NSFR_E_CUDA;
   *tflops = 2.0 * 8 * 16 * (double)iters * threads * blocks / (best * 1e-3) / 1e12;
+  if (sm_mhz) *sm_mhz = mhz;
   return NSFR_OK;
+}
+
+extern "C" int nsfr_gpu_measure_fp64_peak(int device, double* tflops) {
+  return nsfr_gpu_measure_fp64_peak_ex(device, tflops, nullptr);
 }
 
 #ifdef NSFR_PHASE_PROF

@@ -28,6 +28,12 @@ def _fmt(x: float) -> str:
     return repr(float(x)) if math.isfinite(x) else ("nan" if math.isnan(x) else repr(x))
 
 
+def _scheme_label(cfg) -> str:
+    """NSFR-EC / NSFR-EC+Roe, or DG-cons / DG-cons+Roe (SolverConfig.scheme)."""
+    base = "NSFR-EC" if cfg.scheme == "nsfr" else "DG-cons"
+    return base + ("+Roe" if cfg.roe else "")
+
+
 def checkpoint_path(path: str, rank: int, nranks: int) -> str:
     """One file per rank (its z-slab) when the box is decomposed."""
     return path if nranks <= 1 else f"{path}.rank{rank}"
@@ -41,7 +47,7 @@ def write_checkpoint(path: str, solver, exact: bool = False) -> str:
     head = {
         "p": cfg.p, "m": cfg.m, "k0": solver.k0, "k1": solver.k1,
         "nodes": "quadrature" if exact else "solution",
-        "scheme": "NSFR-EC" + ("+Roe" if cfg.roe else ""), "quad_kind": cfg.quad_kind,
+        "scheme": _scheme_label(cfg), "overint": cfg.overint, "quad_kind": cfg.quad_kind,
         "c1d": _fmt(cfg.c1d), "gamma": _fmt(cfg.gamma), "case": cfg.case, "t": _fmt(t),
         "elements": u.shape[0],
     }
@@ -73,11 +79,12 @@ def read_checkpoint(path: str):
                 break
             k, v = line.split(None, 1)
             head[k] = v.strip()
-        for k in ("p", "m", "k0", "k1", "quad_kind", "elements"):
+        head.setdefault("overint", "0")
+        for k in ("p", "m", "k0", "k1", "quad_kind", "elements", "overint"):
             head[k] = int(head[k])
         for k in ("c1d", "gamma", "t"):
             head[k] = float(head[k])
-        n3 = (head["p"] + 1) ** 3
+        n3 = (head["p"] + 1) ** 3  # (the DG state is u_hat in both node modes)
         u = np.empty((head["elements"], 5, n3))
         for e in range(head["elements"]):
             tag = f.readline().split()
@@ -95,7 +102,8 @@ def load_checkpoint(path: str, solver) -> dict:
     """Restore state and time into a solver of the same discretisation and slab."""
     cfg = solver.cfg
     head, u = read_checkpoint(checkpoint_path(path, cfg.rank, cfg.nranks))
-    want = {"p": cfg.p, "m": cfg.m, "k0": solver.k0, "k1": solver.k1, "quad_kind": cfg.quad_kind}
+    want = {"p": cfg.p, "m": cfg.m, "k0": solver.k0, "k1": solver.k1, "quad_kind": cfg.quad_kind,
+            "overint": cfg.overint, "scheme": _scheme_label(cfg)}
     for k, v in want.items():
         if head[k] != v:
             raise ValueError(f"checkpoint {k}={head[k]} does not match the solver ({v})")
@@ -117,7 +125,8 @@ COLUMNS = ("t", "entropy_change", "entropy_change_normalized", "ke_change_volume
 
 def diagnostic_record(solver, u_total0: float | None) -> dict:
     """DiagnosticRecord of the current state; entropy change
-    needs entropy_diag=True (else NaN), L2 errors the vortex case (else NaN)."""
+    needs entropy_diag=True (else NaN), L2 errors the vortex case (else NaN),
+    the kinetic-energy terms the NSFR scheme (else NaN)."""
     cfg = solver.cfg
     rec = {"t": solver.time}
     if cfg.entropy_diag:
@@ -126,8 +135,10 @@ def diagnostic_record(solver, u_total0: float | None) -> dict:
         rec["entropy_change_normalized"] = ds / abs(u_total0) if u_total0 else math.nan
     else:
         rec["entropy_change"] = rec["entropy_change_normalized"] = math.nan
-    rec["ke_change_volume"] = solver.ke_volume()
-    rec["ke_change_total_minus_pressure_work"] = solver.ke_total() if cfg.nranks == 1 else math.nan
+    nsfr = cfg.scheme == "nsfr"  # the kinetic-energy terms are NSFR diagnostics (NaN for DG)
+    rec["ke_change_volume"] = solver.ke_volume() if nsfr else math.nan
+    rec["ke_change_total_minus_pressure_work"] = (solver.ke_total() if nsfr and cfg.nranks == 1
+                                                  else math.nan)
     tot = solver.conserved_totals()
     for k, v in zip(("mass", "momentum_x", "momentum_y", "momentum_z", "energy"), tot):
         rec[k] = float(v)

@@ -146,6 +146,8 @@ def load_library() -> C.CDLL:
         "nsfr_gpu_sync": (C.c_int, [V]),
         "nsfr_gpu_launch_count": (C.c_longlong, [V]),
         "nsfr_gpu_measure_fp64_peak": (C.c_int, [C.c_int, P]),
+        "nsfr_gpu_measure_fp64_peak_ex": (C.c_int, [C.c_int, P, P]),
+        "nsfr_gpu_comm_info": (C.c_int, [V, C.POINTER(C.c_int), C.POINTER(C.c_int), C.POINTER(C.c_int)]),
     }
     for name, (res, args) in sig.items():
         fn = getattr(lib, name)
@@ -172,12 +174,14 @@ def halo_plan(m: int, p: int, rank: int, nranks: int) -> dict:
     return {"k0": hp.k0, "k1": hp.k1, "peer_lo": hp.peer_lo, "peer_hi": hp.peer_hi, "count": hp.count}
 
 
-def measure_fp64_peak(device: int = 0) -> float:
-    """FP64 DFMA peak of the device in TFLOP/s (roofline denominator)."""
+def measure_fp64_peak(device: int = 0, with_clock: bool = False):
+    """FP64 DFMA peak of the device in TFLOP/s (roofline denominator); with
+    with_clock, (tflops, sm_mhz) with the SM clock the DFMA loop ran at."""
     out = np.zeros(1)
-    if load_library().nsfr_gpu_measure_fp64_peak(device, _ptr(out)):
+    mhz = np.zeros(1)
+    if load_library().nsfr_gpu_measure_fp64_peak_ex(device, _ptr(out), _ptr(mhz)):
         raise DeviceError("fp64 peak measurement failed")
-    return float(out[0])
+    return (float(out[0]), float(mhz[0])) if with_clock else float(out[0])
 
 
 def nccl_unique_id() -> bytes:
@@ -298,6 +302,12 @@ class GpuSolver:
 
     def launch_count(self) -> int:
         return int(self.lib.nsfr_gpu_launch_count(self.ctx))
+
+    def comm_info(self) -> dict:
+        """The NCCL communicator as NCCL reports it (nranks 0 without one)."""
+        n, r, d = C.c_int(), C.c_int(), C.c_int()
+        self._check(self.lib.nsfr_gpu_comm_info(self.ctx, C.byref(n), C.byref(r), C.byref(d)))
+        return {"nccl_nranks": n.value, "nccl_rank": r.value, "cuda_device": d.value}
 
     # --- setup products -------------------------------------------------------
     def tables(self) -> dict[str, np.ndarray]:

@@ -85,3 +85,49 @@ def test_diagnostics_csv_round_trip(tmp_path):
     for r, b in zip(recs, back):
         for c in runio.COLUMNS:
             assert (math.isnan(r[c]) and math.isnan(b[c])) or r[c] == b[c]
+
+
+def test_checkpoint_records_scheme(tmp_path):
+    """The header names the scheme (NSFR-EC / DG-cons, +Roe) and overintegration;
+    a checkpoint of one scheme does not load into a solver of the other."""
+    a = FakeSolver(SolverConfig(p=3, m=2, scheme="dg", overint=1))
+    path = runio.write_checkpoint(str(tmp_path / "ck.txt"), a)
+    head, _ = runio.read_checkpoint(path)
+    assert head["scheme"] == "DG-cons+Roe" and head["overint"] == 1
+    with pytest.raises(ValueError):
+        runio.load_checkpoint(path, FakeSolver(SolverConfig(p=3, m=2)))
+    runio.load_checkpoint(path, FakeSolver(SolverConfig(p=3, m=2, scheme="dg", overint=1)))
+
+
+class DiagSolver(FakeSolver):
+    """Stand-in with the diagnostics surface; the KE calls fail for DG like the C ABI."""
+
+    def entropy_total(self):
+        return -1.0
+
+    def entropy_change(self):
+        return -1e-9
+
+    def ke_volume(self):
+        if self.cfg.scheme != "nsfr":
+            raise RuntimeError("NSFR_E_CONFIG")
+        return 0.0
+
+    ke_total = ke_volume
+
+    def conserved_totals(self):
+        return np.ones(5)
+
+    def max_wavespeed(self):
+        return 1.5
+
+    def l2_error(self):
+        return np.array([1e-3, 2e-3])
+
+
+def test_diagnostics_of_dg_run_have_nan_ke():
+    rec = runio.diagnostic_record(DiagSolver(SolverConfig(p=3, m=2, scheme="dg")), -1.0)
+    assert math.isnan(rec["ke_change_volume"]) and math.isnan(rec["ke_change_total_minus_pressure_work"])
+    assert rec["l2_density"] == 1e-3
+    rec = runio.diagnostic_record(DiagSolver(SolverConfig(p=3, m=2)), -1.0)
+    assert rec["ke_change_volume"] == 0.0
