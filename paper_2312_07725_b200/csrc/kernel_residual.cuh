@@ -51,6 +51,10 @@ namespace nsfr_b200 {
 #ifndef NSFR_UNROLL_MAXN
 #define NSFR_UNROLL_MAXN 4
 #endif
+__device__ __forceinline__ PrimH load_prim(const double* __restrict__ Pd, int N3, int i) {
+  return PrimH{Pd[i], Pd[N3 + i], Pd[2 * N3 + i], Pd[3 * N3 + i], Pd[4 * N3 + i], Pd[5 * N3 + i]};
+}
+
 template <int N, bool KE>
 __device__ __forceinline__ void vol_pairs(const double* __restrict__ Pd, const double* __restrict__ Ch,
                                           double* __restrict__ acc,
@@ -99,8 +103,14 @@ struct ResCfg {
   static constexpr int LINES = 3 * N2;
   static constexpr int EPB = LINES <= 32 ? 6 : (LINES <= 64 ? 4 : 2);
   static constexpr int THREADS = ((EPB * LINES + 31) / 32) * 32;
+  // The element's own face traces (30 N2) are staged with the rest where that
+  // helps (N <= 4; measured K2 p=3 -2.4%, p=4 +1.7%): the face loop starts from shared
+  // memory instead of waiting on a global load (K2's largest long-scoreboard
+  // stall); at N = 5 the longer staging wait costs more, at N >= 6 a CTA per SM.
+  static constexpr bool STR = N <= 4;
   // ACCV (3 directions x 5 N3) + node primitives (6 N3) + half cofactors (9 N3)
-  static constexpr int PER_EL = 30 * N3;
+  // [+ own traces 30 N2]
+  static constexpr int PER_EL = 30 * N3 + (STR ? 30 * N2 : 0);
   static constexpr int SMEM = EPB * PER_EL * 8;
 #ifdef NSFR_RES_MINB
   static constexpr int MINB = NSFR_RES_MINB;
@@ -157,18 +167,20 @@ __device__ __forceinline__ void res_prefetch(const ResParams& P, int e0, int tid
 template <int N>
 struct ResSmem {
   static constexpr int N3 = N * N * N, EPB = ResCfg<N>::EPB, AS = 15 * N3;
-  double *ACCV, *PRIM, *COF;
+  double *ACCV, *PRIM, *COF, *TRC;  // TRC [EPB][6][5][N2] (ResCfg::STR), else nullptr
   __device__ __forceinline__ explicit ResSmem(double* sm)
-      : ACCV(sm), PRIM(sm + EPB * AS), COF(sm + EPB * AS + EPB * 6 * N3) {}
+      : ACCV(sm), PRIM(sm + EPB * AS), COF(sm + EPB * AS + EPB * 6 * N3),
+        TRC(ResCfg<N>::STR ? sm + EPB * AS + EPB * 15 * N3 : nullptr) {}
 };
 
 // the staging blocks of batch e0 (pure copies: node primitives of u~ and 0.5 C)
 template <int N>
 __device__ __forceinline__ void res_stage_blocks(const ResParams& P, const ResSmem<N>& S, int e0, int nb,
-                                                 StageBlock (&blk)[2]) {
-  constexpr int N3 = N * N * N;
+                                                 StageBlock (&blk)[3]) {
+  constexpr int N2 = N * N, N3 = N * N * N;
   blk[0] = {S.PRIM, P.ut_vol + (size_t)e0 * 6 * N3, nb * 6 * N3};
   blk[1] = {S.COF, P.cof + (size_t)e0 * 9 * N3, nb * 9 * N3};
+  blk[2] = {S.TRC, P.traces + (size_t)e0 * 30 * N2, ResCfg<N>::STR ? nb * 30 * N2 : 0};
 }
 
 template <int N, int KM>
@@ -186,9 +198,9 @@ __device__ __forceinline__ void res_batch(const ResParams& P, const ResOps<N>& O
   PHASE_START();
   __shared__ unsigned long long bar;
   {
-    StageBlock blk[2];
+    StageBlock blk[3];
     res_stage_blocks<N>(P, S, e0, nb, blk);
-    stage_issue<2>(blk, &bar);
+    stage_issue<3>(blk, &bar);
   }
   __syncthreads();
   stage_wait(&bar);
@@ -240,7 +252,8 @@ __device__ __forceinline__ void res_lines(const ResParams& P, const ResOps<N>& O
       // Through the hybrid loop only the two traces, the face's half-scaled
       // bundle and its halved cofactor column stay live (the primitives are
       // recomputed after it), which keeps the flux chains out of local memory.
-      const double* tr = P.traces + ((size_t)e * 6 + f) * 5 * N2 + k;
+      const double* tr = ResCfg<N>::STR ? S.TRC + (b * 6 + f) * 5 * N2 + k
+                                        : P.traces + ((size_t)e * 6 + f) * 5 * N2 + k;
       const double* nt = nullptr;
       {  // neighbour across face f (geometry.hpp:24-29), its face f^1, same node k
         const int mm = P.m;
@@ -286,8 +299,7 @@ __device__ __forceinline__ void res_lines(const ResParams& P, const ResOps<N>& O
 #pragma unroll 1
       for (int a = 0; a < N; ++a) {
         const int ia = lbase + a * stride;
-        const PrimH pa{Pd[ia], Pd[N3 + ia], Pd[2 * N3 + ia], Pd[3 * N3 + ia],
-                       Pd[4 * N3 + ia], Pd[5 * N3 + ia]};
+        const PrimH pa = load_prim(Pd, N3, ia);
         double fl[NS];
         d_flux_h<(KM != 0)>(pa, pfh, Ch[(0 + dir) * N3 + ia] + ch0, Ch[(3 + dir) * N3 + ia] + ch1,
                             Ch[(6 + dir) * N3 + ia] + ch2, fl);
