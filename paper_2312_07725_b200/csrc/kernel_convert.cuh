@@ -27,12 +27,12 @@ struct ConvCfg {
 // The three passes of op over the staged block S (in place); the zeta pass
 // also writes its results to out when WRITE (consecutive threads, consecutive
 // nodes), and keeps them in S when KEEP.
-template <int N, bool WRITE, bool KEEP>
+template <int N, bool WRITE, bool KEEP, class Team = CtaTeam>
 __device__ __forceinline__ void conv_passes(const double (&op)[N * N], double* S, double* __restrict__ out,
-                                            int e0, int nb) {
+                                            int e0, int nb, const Team& tm = Team{}) {
   using Cfg = ConvCfg<N>;
   constexpr int N2 = Cfg::N2, N3 = Cfg::N3, LINES = Cfg::LINES;
-  const int tid = threadIdx.x, nthr = blockDim.x;
+  const int tid = tm.tid(), nthr = tm.nthr();
 #pragma unroll
   for (int D = 0; D < 3; ++D) {
     const int stride = D == 0 ? 1 : (D == 1 ? N : N2);
@@ -53,18 +53,19 @@ __device__ __forceinline__ void conv_passes(const double (&op)[N * N], double* S
         if (D == 2 && WRITE) out[((size_t)(e0 + b) * 5 + s) * N3 + base + row * N2] = acc;
       }
     }
-    if (D < 2 || KEEP) __syncthreads();
+    if (D < 2 || KEEP) tm.sync();
   }
 }
 
 // lambda_max = max(|u| + a) over the admissible nodes of the [nb][5][N3]
 // block S (synchronised by the caller) into *lam (atomicMax on the bits);
 // every thread of the CTA calls it
-template <int N>
-__device__ __forceinline__ void conv_lambda(const double* S, int nb, double gamma, unsigned long long* lam) {
+template <int N, class Team = CtaTeam>
+__device__ __forceinline__ void conv_lambda(const double* S, int nb, double gamma, unsigned long long* lam,
+                                            const Team& tm = Team{}) {
   constexpr int N3 = N * N * N;
   double lm = 0.0;
-  for (int it = threadIdx.x; it < nb * N3; it += blockDim.x) {
+  for (int it = tm.tid(); it < nb * N3; it += tm.nthr()) {
     const int b = it / N3, q = it - b * N3;
     double uu[NS];
 #pragma unroll
@@ -91,7 +92,8 @@ __global__ void __launch_bounds__(ConvCfg<N>::THREADS)
   constexpr int N3 = Cfg::N3, EPB = Cfg::EPB;
   constexpr bool LAM = MODE != 0;
   extern __shared__ __align__(128) double S[];
-  const int e0 = e_begin + blockIdx.x * EPB;
+  dbg_kernel_entry(S);
+  const int e0 = e_begin + NSFR_BID * EPB;
   const int nb = min(EPB, e_end - e0);
   __shared__ unsigned long long bar;
   {

@@ -128,8 +128,9 @@ __global__ void __launch_bounds__(256) k_dg_states(DgStateParams P, DgOps<NP, NQ
   using Cfg = DgCfg<NP, NQ>;
   constexpr int P3 = Cfg::P3, Q2 = Cfg::Q2, Q3 = Cfg::Q3, EPB = Cfg::EPB;
   extern __shared__ __align__(128) double sm[];
+  dbg_kernel_entry(sm);
   const int tid = threadIdx.x, nthr = blockDim.x;
-  const int e0 = blockIdx.x * EPB, nb = min(EPB, P.E - e0), nbs = nb * 5;
+  const int e0 = NSFR_BID * EPB, nb = min(EPB, P.E - e0), nbs = nb * 5;
   double* U = sm;                            // [EPB*5][P3]
   double* T1 = U + EPB * 5 * P3;             // [EPB*5][NQ NP NP]
   double* T2 = T1 + EPB * 5 * NQ * NP * NP;  // [EPB*5][NQ NQ NP]
@@ -234,8 +235,9 @@ __global__ void __launch_bounds__(256, 2) k_dg_residual(DgResParams P, DgOps<NP,
   constexpr int P3 = Cfg::P3, Q2 = Cfg::Q2, Q3 = Cfg::Q3, EPB = Cfg::EPB;
   constexpr int VS = 5 * Q3, FS = 30 * Q2;
   extern __shared__ __align__(128) double sm[];
+  dbg_kernel_entry(sm);
   const int tid = threadIdx.x, nthr = blockDim.x;
-  const int e0 = blockIdx.x * EPB, nb = min(EPB, P.E - e0), nbs = nb * 5;
+  const int e0 = NSFR_BID * EPB, nb = min(EPB, P.E - e0), nbs = nb * 5;
   double* U = sm;                    // [EPB*5][P3]
   double* CH = U + EPB * 5 * P3;     // [EPB][9][Q3]
   double* WJ = CH + EPB * 9 * Q3;    // [EPB][Q3]

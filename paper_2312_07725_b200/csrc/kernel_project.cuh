@@ -120,15 +120,15 @@ __device__ __forceinline__ void face_contract(const double (&bp)[2 * N], const d
 // S2-S5 for the nb elements whose state u_q (volume quadrature nodes) sits in
 // shared memory A ([EPB*5][N3], synchronised by the caller). B, V: [EPB*5][N3] scratch;
 // F: [3][EPB*5][2][N2] face scratch. Shared by K1 and the fused K3 (kernel_update.cuh).
-template <int N>
+template <int N, int EPB = ProjCfg<N>::EPB, class Team = CtaTeam>
 __device__ __forceinline__ void proj_core(const ProjParams& P, const ProjOps<N>& O, int e0, int nb,
-                                          double* A, double* B, double* V, double* F) {
+                                          double* A, double* B, double* V, double* F, const Team& tm = Team{}) {
   using Cfg = ProjCfg<N>;
-  constexpr int N2 = Cfg::N2, N3 = Cfg::N3, EPB = Cfg::EPB;
+  constexpr int N2 = Cfg::N2, N3 = Cfg::N3;
   double* F0 = F;                   // [EPB*5][2][N2] dir-0 face v~ (index j + N k)
   double* F1 = F0 + EPB * 10 * N2;  // [EPB*5][2][N2] dir-1 face v~ (index i + N k)
   double* F2 = F1 + EPB * 10 * N2;  // [EPB*5][2][N2] dir-2 face v~ (index i + N j)
-  const int tid = threadIdx.x, nthr = blockDim.x;
+  const int tid = tm.tid(), nthr = tm.nthr();
   const double g = P.gamma;
   const int nbs = nb * 5;
   PHASE_START();
@@ -171,15 +171,15 @@ __device__ __forceinline__ void proj_core(const ProjParams& P, const ProjOps<N>&
     for (int o = 16; o > 0; o >>= 1) lam = fmax(lam, __shfl_xor_sync(0xffffffffu, lam, o));
     if ((tid & 31) == 0 && lam > 0.0) atomicMax(P.lam, dbl_bits(lam));
   }
-  __syncthreads();
+  tm.sync();
   // S3 v_hat = Pi^3 v_q: only the entropy diagnostic (-v_hat . R) needs it
   if (P.vhat) {
     line_pass<N, 0, false>(O.proj, V, A, O.bsol, nullptr, nbs, tid, nthr);
-    __syncthreads();
+    tm.sync();
     line_pass<N, 1, false>(O.proj, A, B, O.bsol, nullptr, nbs, tid, nthr);
-    __syncthreads();
+    tm.sync();
     line_pass<N, 2, false>(O.proj, B, A, O.bsol, nullptr, nbs, tid, nthr);
-    __syncthreads();
+    tm.sync();
     double* dst = P.vhat + (size_t)e0 * 5 * N3;
     for (int i = tid; i < nb * 5 * N3; i += nthr) dst[i] = A[i];
   }
@@ -189,7 +189,7 @@ __device__ __forceinline__ void proj_core(const ProjParams& P, const ProjOps<N>&
   face_contract<N, 0>(O.bp, V, F0, nbs, tid, nthr);
   face_contract<N, 1>(O.bp, V, F1, nbs, tid, nthr);
   face_contract<N, 2>(O.bp, V, F2, nbs, tid, nthr);
-  __syncthreads();
+  tm.sync();
   PHASE_MARK(12);
   // S5 u~ = u(v~) at the face nodes
   for (int it = tid; it < nb * 6 * N2; it += nthr) {
@@ -247,14 +247,15 @@ __device__ __forceinline__ void proj_batch(const ProjParams& P, const ProjOps<N>
 template <int N, bool HAT = false>
 __global__ void __launch_bounds__(ProjCfg<N>::THREADS) k_project(ProjParams P, ProjOps<N> O, int ahead) {
   extern __shared__ __align__(128) double sm[];
+  dbg_kernel_entry(sm);
   constexpr int EPB = ProjCfg<N>::EPB, N3 = N * N * N;
   const int nbatch = (P.E - P.e_begin + EPB - 1) / EPB;
-  const long long pb = static_cast<long long>(blockIdx.x) + ahead;
+  const long long pb = static_cast<long long>(NSFR_BID) + ahead;
   if (threadIdx.x == 0 && pb < nbatch) {
     const int e0 = P.e_begin + pb * EPB, nb = min(EPB, P.E - e0);
     l2_prefetch(P.u + (size_t)e0 * 5 * N3, (size_t)nb * 5 * N3 * sizeof(double));
   }
-  proj_batch<N, HAT>(P, O, P.e_begin + blockIdx.x * EPB, sm);
+  proj_batch<N, HAT>(P, O, P.e_begin + NSFR_BID * EPB, sm);
 }
 
 }  // namespace nsfr_b200

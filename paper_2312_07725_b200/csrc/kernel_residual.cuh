@@ -269,6 +269,7 @@ __device__ __forceinline__ void res_lines(const ResParams& P, const ResOps<N>& O
             kl = (kl + P.nz) % P.nz;
           }
         }
+        NSFR_DASSERT(i >= 0 && i < mm && j >= 0 && j < mm && kl >= 0 && kl < P.nz && e < P.E);
         if (!nt) nt = P.traces + (((size_t)(i + mm * (j + mm * kl))) * 6 + (f ^ 1)) * 5 * N2 + k;
       }
       double uf[NS], un[NS];  // loaded now: their latency hides behind the hybrid loop
@@ -366,10 +367,11 @@ template <int N, int KM = 0>
 __global__ void __launch_bounds__(ResCfg<N>::THREADS, ResCfg<N>::MINB)
     k_residual(ResParams P, ResOps<N> O, int ahead) {
   extern __shared__ __align__(128) double sm[];
+  dbg_kernel_entry(sm);
   constexpr int EPB = ResCfg<N>::EPB;
-  const long long pe = P.e_begin + (static_cast<long long>(blockIdx.x) + ahead) * EPB;
+  const long long pe = P.e_begin + (static_cast<long long>(NSFR_BID) + ahead) * EPB;
   if (pe < P.E) res_prefetch<N>(P, static_cast<int>(pe), threadIdx.x);
-  res_batch<N, KM>(P, O, P.e_begin + blockIdx.x * EPB, sm);
+  res_batch<N, KM>(P, O, P.e_begin + NSFR_BID * EPB, sm);
 }
 
 }  // namespace nsfr_b200

@@ -167,10 +167,14 @@ __device__ __forceinline__ void upd_prefetch(const UpdParams& P, int e0, int tid
 // change): IDM: M = Pi~^T chi^T = I as well, so lift + first half of the WA
 // inverse reduce to the pointwise face injection and 1/(w J) (same fma order);
 // IDF: the RK stages also skip the final three (chi Pi~) passes.
-template <int N, bool IDM, bool IDF, bool OUT>
-__device__ __forceinline__ void upd_batch(const UpdParams& P, const UpdOps<N>& O, int e0, double* sm) {
-  using Cfg = UpdCfg<N>;
-  constexpr int N2 = Cfg::N2, N3 = Cfg::N3, EPB = Cfg::EPB;
+// One team (the CTA; team-generic so a warp could own an element) runs the tail for its nb <=
+// EPB elements e0.. in its shared region sm, with its own staging barrier bar.
+// NT: threads per team (compile time: the RK-operand preload depth).
+template <int N, int EPB, int NT, class Team, bool IDM, bool IDF, bool OUT>
+__device__ __forceinline__ void upd_batch(const UpdParams& P, const UpdOps<N>& O, int e0, int nb, double* sm,
+                                          unsigned long long* bar_p, const Team& tm) {
+  constexpr int N2 = N * N, N3 = N * N * N;
+  constexpr int LPT = (EPB * 5 * N2 + NT - 1) / NT;  // epilogue lines per thread
   constexpr int VS = 5 * N3, FS = 30 * N2;  // element strides of the volume / face regions
   double* R0 = sm;                 // vol, then Pi~^T R, then u_{s+1}
   double* R1 = R0 + EPB * VS;
@@ -179,24 +183,22 @@ __device__ __forceinline__ void upd_batch(const UpdParams& P, const UpdOps<N>& O
   double* R4 = R3 + EPB * FS;      // [b][G1 | G2 | H2] (10 N2 each)
   double* WJ = R4 + EPB * FS;
   const TailOps<N>& T = O.t;
-  const int tid = threadIdx.x, nthr = blockDim.x;
-  const int nb = min(EPB, P.pj.E - e0);
+  const int tid = tm.tid(), nthr = tm.nthr();
   const int nbs = nb * 5;
   PHASE_START();
-  __shared__ unsigned long long bar;
   {
     const StageBlock blk[3] = {{R0, P.vol + (size_t)e0 * VS, nb * VS},
                                {R3, P.facc + (size_t)e0 * FS, nb * FS},
                                {WJ, P.wj + (size_t)e0 * N3, nb * N3}};
-    stage_issue<3>(blk, &bar);
+    stage_issue<3>(blk, bar_p, tm);
   }
-  __syncthreads();
+  tm.sync();
   // RK operands of the final pass (zeta lines, same mapping), loaded ahead so
   // their latency hides behind the passes in between
-  double pre_un[Cfg::LPT][N], pre_acc[Cfg::LPT][N];
+  double pre_un[LPT][N], pre_acc[LPT][N];
   auto preload = [&]() {
 #pragma unroll
-    for (int j = 0; j < Cfg::LPT; ++j) {
+    for (int j = 0; j < LPT; ++j) {
       const int it = tid + j * nthr;
 #pragma unroll
       for (int c = 0; c < N; ++c) pre_un[j][c] = pre_acc[j][c] = 0.0;
@@ -215,8 +217,8 @@ __device__ __forceinline__ void upd_batch(const UpdParams& P, const UpdOps<N>& O
   // them; measured K3 -7.6% at p=5, +0.5% at p=4)
   constexpr bool LATE = N >= 6;
   if constexpr (!LATE) preload();
-  stage_wait(&bar);
-  __syncthreads();
+  stage_wait(bar_p);
+  tm.sync();
   PHASE_MARK(8);
 
   if (IDM && !P.dS) {
@@ -235,59 +237,59 @@ __device__ __forceinline__ void upd_batch(const UpdParams& P, const UpdOps<N>& O
       v = fma(T.bm[N + k], fb[20 * N2 + N2 + i + N * j], v);
       R0[it] = v * WJ[b * N3 + q];
     }
-    __syncthreads();
+    tm.sync();
   } else if (!P.dS) {
     // Pi~^T S9 in three fused passes; 1/(w J) in the last
     tail_pass<N, 0, true, false>(T.M, T.bm, R3, FS, R0, VS, R1, VS, WJ, nbs, tid, nthr);
     tail_face_pass<N, 0>(T.M, R3 + 10 * N2, FS, R4, FS, nb, face_vt<N>(tid, nthr, 0), nthr);
     tail_face_pass<N, 0>(T.M, R3 + 20 * N2, FS, R4 + 10 * N2, FS, nb, face_vt<N>(tid, nthr, nb * 10 * N), nthr);
-    __syncthreads();
+    tm.sync();
     tail_pass<N, 1, true, false>(T.M, T.bm, R4, FS, R1, VS, R2, VS, WJ, nbs, tid, nthr);
     tail_face_pass<N, 1>(T.M, R4 + 10 * N2, FS, R4 + 20 * N2, FS, nb, face_vt<N>(tid, nthr, 0), nthr);
-    __syncthreads();
+    tm.sync();
     tail_pass<N, 2, true, true>(T.M, T.bm, R4 + 20 * N2, FS, R2, VS, R0, VS, WJ, nbs, tid, nthr);
-    __syncthreads();
+    tm.sync();
   } else {
     // entropy diagnostic: R = S9 explicitly (chi^T, bound_sol), -v_hat . R, then Pi~^T
     tail_pass<N, 0, true, false>(T.it, T.bs, R3, FS, R0, VS, R1, VS, WJ, nbs, tid, nthr);
     tail_face_pass<N, 0>(T.it, R3 + 10 * N2, FS, R4, FS, nb, face_vt<N>(tid, nthr, 0), nthr);
     tail_face_pass<N, 0>(T.it, R3 + 20 * N2, FS, R4 + 10 * N2, FS, nb, face_vt<N>(tid, nthr, nb * 10 * N), nthr);
-    __syncthreads();
+    tm.sync();
     tail_pass<N, 1, true, false>(T.it, T.bs, R4, FS, R1, VS, R2, VS, WJ, nbs, tid, nthr);
     tail_face_pass<N, 1>(T.it, R4 + 10 * N2, FS, R4 + 20 * N2, FS, nb, face_vt<N>(tid, nthr, 0), nthr);
-    __syncthreads();
+    tm.sync();
     tail_pass<N, 2, true, false>(T.it, T.bs, R4 + 20 * N2, FS, R2, VS, R0, VS, WJ, nbs, tid, nthr);
-    __syncthreads();
+    tm.sync();
     for (int it = tid; it < nbs * N3; it += nthr) R1[it] = P.vhat[(size_t)e0 * VS + it] * R0[it];
-    __syncthreads();
+    tm.sync();
     if (tid < nb) {
       double s = 0.0;
       for (int r = 0; r < VS; ++r) s += R1[tid * VS + r];
       P.dS[e0 + tid] = -s;
     }
-    __syncthreads();
+    tm.sync();
     tail_pass<N, 0, false, false>(T.frt, T.bs, nullptr, 0, R0, VS, R1, VS, WJ, nbs, tid, nthr);
-    __syncthreads();
+    tm.sync();
     tail_pass<N, 1, false, false>(T.frt, T.bs, nullptr, 0, R1, VS, R2, VS, WJ, nbs, tid, nthr);
-    __syncthreads();
+    tm.sync();
     tail_pass<N, 2, false, true>(T.frt, T.bs, nullptr, 0, R2, VS, R0, VS, WJ, nbs, tid, nthr);
-    __syncthreads();
+    tm.sync();
   }
   PHASE_MARK(9);
   if constexpr (LATE) preload();
   // second half of S10: Pi~ along xi, eta
   if constexpr (!IDF) {
     tail_pass<N, 0, false, false>(T.fr, T.bs, nullptr, 0, R0, VS, R1, VS, WJ, nbs, tid, nthr);
-    __syncthreads();
+    tm.sync();
     tail_pass<N, 1, false, false>(T.fr, T.bs, nullptr, 0, R1, VS, R2, VS, WJ, nbs, tid, nthr);
-    __syncthreads();
+    tm.sync();
   }
   // Pi~ along zeta, negate, RK stage epilogue (zeta lines: coalesced across the
   // warp); u_{s+1} also lands in R0 for the projection below
   const double dt = P.stage ? *P.dt : 0.0;
   const double hdt = 0.5 * dt, sdt = dt / 6.0;
 #pragma unroll
-  for (int j = 0; j < Cfg::LPT; ++j) {
+  for (int j = 0; j < LPT; ++j) {
     const int it = tid + j * nthr;
     if (it >= nbs * N2) break;
     const int bsi = it / N2, l = it - bsi * N2;
@@ -342,20 +344,20 @@ __device__ __forceinline__ void upd_batch(const UpdParams& P, const UpdOps<N>& O
     }
   }
   if (P.stage == 0) return;
-  __syncthreads();
+  tm.sync();
   PHASE_MARK(10);
   if constexpr (OUT) {
     // the state leaves for the host: u_hat = Pi^3 u_{n+1} (kernel_convert's
     // passes, same bits as k_convert_lines) and adaptive_dt's lambda of it,
     // instead of a projection the next (uploaded) state would replace
-    conv_passes<N, true, true>(O.p.proj, R0, P.uhat_out, e0, nb);
+    conv_passes<N, true, true, Team>(O.p.proj, R0, P.uhat_out, e0, nb, tm);
     if (P.lam_out) {
-      conv_passes<N, false, true>(O.p.chi, R0, nullptr, e0, nb);
-      conv_lambda<N>(R0, nb, P.pj.gamma, P.lam_out);
+      conv_passes<N, false, true, Team>(O.p.chi, R0, nullptr, e0, nb, tm);
+      conv_lambda<N, Team>(R0, nb, P.pj.gamma, P.lam_out, tm);
     }
     return;
   }
-  proj_core<N>(P.pj, O.p, e0, nb, R0, R1, R2, R3);
+  proj_core<N, EPB, Team>(P.pj, O.p, e0, nb, R0, R1, R2, R3, tm);
 }
 
 // One batch per CTA with look-ahead L2 prefetch (see k_residual).
@@ -363,10 +365,14 @@ template <int N, bool IDM = false, bool IDF = false, bool OUT = false>
 __global__ void __launch_bounds__(UpdCfg<N>::THREADS, UpdCfg<N>::MINB)
     k_update(UpdParams P, UpdOps<N> O, int ahead) {
   extern __shared__ __align__(128) double sm[];
+  dbg_kernel_entry(sm);
   constexpr int EPB = UpdCfg<N>::EPB;
-  const long long pe = P.pj.e_begin + (static_cast<long long>(blockIdx.x) + ahead) * EPB;
+  __shared__ unsigned long long bar;
+  const long long pe = P.pj.e_begin + (static_cast<long long>(NSFR_BID) + ahead) * EPB;
   if (pe < P.pj.E) upd_prefetch<N>(P, static_cast<int>(pe), threadIdx.x);
-  upd_batch<N, IDM, IDF, OUT>(P, O, P.pj.e_begin + blockIdx.x * EPB, sm);
+  const int e0 = P.pj.e_begin + NSFR_BID * EPB;
+  upd_batch<N, EPB, UpdCfg<N>::THREADS, CtaTeam, IDM, IDF, OUT>(P, O, e0, min(EPB, P.pj.E - e0), sm, &bar,
+                                                                 CtaTeam{});
 }
 
 }  // namespace nsfr_b200

@@ -101,6 +101,14 @@ struct DeviceGuard {
   DeviceGuard& operator=(const DeviceGuard&) = delete;
 };
 
+// Blocking copy ordered on the context's (non-blocking) stream: a plain
+// cudaMemcpy runs on the legacy stream, which does NOT wait for work queued on
+// a cudaStreamNonBlocking stream (nor does that work wait for it).
+cudaError_t copy_sync(cudaStream_t st, void* dst, const void* src, size_t bytes, cudaMemcpyKind kind) {
+  cudaError_t e = cudaMemcpyAsync(dst, src, bytes, kind, st);
+  return e == cudaSuccess ? cudaStreamSynchronize(st) : e;
+}
+
 size_t nsol(const nsfr_gpu_ctx* c) { return static_cast<size_t>(c->N) * c->N * c->N; }
 size_t state_count(const nsfr_gpu_ctx* c) { return static_cast<size_t>(c->E) * NS * nsol(c); }
 size_t nquad(const nsfr_gpu_ctx* c) { return static_cast<size_t>(c->NQ) * c->NQ * c->NQ; }
@@ -342,23 +350,24 @@ int launch_update(nsfr_gpu_ctx* ctx, int stage, bool entropy, const double* vhat
   P.uhat_out = uhat_out;
   P.lam_out = lam_out;
   if (int rc = set_attrs<N>(ctx)) return rc;
-  const int grid = (P.pj.E - ea + UpdCfg<N>::EPB - 1) / UpdCfg<N>::EPB;
   ev_begin(ctx, 3);
-  if (uhat_out && ctx->chi_pi_identity)
-    k_update<N, true, true, true><<<grid, UpdCfg<N>::THREADS, UpdCfg<N>::SMEM, ctx->st>>>(
-        P, upd_ops<N>(ctx, stage), ctx->ahead_upd);
-  else if (uhat_out)
-    k_update<N, false, false, true><<<grid, UpdCfg<N>::THREADS, UpdCfg<N>::SMEM, ctx->st>>>(
-        P, upd_ops<N>(ctx, stage), ctx->ahead_upd);
-  else if (ctx->chi_pi_identity && stage > 0)
-    k_update<N, true, true><<<grid, UpdCfg<N>::THREADS, UpdCfg<N>::SMEM, ctx->st>>>(
-        P, upd_ops<N>(ctx, stage), ctx->ahead_upd);
-  else if (ctx->chi_pi_identity && !entropy)
-    k_update<N, true, false><<<grid, UpdCfg<N>::THREADS, UpdCfg<N>::SMEM, ctx->st>>>(
-        P, upd_ops<N>(ctx, stage), ctx->ahead_upd);
-  else
-    k_update<N><<<grid, UpdCfg<N>::THREADS, UpdCfg<N>::SMEM, ctx->st>>>(P, upd_ops<N>(ctx, stage),
-                                                                        ctx->ahead_upd);
+  const UpdOps<N> O = upd_ops<N>(ctx, stage);
+  // variant: 0 general, 1 c_DG identity M (+ entropy-free stage 0), 2 identity M and final passes,
+  // 3 streamed stage 4 (u_hat out), 4 streamed stage 4 with the identity
+  const int var = uhat_out ? (ctx->chi_pi_identity ? 4 : 3)
+                           : (ctx->chi_pi_identity && stage > 0 ? 2 : (ctx->chi_pi_identity && !entropy ? 1 : 0));
+  {
+    using C = UpdCfg<N>;
+    const int grid = (P.pj.E - ea + C::EPB - 1) / C::EPB;
+    const int a = ctx->ahead_upd;
+    switch (var) {
+      case 4: k_update<N, true, true, true><<<grid, C::THREADS, C::SMEM, ctx->st>>>(P, O, a); break;
+      case 3: k_update<N, false, false, true><<<grid, C::THREADS, C::SMEM, ctx->st>>>(P, O, a); break;
+      case 2: k_update<N, true, true><<<grid, C::THREADS, C::SMEM, ctx->st>>>(P, O, a); break;
+      case 1: k_update<N, true, false><<<grid, C::THREADS, C::SMEM, ctx->st>>>(P, O, a); break;
+      default: k_update<N><<<grid, C::THREADS, C::SMEM, ctx->st>>>(P, O, a);
+    }
+  }
   ev_end(ctx);
   ++ctx->launches;
   CK(cudaGetLastError());
@@ -918,7 +927,15 @@ int nsfr_gpu_create(const nsfr_gpu_setup* setup, nsfr_gpu_ctx** out) {
   const size_t ns = state_count(ctx), n3 = static_cast<size_t>(ctx->E) * nquad(ctx);
   const size_t ntr = static_cast<size_t>(ctx->E) * 6 * NS * ctx->NQ * ctx->NQ;
   const size_t nscr = static_cast<size_t>(ctx->E) * NS * std::max(nsol(ctx), nquad(ctx));
-  auto alloc = [&](double** p, size_t n) { return cudaMalloc(p, sizeof(double) * std::max<size_t>(n, 1)); };
+  auto alloc = [&](double** p, size_t n) {
+    cudaError_t e = cudaMalloc(p, sizeof(double) * std::max<size_t>(n, 1));
+#ifdef NSFR_DEBUG_CHECKS
+    // NaN bytes, on the context stream (stream-ordered before every use; the
+    // legacy-stream cudaMemset would not be ordered with the non-blocking ctx->st)
+    if (e == cudaSuccess) e = cudaMemsetAsync(*p, 0xff, sizeof(double) * std::max<size_t>(n, 1), ctx->st);
+#endif
+    return e;
+  };
   if (cudaMalloc(&ctx->d_tab, sizeof(DevTables)) || alloc(&ctx->d_un, ns) || alloc(&ctx->d_vol, nscr) ||
       alloc(&ctx->d_acc, ns) || alloc(&ctx->d_rhs, ns) || alloc(&ctx->d_utv, 6 * n3) ||
       alloc(&ctx->d_tr, ntr) || alloc(&ctx->d_facc, ntr) || alloc(&ctx->d_cof, 9 * n3) || alloc(&ctx->d_jac, n3) ||
@@ -994,9 +1011,9 @@ int nsfr_gpu_create(const nsfr_gpu_setup* setup, nsfr_gpu_ctx** out) {
         }
         wj[static_cast<size_t>(e) * N3 + q] = 1.0 / (w * J);  // K2 multiplies by 1/(w J)
       }
-    if (cudaMemcpy(ctx->d_cof, cof.data(), sizeof(double) * cof.size(), cudaMemcpyHostToDevice) ||
-        cudaMemcpy(ctx->d_jac, setup->jac_vol, sizeof(double) * n3, cudaMemcpyHostToDevice) ||
-        cudaMemcpy(ctx->d_wj, wj.data(), sizeof(double) * n3, cudaMemcpyHostToDevice)) {
+    if (copy_sync(ctx->st, ctx->d_cof, cof.data(), sizeof(double) * cof.size(), cudaMemcpyHostToDevice) ||
+        copy_sync(ctx->st, ctx->d_jac, setup->jac_vol, sizeof(double) * n3, cudaMemcpyHostToDevice) ||
+        copy_sync(ctx->st, ctx->d_wj, wj.data(), sizeof(double) * n3, cudaMemcpyHostToDevice)) {
       ctx->msg = "nsfr_gpu_create: metric upload failed";
       return fail(NSFR_E_CUDA);
     }
@@ -1080,10 +1097,10 @@ int nsfr_gpu_get_metrics(nsfr_gpu_ctx* ctx, double* jac, double* cof) {
   const size_t n3 = static_cast<size_t>(ctx->E) * nquad(ctx);
   const int N3 = static_cast<int>(nquad(ctx));
   CK(cudaStreamSynchronize(ctx->st));
-  if (jac) CK(cudaMemcpy(jac, ctx->d_jac, sizeof(double) * n3, cudaMemcpyDeviceToHost));
+  if (jac) CK(copy_sync(ctx->st, jac, ctx->d_jac, sizeof(double) * n3, cudaMemcpyDeviceToHost));
   if (cof) {
     std::vector<double> c(9 * n3);
-    CK(cudaMemcpy(c.data(), ctx->d_cof, sizeof(double) * c.size(), cudaMemcpyDeviceToHost));
+    CK(copy_sync(ctx->st, c.data(), ctx->d_cof, sizeof(double) * c.size(), cudaMemcpyDeviceToHost));
     for (int e = 0; e < ctx->E; ++e)
       for (int q = 0; q < N3; ++q)
         for (int k = 0; k < 9; ++k)
@@ -1214,8 +1231,8 @@ int nsfr_gpu_rhs(nsfr_gpu_ctx* ctx, double* dudt, double* entropy_change) {
     if (int rc = allreduce_sum(ctx, ctx->d_red, 1)) return rc;
   }
   if (int rc = sync_check(ctx)) return rc;
-  if (dudt) CK(cudaMemcpy(dudt, ctx->d_rhs, sizeof(double) * state_count(ctx), cudaMemcpyDeviceToHost));
-  if (ent) CK(cudaMemcpy(entropy_change, ctx->d_red, sizeof(double), cudaMemcpyDeviceToHost));
+  if (dudt) CK(copy_sync(ctx->st, dudt, ctx->d_rhs, sizeof(double) * state_count(ctx), cudaMemcpyDeviceToHost));
+  if (ent) CK(copy_sync(ctx->st, entropy_change, ctx->d_red, sizeof(double), cudaMemcpyDeviceToHost));
   return NSFR_OK;
 }
 
@@ -1227,7 +1244,7 @@ int nsfr_gpu_entropy_change(nsfr_gpu_ctx* ctx, double* out) {
 int nsfr_gpu_get_traces(nsfr_gpu_ctx* ctx, double* traces) {
   DeviceGuard dev_guard_(ctx);
   CK(cudaStreamSynchronize(ctx->st));
-  CK(cudaMemcpy(traces, ctx->d_tr, sizeof(double) * ctx->E * 6 * NS * ctx->NQ * ctx->NQ,
+  CK(copy_sync(ctx->st, traces, ctx->d_tr, sizeof(double) * ctx->E * 6 * NS * ctx->NQ * ctx->NQ,
                 cudaMemcpyDeviceToHost));
   return NSFR_OK;
 }
@@ -1613,7 +1630,7 @@ int nsfr_gpu_l2_error(nsfr_gpu_ctx* ctx, int kind, double out2[2]) {
   if (int rc = allreduce_sum(ctx, ctx->d_red, 2)) return rc;
   if (int rc = sync_check(ctx)) return rc;
   double h[2];
-  CK(cudaMemcpy(h, ctx->d_red, sizeof h, cudaMemcpyDeviceToHost));
+  CK(copy_sync(ctx->st, h, ctx->d_red, sizeof h, cudaMemcpyDeviceToHost));
   out2[0] = std::sqrt(h[0]);
   out2[1] = std::sqrt(h[1]);
   return NSFR_OK;
@@ -1633,7 +1650,7 @@ static int totals(nsfr_gpu_ctx* ctx, double out6[NTOT]) {
   CK(cudaGetLastError());
   if (int rc = allreduce_sum(ctx, ctx->d_red, NTOT)) return rc;
   if (int rc = sync_check(ctx)) return rc;
-  CK(cudaMemcpy(out6, ctx->d_red, sizeof(double) * NTOT, cudaMemcpyDeviceToHost));
+  CK(copy_sync(ctx->st, out6, ctx->d_red, sizeof(double) * NTOT, cudaMemcpyDeviceToHost));
   return NSFR_OK;
 }
 
@@ -1706,8 +1723,8 @@ int nsfr_gpu_residual(nsfr_gpu_ctx* ctx, double* dudt, double* entropy_change) {
     if (int rc = allreduce_sum(ctx, ctx->d_red, 1)) return rc;
   }
   if (int rc = sync_check(ctx)) return rc;
-  if (dudt) CK(cudaMemcpy(dudt, ctx->d_rhs, sizeof(double) * state_count(ctx), cudaMemcpyDeviceToHost));
-  if (ent) CK(cudaMemcpy(entropy_change, ctx->d_red, sizeof(double), cudaMemcpyDeviceToHost));
+  if (dudt) CK(copy_sync(ctx->st, dudt, ctx->d_rhs, sizeof(double) * state_count(ctx), cudaMemcpyDeviceToHost));
+  if (ent) CK(copy_sync(ctx->st, entropy_change, ctx->d_red, sizeof(double), cudaMemcpyDeviceToHost));
   return NSFR_OK;
 }
 
@@ -1773,7 +1790,7 @@ int nsfr_gpu_ke_volume(nsfr_gpu_ctx* ctx, double* out) {
   CK(cudaGetLastError());
   if (int rc = allreduce_sum(ctx, ctx->d_red, 1)) return rc;
   if (int rc = sync_check(ctx)) return rc;
-  CK(cudaMemcpy(out, ctx->d_red, sizeof(double), cudaMemcpyDeviceToHost));
+  CK(copy_sync(ctx->st, out, ctx->d_red, sizeof(double), cudaMemcpyDeviceToHost));
   return NSFR_OK;
 }
 
@@ -1798,7 +1815,7 @@ int nsfr_gpu_ke_total(nsfr_gpu_ctx* ctx, double* out) {
   ++ctx->launches;
   if (int rc = allreduce_sum(ctx, ctx->d_red, 1)) return rc;
   if (int rc = sync_check(ctx)) return rc;
-  CK(cudaMemcpy(out, ctx->d_red, sizeof(double), cudaMemcpyDeviceToHost));
+  CK(copy_sync(ctx->st, out, ctx->d_red, sizeof(double), cudaMemcpyDeviceToHost));
   return NSFR_OK;
 }
 

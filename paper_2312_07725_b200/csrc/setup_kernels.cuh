@@ -133,8 +133,9 @@ __device__ __forceinline__ void tp3_rt(const double* A, int rows, int g, const d
 
 __global__ void k_metrics(MetricParams P) {
   extern __shared__ double sm[];
+  dbg_kernel_entry(sm);
   const DevTables& T = *P.tab;
-  const int e = blockIdx.x;
+  const int e = NSFR_BID;
   if (e >= P.E) return;
   const int tid = threadIdx.x, nthr = blockDim.x;
   const int g = T.g, nq = T.nq, G3 = g * g * g, N3 = nq * nq * nq;
@@ -232,8 +233,9 @@ struct InitParams {
 
 __global__ void k_init(InitParams P) {
   extern __shared__ double sm[];
+  dbg_kernel_entry(sm);
   const DevTables& T = *P.tab;
-  const int e = blockIdx.x;
+  const int e = NSFR_BID;
   if (e >= P.E) return;
   const int tid = threadIdx.x, nthr = blockDim.x;
   const int g = T.g, np = T.np, G3 = g * g * g, S3 = np * np * np;
@@ -270,8 +272,9 @@ __global__ void k_init(InitParams P) {
 // for n_q = n_p). One CTA per element, 5 states.
 __global__ void k_convert(const DevTables* tab, const double* in, double* out, int E, int to_quad) {
   extern __shared__ double sm[];
+  dbg_kernel_entry(sm);
   const DevTables& T = *tab;
-  const int e = blockIdx.x;
+  const int e = NSFR_BID;
   if (e >= E) return;
   const int tid = threadIdx.x, nthr = blockDim.x;
   const int np = T.np, nq = T.nq;
@@ -304,8 +307,9 @@ struct L2Params {
 
 __global__ void k_l2(L2Params P) {
   extern __shared__ double sm[];
+  dbg_kernel_entry(sm);
   const DevTables& T = *P.tab;
-  const int e = blockIdx.x;
+  const int e = NSFR_BID;
   if (e >= P.E) return;
   const int tid = threadIdx.x, nthr = blockDim.x;
   const int g = T.g, n = T.nq, G3 = g * g * g, N3 = n * n * n;
@@ -384,7 +388,7 @@ __global__ void k_totals(const DevTables* tab, const double* u, const double* ja
                          double* part, int E) {
   __shared__ double red[NTOT][128];
   const DevTables& T = *tab;
-  const int e = blockIdx.x;
+  const int e = NSFR_BID;
   if (e >= E) return;
   const int tid = threadIdx.x, nthr = blockDim.x;  // nthr <= 128
   const int n = T.nq, N3 = n * n * n;
@@ -419,7 +423,7 @@ __global__ void k_totals(const DevTables* tab, const double* u, const double* ja
 // v_KE = (-|v|^2/2, v_x, v_y, v_z, 0). Fixed-order sums.
 __global__ void k_ke_dot(const double* u, const double* vol, int N3, double* part, int E) {
   __shared__ double red[128];
-  const int e = blockIdx.x;
+  const int e = NSFR_BID;
   if (e >= E) return;
   const int tid = threadIdx.x, nthr = blockDim.x;  // nthr <= 128
   const double* ue = u + (size_t)e * NS * N3;
@@ -445,8 +449,9 @@ __global__ void k_ke_dot(const double* u, const double* vol, int N3, double* par
 // euler.cpp:83-87), for the KE change diagnostic. One CTA per element.
 __global__ void k_ke_vars(const DevTables* tab, const double* uq, double* vhat, int E) {
   extern __shared__ double sm[];
+  dbg_kernel_entry(sm);
   const DevTables& T = *tab;
-  const int e = blockIdx.x;
+  const int e = NSFR_BID;
   if (e >= E) return;
   const int tid = threadIdx.x, nthr = blockDim.x;
   const int n = T.nq, N3 = n * n * n;  // n_q = n_p

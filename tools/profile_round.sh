@@ -26,6 +26,8 @@ for k in $KERNELS; do
     "ncu --set full --import-source on --clock-control none -k regex:$k -s $skip -c 1 $CMD" \
     $OUT/$k.md > /dev/null 2>&1
   python tools/ncu_ops_by_line.py /tmp/full_$k.ncu-rep 40 > $OUT/${k}_ops_by_line.txt 2>&1
+  python tools/ncu_opcode_hist.py /tmp/full_$k.ncu-rep 40 > $OUT/${k}_opcodes.txt 2>&1
+  [ "$k" = "k_residual" ] && cp /tmp/full_$k.ncu-rep $OUT/ 2>/dev/null
   for r in barrier wait short_sb long_sb mio lg; do
     python tools/ncu_stall_by_line.py /tmp/full_$k.ncu-rep $r 10; done > $OUT/${k}_stalls_by_line.txt 2>&1
   case $k in
