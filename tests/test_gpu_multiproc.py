@@ -91,3 +91,51 @@ def test_slab_processes_match_whole_box(world):
         assert [int(x["k0"]) for x in parts] == [pkg.halo_plan(M, P_DEG, r, world)["k0"] for r in range(world)]
         # external-halo contexts carry no NCCL communicator
         assert all(int(x["comm"][0]) == 0 for x in parts)
+
+
+def _nccl_worker(rank, world, port, outdir):
+    import torch
+    import torch.distributed as dist
+
+    import paper_2312_07725_b200 as pkg
+    os.environ.update(MASTER_ADDR="127.0.0.1", MASTER_PORT=str(port))
+    dist.init_process_group("gloo", rank=rank, world_size=world)
+    torch.cuda.set_device(rank)
+    obj = [pkg.nccl_unique_id() if rank == 0 else None]
+    dist.broadcast_object_list(obj, src=0)
+    g = pkg.GpuSolver(pkg.SolverConfig(p=P_DEG, m=M, c1d=C1D, rank=rank, nranks=world, device=rank),
+                      nccl_id=obj[0])
+    comm = g.comm_info()
+    g.init_case()
+    rhs = g.rhs()
+    t = g.advance(STEPS, cfl=0.1)
+    np.savez(os.path.join(outdir, f"nccl{rank}.npz"), rhs=rhs, uq=g.get_state_q(), t=t,
+             l2=g.l2_error(), comm=np.array([comm["nccl_nranks"], comm["nccl_rank"], comm["cuda_device"]]))
+    g.close()
+    dist.barrier()
+    dist.destroy_process_group()
+
+
+def test_nccl_slabs_on_two_gpus_match_whole_box():
+    """The NCCL path between DISTINCT GPUs (one process per GPU, grouped
+    send/recv halos, lambda MAX and L2 SUM allreduces, inside the step graph):
+    gathered slabs equal the whole box bitwise. Needs >= 2 GPUs (this pool has
+    one per box, so it skips here; it runs on any multi-GPU node)."""
+    import torch
+    import torch.multiprocessing as mp
+
+    import paper_2312_07725_b200 as pkg
+    if torch.cuda.device_count() < 2:
+        pytest.skip("needs 2 GPUs")
+    world = 2
+    with tempfile.TemporaryDirectory() as d:
+        mp.spawn(_nccl_worker, args=(world, _free_port(), d), nprocs=world, join=True)
+        parts = [np.load(os.path.join(d, f"nccl{r}.npz")) for r in range(world)]
+        whole = pkg.GpuSolver(pkg.SolverConfig(p=P_DEG, m=M, c1d=C1D))
+        whole.init_case()
+        np.testing.assert_array_equal(np.concatenate([x["rhs"] for x in parts]), whole.rhs())
+        t = whole.advance(STEPS, cfl=0.1)
+        assert all(float(x["t"]) == t for x in parts)
+        np.testing.assert_array_equal(np.concatenate([x["uq"] for x in parts]), whole.get_state_q())
+        np.testing.assert_allclose(parts[0]["l2"], whole.l2_error(), rtol=1e-14)
+        assert [tuple(x["comm"][:2]) for x in parts] == [(world, r) for r in range(world)]
