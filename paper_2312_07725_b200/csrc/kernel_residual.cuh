@@ -101,7 +101,12 @@ template <int N>
 struct ResCfg {
   static constexpr int N2 = N * N, N3 = N * N * N;
   static constexpr int LINES = 3 * N2;
-  static constexpr int EPB = LINES <= 32 ? 6 : (LINES <= 64 ? 4 : 2);
+// n >= 6: one element per CTA (108 / 147 lines in 128 / 160 threads, 4 CTAs
+// per SM at p=5) beats two (224 / 320 threads, 2 CTAs): K2 p=5 -1.6%, p=6 -7%.
+#ifndef NSFR_RES_EPB_HI
+#define NSFR_RES_EPB_HI 1
+#endif
+  static constexpr int EPB = LINES <= 32 ? 6 : (LINES <= 64 ? 4 : (N >= 6 ? NSFR_RES_EPB_HI : 2));
   static constexpr int THREADS = ((EPB * LINES + 31) / 32) * 32;
   // The element's own face traces (30 N2) are staged with the rest where that
   // helps (N <= 4; measured K2 p=3 -2.4%, p=4 +1.7%): the face loop starts from shared
