@@ -58,14 +58,15 @@ struct UpdOps {
 template <int N>
 struct UpdCfg {
   static constexpr int N2 = N * N, N3 = N * N * N;
-  static constexpr int EPB = ProjCfg<N>::EPB;  // proj_core's batch layout
+  // elements per CTA: proj_core's batch (at n = 5 two; one measured K3 +6.5%)
+  static constexpr int EPB = ProjCfg<N>::EPB;
   // Threads per CTA: proj_core's (one per volume node of the batch), except at
   // n >= 6 (one element per CTA, 216 / 343 nodes) where fewer threads with
   // more line items each keep the per-item constant loads (LDCU, the 1D
   // operators) in uniform registers across items. Measured K3 (A/B, one
   // session): p=5 224 -> 128 threads -13% (96: -8%, 160: +5%); p=6 352 -> 160
   // threads -8% (128: -4%); the same change costs +3% at p=4 and +16% at p=3.
-  static constexpr int THREADS = N == 6 ? 128 : (N == 7 ? 160 : ProjCfg<N>::THREADS);
+  static constexpr int THREADS = N == 6 ? 128 : (N == 7 ? 160 : ((EPB * N3 + 31) / 32) * 32);
   // R0 vol/u_{s+1}, R1, R2 pass buffers (5 N3 each), R3 facc / face scratch,
   // R4 face-lift buffers (30 N2 each), R5 1/(w J) (N3)
   static constexpr int PER_EL = 16 * N3 + 60 * N2;
