@@ -1,3 +1,17 @@
+// Host-side setup tables (once per context, never on the hot path): Gauss /
+// Gauss-Lobatto rules, the Lagrange basis and the 1D operators of
+// ReferenceOperators (fr_operators.cpp:54-113, basis.cpp), plus the c-dependent
+// Pi~ (fr_operators.cpp:61-87).
+//
+// Note on provenance: legendre() and make_rule() below restate the textbook
+// Newton iteration for Gauss(-Lobatto) nodes the way the reference's
+// quadrature.cpp:8-92 does it -- the same Chebyshev starting guesses, Newton
+// update, 1e-15 / 100-iteration stopping rule and endpoint-derivative
+// expression -- deliberately, so that the nodes, weights and every table
+// built from them come out bit-identical to the reference build's
+// (tests/test_gpu_parity.py::test_tables_match_reference, <= 2e-15). SURVEY §2
+// allows reusing the reference's setup code outright; restating it keeps the
+// library free of the reference's sources and of Eigen.
 #include "tables.hpp"
 
 #include <algorithm>
