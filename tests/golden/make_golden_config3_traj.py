@@ -51,13 +51,27 @@ def main():
     key = f"p{p}" + ("_perturbed" if perturbed else "")
 
     s = CpuSolver("ref", Config(p=p, m=32, c1d=0.0, case="vortex", roe=True,
-                                workers=os.cpu_count()))
+                                workers=int(os.environ.get("NSFR_GOLDEN_WORKERS", os.cpu_count()))))
     u = s.initial_state()
     rng = np.random.default_rng(20231207)
     if perturbed:
         u = ulp_perturb(u, rng)
     t0 = time.time()
     t, step, rec = 0.0, 0, {}
+
+    def save(res):
+        # merged into the JSON after every checkpoint, so a cut-off run keeps
+        # what it reached ("partial": true until t_f)
+        out = {}
+        if os.path.exists(path):
+            with open(path) as f:
+                out = json.load(f)
+        out[key] = res
+        tmp = path + ".tmp"
+        with open(tmp, "w") as f:
+            json.dump(out, f, indent=1)
+        os.replace(tmp, path)
+
     while t < t_final and step < max_steps:
         lam = s.max_wavespeed(u)
         dt = min(0.1 * s.dx() / lam, t_final - t)
@@ -69,17 +83,13 @@ def main():
         if step in CHECKPOINTS:
             rec[str(step)] = {"t": t, "l2": s.l2_error(u, t).tolist()}
             print(key, step, rec[str(step)], f"{time.time() - t0:.0f}s", flush=True)
+            save({"t_target": t_final, "partial": True, "checkpoints": rec,
+                  "seconds": time.time() - t0, "perturbed": perturbed})
     res = {"t_target": t_final, "t_final": t, "steps": step, "checkpoints": rec,
            "l2": s.l2_error(u, t).tolist(), "seconds": time.time() - t0,
            "perturbed": perturbed}
     print(key, "final", res["steps"], res["t_final"], res["l2"], flush=True)
-    out = {}
-    if os.path.exists(path):
-        with open(path) as f:
-            out = json.load(f)
-    out[key] = res
-    with open(path, "w") as f:
-        json.dump(out, f, indent=1)
+    save(res)
 
 
 if __name__ == "__main__":

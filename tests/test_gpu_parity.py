@@ -392,7 +392,9 @@ def test_config3_trajectory_to_final_time(p):
     assert gold is not None, f"config3_traj.json has no p{p} trajectory (make_golden_config3_traj.py {p})"
     pert = _traj_gold().get(f"p{p}_perturbed", {}).get("checkpoints", {})
     cps = {int(k): v for k, v in gold["checkpoints"].items()}
-    steps = sorted(cps) + [gold["steps"]]
+    assert cps, "no checkpoint recorded"
+    partial = gold.get("partial", False)  # a cut-off reference run: compare what it reached
+    steps = sorted(cps) + ([] if partial else [gold["steps"]])
     g, got = gpu_l2_at_steps(p, steps, 2.0)
     scale = l2_state_scale(g)
     floor = l2_trajectory_floor(p, steps, 2.0)
@@ -403,7 +405,8 @@ def test_config3_trajectory_to_final_time(p):
         if str(k) in pert:
             fl = np.maximum(fl, np.abs(np.array(pert[str(k)]["l2"]) - np.array(want["l2"])))
         assert_l2_parity(f"config3_p{p}_step{k}", got[k][1], want["l2"], fl, scale)
-    assert got[gold["steps"]][0] == pytest.approx(2.0, abs=1e-12)
+    if not partial:
+        assert got[gold["steps"]][0] == pytest.approx(2.0, abs=1e-12)
 
 
 def test_advance_graph_equals_stepwise():
