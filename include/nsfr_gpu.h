@@ -124,7 +124,7 @@ typedef struct nsfr_gpu_halo_plan {
   int k0, k1;        /* z planes owned */
   int peer_lo;       /* rank owning plane k0-1 (periodic) */
   int peer_hi;       /* rank owning plane k1 (periodic) */
-  long long count;   /* doubles per message: m*m*5*nq*nq */
+  long long count;   /* doubles per message: m*m*6*nq*nq (6 values per face node, see below) */
 } nsfr_gpu_halo_plan;
 int nsfr_gpu_halo_plan_for(int m, int p, int rank, int nranks, nsfr_gpu_halo_plan* out);
 
@@ -146,7 +146,8 @@ int nsfr_gpu_get_time(nsfr_gpu_ctx* ctx, double* t);
 /* One residual dU/dt of the current state; dudt may be NULL (kept on device).
  * entropy_change may be NULL; else receives -sum v_hat . R (allreduced). */
 int nsfr_gpu_rhs(nsfr_gpu_ctx* ctx, double* dudt, double* entropy_change);
-/* Entropy-projected face traces of the local elements [e][6][5][nq^2]. */
+/* Entropy-projected face traces of the local elements, conservative,
+ * [e][6 faces][5][nq^2] (converted from the device's primitive form). */
 int nsfr_gpu_get_traces(nsfr_gpu_ctx* ctx, double* traces);
 
 /* One classical RK4 step; dt = cfl*dx/lambda_max (allreduced) from u_n,
@@ -215,7 +216,10 @@ int nsfr_gpu_measure_fp64_peak_ex(int device, double* tflops, double* sm_mhz);
 /* ---- Stage-level driving and external halo transport ----------------------
  * A context created with nranks > 1 but nccl_id == NULL exchanges no data
  * itself: the caller moves the z-halo planes (e.g. over MPI, or between two
- * contexts in a test). Each plane is [m*m][5][nq^2] (halo_plan.count doubles):
+ * contexts in a test). Each plane is an opaque block of halo_plan.count doubles,
+ * [m*m][6][nq^2]: the NSFR kernels keep face traces as the six primitives
+ * (rho, u, v, w, p, rho/p) of u(v~); the DG scheme uses the first 5/6 of the
+ * block for its conservative face states. Move the block as it is:
  * rank r's send_lo goes to rank r-1's recv_hi and its send_hi to rank r+1's
  * recv_lo (periodic). The driving sequence is
  *   nsfr_gpu_project;  [swap];  nsfr_gpu_residual            (one RHS), or

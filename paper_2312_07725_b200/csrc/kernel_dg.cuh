@@ -247,6 +247,7 @@ __global__ void __launch_bounds__(256, 2) k_dg_residual(DgResParams P, DgOps<NP,
   double* FACC = VOL + EPB * VS;     // [EPB][3][5][2][Q2]
   double* G = FACC + EPB * FS;       // [EPB][30 Q2]
   const double g = P.gamma;
+  const GasC gas = GasC::make(g);
   __shared__ unsigned long long bar;
   {
     const StageBlock blk[3] = {{U, P.us + (size_t)e0 * 5 * P3, nb * 5 * P3},
@@ -405,7 +406,7 @@ __global__ void __launch_bounds__(256, 2) k_dg_residual(DgResParams P, DgOps<NP,
       if (P.roe) {
         double d[NS];
         const PrimX pl = d_primx(g, ul), pr = d_primx(g, ur);
-        if (!d_roe_x(g, ul, ur, pl, pr, nrm, d)) atomicOr(P.err, ERR_ROE);
+        if (!d_roe_prim(gas, pl, pr, nrm, d)) atomicOr(P.err, ERR_ROE);
 #pragma unroll
         for (int s = 0; s < NS; ++s) fn[s] -= d[s];
       }

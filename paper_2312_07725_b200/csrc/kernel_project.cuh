@@ -20,10 +20,10 @@ namespace nsfr_b200 {
 struct ProjParams {
   const double* u;       // [E][5][N^3] stage input u_q at the volume quadrature nodes
   double* ut_vol;        // [E][6][N^3] rho,u,v,w,p,rho/p of the entropy-projected volume state
-  double* traces;        // [E][6][5][N^2]
+  double* traces;        // [E][6 faces][NTR][N^2] primitives rho,u,v,w,p,rho/p of u(v~) (physics.cuh)
   double* vhat;          // [E][5][N^3] or nullptr
-  double* send_lo;       // [m*m][5][N^2] face 4 of plane 0, or nullptr
-  double* send_hi;       // [m*m][5][N^2] face 5 of plane nz-1, or nullptr
+  double* send_lo;       // [m*m][NTR][N^2] face 4 of plane 0, or nullptr
+  double* send_hi;       // [m*m][NTR][N^2] face 5 of plane nz-1, or nullptr
   unsigned long long* lam;  // lambda_max bits or nullptr
   unsigned* err;
   int E, m, nz;          // E: end of the launched element range [e_begin, E) (the slab by default)
@@ -42,8 +42,8 @@ struct ProjOps {
 };
 
 template <int N>
-__device__ __forceinline__ bool u_of_v(const ProjOps<N>& O, double g, const double* v, double* u) {
-  return O.c35 > 0.0 ? d_entropy_to_cons_35(g, O.c35, v, u) : d_entropy_to_cons(g, v, u);
+__device__ __forceinline__ bool prim_of_v(const ProjOps<N>& O, double g, const double* v, double* q) {
+  return O.c35 > 0.0 ? d_entropy_to_prim_35(g, O.c35, v, q) : d_entropy_to_prim(g, v, q);
 }
 
 template <int N>
@@ -191,29 +191,29 @@ __device__ __forceinline__ void proj_core(const ProjParams& P, const ProjOps<N>&
   face_contract<N, 2>(O.bp, V, F2, nbs, tid, nthr);
   tm.sync();
   PHASE_MARK(12);
-  // S5 u~ = u(v~) at the face nodes
+  // S5 u~ = u(v~) at the face nodes, kept as primitives (NTR values per node)
   for (int it = tid; it < nb * 6 * N2; it += nthr) {
     const int b = it / (6 * N2), r = it - b * 6 * N2, f = r / N2, k = r - f * N2;
     const int dir = f / 2, side = f % 2;
     const double* Fd = dir == 0 ? F0 : (dir == 1 ? F1 : F2);
-    double vv[NS], uu[NS];
+    double vv[NS], qq[NTR];
 #pragma unroll
     for (int s = 0; s < NS; ++s) vv[s] = Fd[((b * 5 + s) * 2 + side) * N2 + k];
-    if (!u_of_v<N>(O, g, vv, uu)) atomicOr(P.err, ERR_STATE);
+    if (!prim_of_v<N>(O, g, vv, qq)) atomicOr(P.err, ERR_STATE);
     const int e = e0 + b;
-    double* dst = P.traces + ((size_t)e * 6 + f) * 5 * N2 + k;
+    double* dst = P.traces + ((size_t)e * 6 + f) * NTR * N2 + k;
 #pragma unroll
-    for (int s = 0; s < NS; ++s) dst[s * N2] = uu[s];
+    for (int s = 0; s < NTR; ++s) dst[s * N2] = qq[s];
     // boundary planes also go to the halo send buffers (z faces of slab contexts only)
     if ((P.send_lo && f == 4) || (P.send_hi && f == 5)) {
       const int mm = P.m * P.m, kl = e / mm, plane = e - kl * mm;
       if (f == 4 && kl == 0) {
 #pragma unroll
-        for (int s = 0; s < NS; ++s) P.send_lo[((size_t)plane * 5 + s) * N2 + k] = uu[s];
+        for (int s = 0; s < NTR; ++s) P.send_lo[((size_t)plane * NTR + s) * N2 + k] = qq[s];
       }
       if (f == 5 && kl == P.nz - 1) {
 #pragma unroll
-        for (int s = 0; s < NS; ++s) P.send_hi[((size_t)plane * 5 + s) * N2 + k] = uu[s];
+        for (int s = 0; s < NTR; ++s) P.send_hi[((size_t)plane * NTR + s) * N2 + k] = qq[s];
       }
     }
   }

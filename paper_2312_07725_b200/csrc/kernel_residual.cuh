@@ -23,29 +23,36 @@ namespace nsfr_b200 {
 // (compile-time indices and coefficients; p=3 K2 -1.6%), used for n <= 4;
 // rolled above (the unrolled code outgrows the instruction cache: p=4 +4%,
 // p=5 +1.5%; measured).
+// Running pointers (node a / node b of PRIM, their cofactor column, the line's
+// accumulator) advance by the line stride: the rolled loops carry three
+// addresses instead of rebuilding each from (lbase, stride, index) and the
+// shared window base every pair (S2R + LEA + 5 IMAD per pair in the SASS).
 #define NSFR_VOL_PAIRS_BODY                                                                    \
   {                                                                                            \
-    const int ia = lbase + a * stride;                                                         \
-    const PrimH pa{Pd[ia], Pd[N3 + ia], Pd[2 * N3 + ia], Pd[3 * N3 + ia], Pd[4 * N3 + ia],     \
-                   Pd[5 * N3 + ia]};                                                           \
-    const double ca0 = Ch[(0 + dir) * N3 + ia], ca1 = Ch[(3 + dir) * N3 + ia],                 \
-                 ca2 = Ch[(6 + dir) * N3 + ia];                                                \
+    const PrimH pa{pa_p[0], pa_p[N3], pa_p[2 * N3], pa_p[3 * N3], pa_p[4 * N3], pa_p[5 * N3]}; \
+    const double ca0 = ca_p[0], ca1 = ca_p[3 * N3], ca2 = ca_p[6 * N3];                        \
     double fa[NS] = {0.0, 0.0, 0.0, 0.0, 0.0};                                                 \
+    const double* __restrict__ pb_p = pa_p + stride;                                           \
+    const double* __restrict__ cb_p = ca_p + stride;                                           \
+    double* __restrict__ ab_p = aa_p + stride;                                                 \
     NSFR_INNER_UNROLL                                                                          \
     for (int bb = a + 1; bb < N; ++bb) {                                                       \
-      const int ib = lbase + bb * stride;                                                      \
-      const PrimH pb{Pd[ib], Pd[N3 + ib], Pd[2 * N3 + ib], Pd[3 * N3 + ib], Pd[4 * N3 + ib],   \
-                     Pd[5 * N3 + ib]};                                                         \
+      const PrimH pb{pb_p[0], pb_p[N3], pb_p[2 * N3], pb_p[3 * N3], pb_p[4 * N3], pb_p[5 * N3]}; \
       double f[NS];                                                                            \
-      d_flux_h<KE>(pa, pb, ca0 + Ch[(0 + dir) * N3 + ib], ca1 + Ch[(3 + dir) * N3 + ib],       \
-                   ca2 + Ch[(6 + dir) * N3 + ib], f);                                                 \
+      d_flux_h<KE>(pa, pb, ca0 + cb_p[0], ca1 + cb_p[3 * N3], ca2 + cb_p[6 * N3], f);          \
       const double c = wt * q[a * N + bb];                                                     \
       _Pragma("unroll") for (int s = 0; s < NS; ++s) {                                         \
         fa[s] = fma(c, f[s], fa[s]);                                                           \
-        acc[s * N3 + ib] = fma(-c, f[s], acc[s * N3 + ib]);                                    \
+        ab_p[s * N3] = fma(-c, f[s], ab_p[s * N3]);                                            \
       }                                                                                        \
+      pb_p += stride;                                                                          \
+      cb_p += stride;                                                                          \
+      ab_p += stride;                                                                          \
     }                                                                                          \
-    _Pragma("unroll") for (int s = 0; s < NS; ++s) acc[s * N3 + ia] += fa[s];                  \
+    _Pragma("unroll") for (int s = 0; s < NS; ++s) aa_p[s * N3] += fa[s];                      \
+    pa_p += stride;                                                                            \
+    ca_p += stride;                                                                            \
+    aa_p += stride;                                                                            \
   }
 
 #ifndef NSFR_UNROLL_MAXN
@@ -61,6 +68,9 @@ __device__ __forceinline__ void vol_pairs(const double* __restrict__ Pd, const d
                                           const double (&q)[N * N], double wt, int lbase,
                                           int stride, int dir) {
   constexpr int N3 = N * N * N;
+  const double* __restrict__ pa_p = Pd + lbase;
+  const double* __restrict__ ca_p = Ch + dir * N3 + lbase;
+  double* __restrict__ aa_p = acc + lbase;
   if constexpr (N <= NSFR_UNROLL_MAXN) {
 #define NSFR_INNER_UNROLL _Pragma("unroll")
 #pragma unroll
@@ -77,9 +87,9 @@ __device__ __forceinline__ void vol_pairs(const double* __restrict__ Pd, const d
 
 struct ResParams {
   const double* ut_vol;   // [E][6][N^3] half-scaled primitives of u~ (K1 / K3)
-  const double* traces;   // [E][6][5][N^2]
-  const double* halo_lo;  // [m*m][5][N^2] face 5 of plane k0-1 (nullptr: wrap locally)
-  const double* halo_hi;  // [m*m][5][N^2] face 4 of plane k1
+  const double* traces;   // [E][6 faces][NTR][N^2] primitives of u(v~) (physics.cuh)
+  const double* halo_lo;  // [m*m][NTR][N^2] face 5 of plane k0-1 (nullptr: wrap locally)
+  const double* halo_hi;  // [m*m][NTR][N^2] face 4 of plane k1
   const double* cof;      // [E][9][N^3] = 0.5 C
   double* vol;            // [E][5][N^3] volume rows
   double* facc;           // [E][3][5][2][N^2] face rows
@@ -88,6 +98,7 @@ struct ResParams {
   double gamma;
   int roe;
   int e_begin;            // first element of the launched range (a multiple of 8)
+  GasC gas;               // gamma and its reciprocals (host-formed)
 };
 
 template <int N>
@@ -108,14 +119,14 @@ struct ResCfg {
 #endif
   static constexpr int EPB = LINES <= 32 ? 6 : (LINES <= 64 ? 4 : (N >= 6 ? NSFR_RES_EPB_HI : 2));
   static constexpr int THREADS = ((EPB * LINES + 31) / 32) * 32;
-  // The element's own face traces (30 N2) are staged with the rest where that
+  // The element's own face traces (6 NTR N2) are staged with the rest where that
   // helps (N <= 4; measured K2 p=3 -2.4%, p=4 +1.7%): the face loop starts from shared
   // memory instead of waiting on a global load (K2's largest long-scoreboard
   // stall); at N = 5 the longer staging wait costs more, at N >= 6 a CTA per SM.
   static constexpr bool STR = N <= 4;
   // ACCV (3 directions x 5 N3) + node primitives (6 N3) + half cofactors (9 N3)
-  // [+ own traces 30 N2]
-  static constexpr int PER_EL = 30 * N3 + (STR ? 30 * N2 : 0);
+  // [+ own traces 6 NTR N2]
+  static constexpr int PER_EL = 30 * N3 + (STR ? 6 * NTR * N2 : 0);
   static constexpr int SMEM = EPB * PER_EL * 8;
 #ifdef NSFR_RES_MINB
   static constexpr int MINB = NSFR_RES_MINB;
@@ -128,7 +139,10 @@ struct ResCfg {
 #endif
 };
 
-// L2 prefetch of everything batch `e0` will read (issued one batch ahead).
+// L2 prefetch of everything batch `e0` will read (issued one batch ahead) by the
+// first lanes of warp 0: the three element blocks and the 6 nb neighbour face
+// blocks. (Dealing the items to every warp instead measured no gain at p=4 and
+// +8% at p=3.)
 template <int N>
 __device__ __forceinline__ void res_prefetch(const ResParams& P, int e0, int tid) {
   using Cfg = ResCfg<N>;
@@ -139,7 +153,7 @@ __device__ __forceinline__ void res_prefetch(const ResParams& P, int e0, int tid
   switch (tid) {
     case 0: l2_prefetch(P.ut_vol + (size_t)e0 * 6 * N3, nb * 6 * N3 * b8); break;
     case 1: l2_prefetch(P.cof + (size_t)e0 * 9 * N3, nb * 9 * N3 * b8); break;
-    case 2: l2_prefetch(P.traces + (size_t)e0 * 30 * N2, nb * 30 * N2 * b8); break;
+    case 2: l2_prefetch(P.traces + (size_t)e0 * 6 * NTR * N2, nb * 6 * NTR * N2 * b8); break;
     default: {  // neighbour face blocks (geometry.hpp:24-29), lanes 3.. : (element, face)
       const int j = tid - 3;
       if (j >= 6 * nb) break;
@@ -153,13 +167,13 @@ __device__ __forceinline__ void res_prefetch(const ResParams& P, int e0, int tid
         if (kl < 0 || kl >= P.nz) {
           const double* halo = kl < 0 ? P.halo_lo : P.halo_hi;
           if (halo) {
-            l2_prefetch(halo + (size_t)(i + mm * jj) * 5 * N2, 5 * N2 * b8);
+            l2_prefetch(halo + (size_t)(i + mm * jj) * NTR * N2, NTR * N2 * b8);
             break;
           }
           kl = (kl + P.nz) % P.nz;
         }
       }
-      l2_prefetch(P.traces + ((size_t)(i + mm * (jj + mm * kl)) * 6 + (f ^ 1)) * 5 * N2, 5 * N2 * b8);
+      l2_prefetch(P.traces + ((size_t)(i + mm * (jj + mm * kl)) * 6 + (f ^ 1)) * NTR * N2, NTR * N2 * b8);
     }
   }
 }
@@ -172,7 +186,7 @@ __device__ __forceinline__ void res_prefetch(const ResParams& P, int e0, int tid
 template <int N>
 struct ResSmem {
   static constexpr int N3 = N * N * N, EPB = ResCfg<N>::EPB, AS = 15 * N3;
-  double *ACCV, *PRIM, *COF, *TRC;  // TRC [EPB][6][5][N2] (ResCfg::STR), else nullptr
+  double *ACCV, *PRIM, *COF, *TRC;  // TRC [EPB][6][NTR][N2] (ResCfg::STR), else nullptr
   __device__ __forceinline__ explicit ResSmem(double* sm)
       : ACCV(sm), PRIM(sm + EPB * AS), COF(sm + EPB * AS + EPB * 6 * N3),
         TRC(ResCfg<N>::STR ? sm + EPB * AS + EPB * 15 * N3 : nullptr) {}
@@ -185,7 +199,7 @@ __device__ __forceinline__ void res_stage_blocks(const ResParams& P, const ResSm
   constexpr int N2 = N * N, N3 = N * N * N;
   blk[0] = {S.PRIM, P.ut_vol + (size_t)e0 * 6 * N3, nb * 6 * N3};
   blk[1] = {S.COF, P.cof + (size_t)e0 * 9 * N3, nb * 9 * N3};
-  blk[2] = {S.TRC, P.traces + (size_t)e0 * 30 * N2, ResCfg<N>::STR ? nb * 30 * N2 : 0};
+  blk[2] = {S.TRC, P.traces + (size_t)e0 * 6 * NTR * N2, ResCfg<N>::STR ? nb * 6 * NTR * N2 : 0};
 }
 
 template <int N, int KM>
@@ -194,20 +208,35 @@ __device__ __forceinline__ void res_lines(const ResParams& P, const ResOps<N>& O
 template <int N>
 __device__ __forceinline__ void res_writeout(const ResParams& P, int e0, int nb, const double* ACCV);
 
+// Order of a batch: thread 0 initialises the staging barrier, everybody syncs on
+// that alone, and while thread 0 issues the TMA copies (and warp 0 the L2
+// prefetch of the look-ahead batch `pe`) the other warps clear the direction
+// accumulators, so only the data's own flight time is waited for. (With the
+// barrier behind the TMA issue and the prefetch, the other four warps spent
+// 9.7% of the kernel's warp time waiting for warp 0: K2 -9% at p=4.)
 template <int N, int KM>
-__device__ __forceinline__ void res_batch(const ResParams& P, const ResOps<N>& O, int e0, double* sm) {
+__device__ __forceinline__ void res_batch(const ResParams& P, const ResOps<N>& O, int e0, long long pe,
+                                          double* sm) {
   using Cfg = ResCfg<N>;
-  constexpr int EPB = Cfg::EPB;
+  constexpr int EPB = Cfg::EPB, N3 = Cfg::N3;
   const ResSmem<N> S(sm);
   const int nb = min(EPB, P.E - e0);
   PHASE_START();
   __shared__ unsigned long long bar;
+  if (threadIdx.x == 0) mbar_init(&bar, 1);
+  __syncthreads();
   {
     StageBlock blk[3];
     res_stage_blocks<N>(P, S, e0, nb, blk);
-    stage_issue<3>(blk, &bar);
+    stage_copy<3>(blk, &bar);
   }
-  __syncthreads();
+  if (pe < P.E) res_prefetch<N>(P, static_cast<int>(pe), threadIdx.x);
+  {  // ACCV (EPB * 15 N3 doubles, 16-byte aligned) = 0
+    double2* z = reinterpret_cast<double2*>(S.ACCV);
+    constexpr int ND = EPB * 15 * N3, NZ = ND / 2;
+    for (int i = threadIdx.x; i < NZ; i += Cfg::THREADS) z[i] = make_double2(0.0, 0.0);
+    if ((ND & 1) && threadIdx.x == 0) S.ACCV[ND - 1] = 0.0;
+  }
   stage_wait(&bar);
   __syncthreads();
   PHASE_MARK(0);
@@ -243,10 +272,6 @@ __device__ __forceinline__ void res_lines(const ResParams& P, const ResOps<N>& O
     const double* __restrict__ Ch = COF + b * 9 * N3;
     double* __restrict__ acc = ACCV + b * AS + dir * 5 * N3;
     const double wt = O.wq[t1] * O.wq[t2];
-#pragma unroll
-    for (int a = 0; a < N; ++a)
-#pragma unroll
-      for (int s = 0; s < NS; ++s) acc[s * N3 + lbase + a * stride] = 0.0;
     vol_pairs<N, (KM != 0)>(Pd, Ch, acc, O.q, wt, lbase, stride, dir);
     // S7 hybrid surface pairs + S8 face flux for the two faces this line pierces
 #pragma unroll 1
@@ -257,8 +282,8 @@ __device__ __forceinline__ void res_lines(const ResParams& P, const ResOps<N>& O
       // Through the hybrid loop only the two traces, the face's half-scaled
       // bundle and its halved cofactor column stay live (the primitives are
       // recomputed after it), which keeps the flux chains out of local memory.
-      const double* tr = ResCfg<N>::STR ? S.TRC + (b * 6 + f) * 5 * N2 + k
-                                        : P.traces + ((size_t)e * 6 + f) * 5 * N2 + k;
+      const double* tr = ResCfg<N>::STR ? S.TRC + (b * 6 + f) * NTR * N2 + k
+                                        : P.traces + ((size_t)e * 6 + f) * NTR * N2 + k;
       const double* nt = nullptr;
       {  // neighbour across face f (geometry.hpp:24-29), its face f^1, same node k
         const int mm = P.m;
@@ -270,20 +295,28 @@ __device__ __forceinline__ void res_lines(const ResParams& P, const ResOps<N>& O
           kl += step;
           if (kl < 0 || kl >= P.nz) {
             const double* halo = kl < 0 ? P.halo_lo : P.halo_hi;
-            if (halo) nt = halo + (size_t)(i + mm * j) * 5 * N2 + k;
+            if (halo) nt = halo + (size_t)(i + mm * j) * NTR * N2 + k;
             kl = (kl + P.nz) % P.nz;
           }
         }
         NSFR_DASSERT(i >= 0 && i < mm && j >= 0 && j < mm && kl >= 0 && kl < P.nz && e < P.E);
-        if (!nt) nt = P.traces + (((size_t)(i + mm * (j + mm * kl))) * 6 + (f ^ 1)) * 5 * N2 + k;
+        if (!nt) nt = P.traces + (((size_t)(i + mm * (j + mm * kl))) * 6 + (f ^ 1)) * NTR * N2 + k;
       }
-      double uf[NS], un[NS];  // loaded now: their latency hides behind the hybrid loop
+      // the own and the neighbour's face state (primitives), loaded now: the
+      // neighbour's latency hides behind the hybrid loop
+      double qn[NTR];
+      PrimH pfh;
+      double rp_own;
+      {
+        double qf[NTR];
 #pragma unroll
-      for (int s = 0; s < NS; ++s) {
-        uf[s] = tr[s * N2];
-        un[s] = nt[s * N2];
+        for (int s = 0; s < NTR; ++s) {
+          qf[s] = tr[s * N2];
+          qn[s] = nt[s * N2];
+        }
+        pfh = PrimH{0.5 * qf[0], 0.5 * qf[1], 0.5 * qf[2], 0.5 * qf[3], 0.5 * qf[4], (0.5 * gm1) * qf[5]};
+        rp_own = qf[5];
       }
-      const PrimH pfh = to_half(gm1, d_primx(g, uf));
       // own face cofactor column C_f[:,dir] = sum_a bound_flux(side,a) C_a (geometry.cpp:218-226),
       // kept halved (ch = C_f/2; doubling it back is exact)
       double ch0, ch1, ch2;
@@ -302,32 +335,45 @@ __device__ __forceinline__ void res_lines(const ResParams& P, const ResOps<N>& O
         ch2 = 0.5 * cf2;
       }
       double ff[NS] = {0.0, 0.0, 0.0, 0.0, 0.0};
+      {
+        // running pointers along the line (see vol_pairs)
+        const double* __restrict__ pa_p = Pd + lbase;
+        const double* __restrict__ ca_p = Ch + dir * N3 + lbase;
+        double* __restrict__ aa_p = acc + lbase;
+        const double swt = sign * wt;
 #pragma unroll 1
-      for (int a = 0; a < N; ++a) {
-        const int ia = lbase + a * stride;
-        const PrimH pa = load_prim(Pd, N3, ia);
-        double fl[NS];
-        d_flux_h<(KM != 0)>(pa, pfh, Ch[(0 + dir) * N3 + ia] + ch0, Ch[(3 + dir) * N3 + ia] + ch1,
-                            Ch[(6 + dir) * N3 + ia] + ch2, fl);
-        const double c = sign * O.bflux[side * N + a] * wt;
+        for (int a = 0; a < N; ++a) {
+          const PrimH pa = load_prim(pa_p, N3, 0);
+          double fl[NS];
+          d_flux_h<(KM != 0)>(pa, pfh, ca_p[0] + ch0, ca_p[3 * N3] + ch1, ca_p[6 * N3] + ch2, fl);
+          const double c = swt * O.bflux[side * N + a];
 #pragma unroll
-        for (int s = 0; s < NS; ++s) {
-          acc[s * N3 + ia] = fma(c, fl[s], acc[s * N3 + ia]);
-          ff[s] = fma(-c, fl[s], ff[s]);
+          for (int s = 0; s < NS; ++s) {
+            aa_p[s * N3] = fma(c, fl[s], aa_p[s * N3]);
+            ff[s] = fma(-c, fl[s], ff[s]);
+          }
+          pa_p += stride;
+          ca_p += stride;
+          aa_p += stride;
         }
       }
       // S8 f*.n with the own unit normal and J^Gamma (geometry.cpp:227-236)
       const double v0 = sign * (2.0 * ch0), v1 = sign * (2.0 * ch1), v2 = sign * (2.0 * ch2);
-      const double jg = sqrt(v0 * v0 + v1 * v1 + v2 * v2);
-      const double ijg = 1.0 / jg;
+      const double j2 = v0 * v0 + v1 * v1 + v2 * v2;
+      const double ijg = rsqrt(j2), jg = j2 * ijg;
       const double nrm[3] = {v0 * ijg, v1 * ijg, v2 * ijg};
-      const PrimX pf = d_primx(g, uf);  // recomputed rather than kept through the loop
-      const PrimX pn = d_primx(g, un);
+      // the own primitives back from the half-scaled bundle (doubling is exact);
+      // rho/p is kept as loaded: rebuilt from the scaled grp it carries a rounding
+      // the neighbour's does not, a one-sided bias in Roe's entropy-variable jump
+      // that drifts a long run (configs[2] p=4 to t=2: L2 off by 2.6e-10 instead
+      // of 3e-11 relative)
+      const PrimX pf{2.0 * pfh.hr, 2.0 * pfh.hu, 2.0 * pfh.hv, 2.0 * pfh.hw, 2.0 * pfh.hp, rp_own, 0.0, 0.0};
+      const PrimX pn{qn[0], qn[1], qn[2], qn[3], qn[4], qn[5], 0.0, 0.0};
       double fn[NS];
       d_flux_h<(KM != 0)>(pfh, to_half(gm1, pn), nrm[0], nrm[1], nrm[2], fn);
       if (P.roe && KM == 0) {
         double d[NS];
-        if (!d_roe_x(g, uf, un, pf, pn, nrm, d)) atomicOr(P.err, ERR_ROE);
+        if (!d_roe_prim(P.gas, pf, pn, nrm, d)) atomicOr(P.err, ERR_ROE);
 #pragma unroll
         for (int s = 0; s < NS; ++s) fn[s] -= d[s];
       }
@@ -375,8 +421,7 @@ __global__ void __launch_bounds__(ResCfg<N>::THREADS, ResCfg<N>::MINB)
   dbg_kernel_entry(sm);
   constexpr int EPB = ResCfg<N>::EPB;
   const long long pe = P.e_begin + (static_cast<long long>(NSFR_BID) + ahead) * EPB;
-  if (pe < P.E) res_prefetch<N>(P, static_cast<int>(pe), threadIdx.x);
-  res_batch<N, KM>(P, O, P.e_begin + NSFR_BID * EPB, sm);
+  res_batch<N, KM>(P, O, P.e_begin + NSFR_BID * EPB, pe, sm);
 }
 
 }  // namespace nsfr_b200

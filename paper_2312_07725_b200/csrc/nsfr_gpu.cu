@@ -304,6 +304,7 @@ int launch_residual(nsfr_gpu_ctx* ctx, int km, int ea, int eb) {
   P.m = ctx->m;
   P.nz = ctx->nz;
   P.gamma = ctx->s.gamma;
+  P.gas = GasC::make(ctx->s.gamma);
   P.roe = ctx->s.roe;
   P.e_begin = ea;
   P.E = range_end(ctx, eb);
@@ -855,7 +856,7 @@ int nsfr_gpu_halo_plan_for(int m, int p, int rank, int nranks, nsfr_gpu_halo_pla
   out->k1 = static_cast<int>(static_cast<long long>(rank + 1) * m / nranks);
   out->peer_lo = (rank - 1 + nranks) % nranks;
   out->peer_hi = (rank + 1) % nranks;
-  out->count = static_cast<long long>(m) * m * NS * (p + 1) * (p + 1);
+  out->count = static_cast<long long>(m) * m * NTR * (p + 1) * (p + 1);
   return NSFR_OK;
 }
 
@@ -925,7 +926,8 @@ int nsfr_gpu_create(const nsfr_gpu_setup* setup, nsfr_gpu_ctx** out) {
     ctx->chi_pi_identity = dev < 1e-13;
   }
   const size_t ns = state_count(ctx), n3 = static_cast<size_t>(ctx->E) * nquad(ctx);
-  const size_t ntr = static_cast<size_t>(ctx->E) * 6 * NS * ctx->NQ * ctx->NQ;
+  const size_t ntr = static_cast<size_t>(ctx->E) * 6 * NS * ctx->NQ * ctx->NQ;    // face rows
+  const size_t ntrace = static_cast<size_t>(ctx->E) * 6 * NTR * ctx->NQ * ctx->NQ;  // face traces (DG: NS of NTR used)
   const size_t nscr = static_cast<size_t>(ctx->E) * NS * std::max(nsol(ctx), nquad(ctx));
   auto alloc = [&](double** p, size_t n) {
     cudaError_t e = cudaMalloc(p, sizeof(double) * std::max<size_t>(n, 1));
@@ -938,7 +940,7 @@ int nsfr_gpu_create(const nsfr_gpu_setup* setup, nsfr_gpu_ctx** out) {
   };
   if (cudaMalloc(&ctx->d_tab, sizeof(DevTables)) || alloc(&ctx->d_un, ns) || alloc(&ctx->d_vol, nscr) ||
       alloc(&ctx->d_acc, ns) || alloc(&ctx->d_rhs, ns) || alloc(&ctx->d_utv, 6 * n3) ||
-      alloc(&ctx->d_tr, ntr) || alloc(&ctx->d_facc, ntr) || alloc(&ctx->d_cof, 9 * n3) || alloc(&ctx->d_jac, n3) ||
+      alloc(&ctx->d_tr, ntrace) || alloc(&ctx->d_facc, ntr) || alloc(&ctx->d_cof, 9 * n3) || alloc(&ctx->d_jac, n3) ||
       alloc(&ctx->d_wj, n3) || alloc(&ctx->d_dS, ctx->E) || alloc(&ctx->d_part, 2 * (size_t)ctx->E) ||
       alloc(&ctx->d_red, 8) || cudaMalloc(&ctx->d_step, sizeof(StepState)) ||
       cudaMalloc(&ctx->d_err, sizeof(unsigned)) ||
@@ -962,7 +964,7 @@ int nsfr_gpu_create(const nsfr_gpu_setup* setup, nsfr_gpu_ctx** out) {
     }
     ctx->peer_lo = plan.peer_lo;
     ctx->peer_hi = plan.peer_hi;
-    ctx->halo_count = static_cast<long long>(s.m) * s.m * NS * ctx->NQ * ctx->NQ;
+    ctx->halo_count = static_cast<long long>(s.m) * s.m * NTR * ctx->NQ * ctx->NQ;
     const size_t hc = static_cast<size_t>(ctx->halo_count);
     if (alloc(&ctx->d_send_lo, hc) || alloc(&ctx->d_send_hi, hc) || alloc(&ctx->d_halo_lo, hc) ||
         alloc(&ctx->d_halo_hi, hc)) {
@@ -1244,8 +1246,27 @@ int nsfr_gpu_entropy_change(nsfr_gpu_ctx* ctx, double* out) {
 int nsfr_gpu_get_traces(nsfr_gpu_ctx* ctx, double* traces) {
   DeviceGuard dev_guard_(ctx);
   CK(cudaStreamSynchronize(ctx->st));
-  CK(copy_sync(ctx->st, traces, ctx->d_tr, sizeof(double) * ctx->E * 6 * NS * ctx->NQ * ctx->NQ,
-                cudaMemcpyDeviceToHost));
+  const size_t q2 = static_cast<size_t>(ctx->NQ) * ctx->NQ, nf = static_cast<size_t>(ctx->E) * 6;
+  if (ctx->dg) {  // the DG kernels keep conservative face states
+    CK(copy_sync(ctx->st, traces, ctx->d_tr, sizeof(double) * nf * NS * q2, cudaMemcpyDeviceToHost));
+    return NSFR_OK;
+  }
+  // NSFR traces are primitives (rho, u, v, w, p, rho/p; physics.cuh): back to
+  // the conservative [E][6][5][nq^2] the interface speaks
+  std::vector<double> prim(nf * NTR * q2);
+  CK(copy_sync(ctx->st, prim.data(), ctx->d_tr, sizeof(double) * prim.size(), cudaMemcpyDeviceToHost));
+  const double igm1 = 1.0 / (ctx->s.gamma - 1.0);
+  for (size_t f = 0; f < nf; ++f)
+    for (size_t k = 0; k < q2; ++k) {
+      const double* q = prim.data() + f * NTR * q2 + k;
+      double* u = traces + f * NS * q2 + k;
+      const double rho = q[0], vx = q[q2], vy = q[2 * q2], vz = q[3 * q2], pr = q[4 * q2];
+      u[0] = rho;
+      u[q2] = rho * vx;
+      u[2 * q2] = rho * vy;
+      u[3 * q2] = rho * vz;
+      u[4 * q2] = pr * igm1 + 0.5 * rho * (vx * vx + vy * vy + vz * vz);
+    }
   return NSFR_OK;
 }
 

@@ -440,7 +440,8 @@ class GpuSolver:
     # --- stage-level driving / external halo transport (nranks > 1, no NCCL id)
     @property
     def halo_shape(self):
-        return (self.cfg.m * self.cfg.m, 5, self.nq * self.nq)
+        # NTR = 6 values per face node (NSFR: primitives rho,u,v,w,p,rho/p; DG uses 5 of them)
+        return (self.cfg.m * self.cfg.m, 6, self.nq * self.nq)
 
     def halo_get(self):
         """The two send planes (face 4 of plane k0, face 5 of plane k1-1)."""

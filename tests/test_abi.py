@@ -40,7 +40,7 @@ def test_halo_plan_partition(m, n):
     for r in range(n):
         h = P.halo_plan(m, 4, r, n)
         assert h["peer_lo"] == (r - 1) % n and h["peer_hi"] == (r + 1) % n
-        assert h["count"] == m * m * 5 * 25
+        assert h["count"] == m * m * 6 * 25  # NTR = 6 values per face node
         assert h["k1"] > h["k0"]
         planes += list(range(h["k0"], h["k1"]))
     assert planes == list(range(m))
