@@ -124,10 +124,22 @@ struct ResCfg {
   // memory instead of waiting on a global load (K2's largest long-scoreboard
   // stall); at N = 5 the longer staging wait costs more, at N >= 6 a CTA per SM.
   static constexpr bool STR = N <= 4;
-  // ACCV (3 directions x 5 N3) + node primitives (6 N3) + half cofactors (9 N3)
+  // The line phase is bound by the shared-memory data pipe (ncu: l1tex data-pipe
+  // wavefronts at 93% of peak), and with the natural thread -> line order its
+  // 64-bit accesses cost 1.65 wavefronts per ideal one (bank conflicts between
+  // the lines of a half-warp). MAPPED: the lines are dealt to the lanes by a
+  // table and the direction accumulators are padded (element stride AS,
+  // direction offsets DOFF) so that the same accesses cost ~1.2x
+  // (tools/k2_bankmap.c anneals both against the bank model, which reproduces
+  // the measured 1.65x). Results are bitwise unchanged: which lane runs a line
+  // does not enter its arithmetic.
+  static constexpr bool MAPPED = N == 5;
+  static constexpr int DOFF1 = MAPPED ? 631 : 5 * N3, DOFF2 = MAPPED ? 1264 : 10 * N3;
+  static constexpr int AS = MAPPED ? 1901 : 15 * N3;   // doubles per element of ACCV
+  static constexpr int ACC_ALL = (EPB * AS + 1) / 2 * 2;  // ACCV region (even: PRIM stays 16-byte aligned)
+  // ACCV (3 directions x 5 N3, padded) + node primitives (6 N3) + half cofactors (9 N3)
   // [+ own traces 6 NTR N2]
-  static constexpr int PER_EL = 30 * N3 + (STR ? 6 * NTR * N2 : 0);
-  static constexpr int SMEM = EPB * PER_EL * 8;
+  static constexpr int SMEM = (ACC_ALL + EPB * (15 * N3 + (STR ? 6 * NTR * N2 : 0))) * 8;
 #ifdef NSFR_RES_MINB
   static constexpr int MINB = NSFR_RES_MINB;
 #else
@@ -182,14 +194,14 @@ __device__ __forceinline__ void res_prefetch(const ResParams& P, int e0, int tid
 //   0 the residual; 1 volume rows only (S6); 2 all rows (S6-S8) without Roe.
 
 // Shared-memory carve-up of one batch: ACCV [EPB][3][5][N3] direction
-// accumulators, PRIM [EPB][6][N3] half-scaled primitives, COF [EPB][9][N3] 0.5 C.
+// accumulators (element stride AS, direction offsets 0 / DOFF1 / DOFF2), PRIM [EPB][6][N3] half-scaled primitives, COF [EPB][9][N3] 0.5 C.
 template <int N>
 struct ResSmem {
-  static constexpr int N3 = N * N * N, EPB = ResCfg<N>::EPB, AS = 15 * N3;
+  static constexpr int N3 = N * N * N, EPB = ResCfg<N>::EPB, ACC_ALL = ResCfg<N>::ACC_ALL;
   double *ACCV, *PRIM, *COF, *TRC;  // TRC [EPB][6][NTR][N2] (ResCfg::STR), else nullptr
   __device__ __forceinline__ explicit ResSmem(double* sm)
-      : ACCV(sm), PRIM(sm + EPB * AS), COF(sm + EPB * AS + EPB * 6 * N3),
-        TRC(ResCfg<N>::STR ? sm + EPB * AS + EPB * 15 * N3 : nullptr) {}
+      : ACCV(sm), PRIM(sm + ACC_ALL), COF(sm + ACC_ALL + EPB * 6 * N3),
+        TRC(ResCfg<N>::STR ? sm + ACC_ALL + EPB * 15 * N3 : nullptr) {}
 };
 
 // the staging blocks of batch e0 (pure copies: node primitives of u~ and 0.5 C)
@@ -200,6 +212,28 @@ __device__ __forceinline__ void res_stage_blocks(const ResParams& P, const ResSm
   blk[0] = {S.PRIM, P.ut_vol + (size_t)e0 * 6 * N3, nb * 6 * N3};
   blk[1] = {S.COF, P.cof + (size_t)e0 * 9 * N3, nb * 9 * N3};
   blk[2] = {S.TRC, P.traces + (size_t)e0 * 6 * NTR * N2, ResCfg<N>::STR ? nb * 6 * NTR * N2 : 0};
+}
+
+// Thread -> line table of the MAPPED configurations (tools/k2_bankmap.c; code =
+// b << 12 | dir << 8 | t2 << 4 | t1, 0xffff = idle lane). N = 5, two elements
+// per CTA: 1.197 wavefronts per ideal one in the bank model (natural order 1.656).
+__device__ const unsigned short g_res_map5[160] = {
+    0x0013, 0x0004, 0x0210, 0x0214, 0x0201, 0x0212, 0xffff, 0x0033, 0x0031, 0x0203, 0x0230, 0x0042, 0x0022, 0x0024, 0x0020, 0x0223,
+    0xffff, 0x1212, 0x0140, 0x1103, 0xffff, 0x0244, 0x0131, 0x1130, 0x0211, 0x1114, 0x0233, 0x0231, 0xffff, 0x0220, 0x1141, 0x0224,
+    0x0141, 0x0114, 0x1231, 0x1120, 0x0221, 0x0243, 0x1140, 0x1124, 0x1111, 0x1213, 0xffff, 0x0232, 0x1113, 0x1133, 0x0234, 0xffff,
+    0x0204, 0x0041, 0x0023, 0x0014, 0x0012, 0xffff, 0x0222, 0x0213, 0x0001, 0xffff, 0x0242, 0x0202, 0x0200, 0x0030, 0x0003, 0x0021,
+    0x1100, 0x1134, 0x1123, 0x1142, 0x1131, 0x1101, 0xffff, 0x1102, 0x1121, 0x1112, 0x1144, 0x1110, 0x1132, 0x1143, 0xffff, 0x1122,
+    0x1033, 0x1031, 0x1023, 0x1010, 0x1014, 0x1012, 0x1020, 0x1011, 0x1004, 0x1013, 0x1022, 0x1034, 0x1030, 0x1024, 0x1021, 0x1032,
+    0x0113, 0x0130, 0x0123, 0x0132, 0x0122, 0x0133, 0x0144, 0x0110, 0x0134, 0x0143, 0x0101, 0x0120, 0x0111, 0x0103, 0x0100, 0x0142,
+    0x0112, 0x1232, 0x1104, 0x0032, 0x1233, 0x1204, 0x0102, 0x0241, 0x0240, 0x1043, 0x0104, 0x1242, 0x0124, 0x0121, 0x1203, 0x1241,
+    0x0040, 0x0002, 0x0043, 0x0034, 0x0010, 0x1044, 0x0000, 0x1042, 0x1000, 0x1003, 0x0011, 0x0044, 0x1040, 0x1002, 0x1001, 0x1041,
+    0x1211, 0x1240, 0x1234, 0x1224, 0x1221, 0x1220, 0x1244, 0x1222, 0x1200, 0x1214, 0x1201, 0x1202, 0x1243, 0x1210, 0x1230, 0x1223};
+// A global (L1-cached) table, not a __constant__ one: every lane reads its own
+// entry, which the constant cache would serialise 32 ways.
+template <int N>
+__device__ __forceinline__ unsigned res_line_map(int tid) {
+  static_assert(N == 5, "no line map for this degree");
+  return __ldg(&g_res_map5[tid]);
 }
 
 template <int N, int KM>
@@ -218,7 +252,7 @@ template <int N, int KM>
 __device__ __forceinline__ void res_batch(const ResParams& P, const ResOps<N>& O, int e0, long long pe,
                                           double* sm) {
   using Cfg = ResCfg<N>;
-  constexpr int EPB = Cfg::EPB, N3 = Cfg::N3;
+  constexpr int EPB = Cfg::EPB;
   const ResSmem<N> S(sm);
   const int nb = min(EPB, P.E - e0);
   PHASE_START();
@@ -231,11 +265,10 @@ __device__ __forceinline__ void res_batch(const ResParams& P, const ResOps<N>& O
     stage_copy<3>(blk, &bar);
   }
   if (pe < P.E) res_prefetch<N>(P, static_cast<int>(pe), threadIdx.x);
-  {  // ACCV (EPB * 15 N3 doubles, 16-byte aligned) = 0
+  {  // ACCV (an even number of doubles, 16-byte aligned) = 0
     double2* z = reinterpret_cast<double2*>(S.ACCV);
-    constexpr int ND = EPB * 15 * N3, NZ = ND / 2;
+    constexpr int NZ = Cfg::ACC_ALL / 2;
     for (int i = threadIdx.x; i < NZ; i += Cfg::THREADS) z[i] = make_double2(0.0, 0.0);
-    if ((ND & 1) && threadIdx.x == 0) S.ACCV[ND - 1] = 0.0;
   }
   stage_wait(&bar);
   __syncthreads();
@@ -252,25 +285,40 @@ __device__ __forceinline__ void res_lines(const ResParams& P, const ResOps<N>& O
                                           const ResSmem<N>& S) {
   using Cfg = ResCfg<N>;
   constexpr int N2 = Cfg::N2, N3 = Cfg::N3, LINES = Cfg::LINES;
-  constexpr int AS = 15 * N3;     // element stride of ACCV
+  constexpr int AS = Cfg::AS;     // element stride of ACCV
   double* ACCV = S.ACCV;
   const double* PRIM = S.PRIM;
   const double* COF = S.COF;
   const int tid = threadIdx.x;
   const double g = P.gamma, gm1 = g - 1.0;
 
-  // ---- line phase: one thread owns one 1D line (dir, t1, t2) ----
-  const int lb = tid / LINES;
-  const int ll = tid - lb * LINES;
-  const int ldir = ll / N2, lrem = ll - ldir * N2;
+  // ---- line phase: one thread owns one 1D line (b, dir, t1, t2) ----
+  int lb, ldir, lt1, lt2;
+  if constexpr (Cfg::MAPPED) {
+    const unsigned code = res_line_map<N>(tid);  // 0xffff: idle lane
+    lb = code >> 12;                             // 15 for an idle lane (>= nb)
+    ldir = (code >> 8) & 3;
+    lt2 = (code >> 4) & 15;
+    lt1 = code & 15;
+    // opaque from here on: under register pressure the compiler otherwise
+    // re-reads the table inside the pair loops to rebuild dir
+    asm volatile("" : "+r"(lb), "+r"(ldir), "+r"(lt1), "+r"(lt2));
+  } else {
+    lb = tid / LINES;
+    const int ll = tid - lb * LINES;
+    ldir = ll / N2;
+    const int lrem = ll - ldir * N2;
+    lt1 = lrem % N;
+    lt2 = lrem / N;
+  }
   if (lb < nb) {
-    const int b = lb, e = e0 + b, dir = ldir, t1 = lrem % N, t2 = lrem / N;
+    const int b = lb, e = e0 + b, dir = ldir, t1 = lt1, t2 = lt2;
     const int stride = dir == 0 ? 1 : (dir == 1 ? N : N2);
     const int lbase = dir == 0 ? N * (t1 + N * t2) : (dir == 1 ? t1 + N2 * t2 : t1 + N * t2);
     // disjoint shared-memory regions: lets the next pair's loads pass this pair's stores
     const double* __restrict__ Pd = PRIM + b * 6 * N3;
     const double* __restrict__ Ch = COF + b * 9 * N3;
-    double* __restrict__ acc = ACCV + b * AS + dir * 5 * N3;
+    double* __restrict__ acc = ACCV + b * AS + (dir == 0 ? 0 : (dir == 1 ? Cfg::DOFF1 : Cfg::DOFF2));
     const double wt = O.wq[t1] * O.wq[t2];
     vol_pairs<N, (KM != 0)>(Pd, Ch, acc, O.q, wt, lbase, stride, dir);
     // S7 hybrid surface pairs + S8 face flux for the two faces this line pierces
@@ -390,7 +438,7 @@ __device__ __forceinline__ void res_lines(const ResParams& P, const ResOps<N>& O
 // volume rows: sum of the three direction accumulators
 template <int N>
 __device__ __forceinline__ void res_writeout(const ResParams& P, int e0, int nb, const double* ACCV) {
-  constexpr int N3 = N * N * N, AS = 15 * N3;
+  constexpr int N3 = N * N * N, AS = ResCfg<N>::AS, D1 = ResCfg<N>::DOFF1, D2 = ResCfg<N>::DOFF2;
   // compile-time trip count: every thread's shared loads issue before its sums
   constexpr int T = ResCfg<N>::THREADS, ITS = (ResCfg<N>::EPB * 5 * N3 + T - 1) / T;
   const int lim = nb * 5 * N3;
@@ -400,7 +448,7 @@ __device__ __forceinline__ void res_writeout(const ResParams& P, int e0, int nb,
     const int it = threadIdx.x + j * T;
     const int b = it / (5 * N3), r = it - b * 5 * N3;
     const double* a0 = ACCV + b * AS;
-    v[j] = it < lim ? a0[r] + a0[5 * N3 + r] + a0[10 * N3 + r] : 0.0;
+    v[j] = it < lim ? a0[r] + a0[D1 + r] + a0[D2 + r] : 0.0;
   }
 #pragma unroll
   for (int j = 0; j < ITS; ++j) {
