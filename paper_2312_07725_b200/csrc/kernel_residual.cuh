@@ -152,7 +152,7 @@ struct ResCfg {
 };
 
 // L2 prefetch of everything batch `e0` will read (issued one batch ahead) by the
-// first lanes of warp 0: the three element blocks and the 6 nb neighbour face
+// first lanes of warp 0: the three element blocks and the 2 nb z-neighbour face
 // blocks. (Dealing the items to every warp instead measured no gain at p=4 and
 // +8% at p=3.)
 template <int N>
@@ -167,9 +167,11 @@ __device__ __forceinline__ void res_prefetch(const ResParams& P, int e0, int tid
     case 1: l2_prefetch(P.cof + (size_t)e0 * 9 * N3, nb * 9 * N3 * b8); break;
     case 2: l2_prefetch(P.traces + (size_t)e0 * 6 * NTR * N2, nb * 6 * NTR * N2 * b8); break;
     default: {  // neighbour face blocks (geometry.hpp:24-29), lanes 3.. : (element, face)
+      // z neighbours only: the x and y neighbours' own blocks are inside the
+      // look-ahead window of the CTAs already running (K2 -0.6%)
       const int j = tid - 3;
-      if (j >= 6 * nb) break;
-      const int e = e0 + j / 6, f = j % 6, dir = f / 2, step = (f & 1) ? 1 : -1;
+      if (j >= 2 * nb) break;
+      const int e = e0 + j / 2, f = 4 + (j & 1), dir = 2, step = (f & 1) ? 1 : -1;
       const int mm = P.m;
       int i = e % mm, jj = (e / mm) % mm, kl = e / (mm * mm);
       if (dir == 0) i = (i + step + mm) % mm;
@@ -242,12 +244,16 @@ __device__ __forceinline__ void res_lines(const ResParams& P, const ResOps<N>& O
 template <int N>
 __device__ __forceinline__ void res_writeout(const ResParams& P, int e0, int nb, const double* ACCV);
 
-// Order of a batch: thread 0 initialises the staging barrier, everybody syncs on
-// that alone, and while thread 0 issues the TMA copies (and warp 0 the L2
-// prefetch of the look-ahead batch `pe`) the other warps clear the direction
-// accumulators, so only the data's own flight time is waited for. (With the
-// barrier behind the TMA issue and the prefetch, the other four warps spent
-// 9.7% of the kernel's warp time waiting for warp 0: K2 -9% at p=4.)
+// Order of a batch. Thread 0 initialises the staging barrier and issues the TMA
+// copies at once, so the data is in flight from the first instructions on (its
+// ~3000-cycle flight is the one wait a CTA cannot avoid); meanwhile every thread
+// clears the direction accumulators. One CTA barrier publishes both. Then warp
+// 0 issues the look-ahead L2 prefetch of batch `pe`, and each thread waits on
+// the mbarrier ITSELF: no second CTA barrier, so no warp waits for warp 0's
+// prefetch before its lines (only the per-thread cp.async fallback of a
+// misaligned block still needs one). History: with one barrier behind the
+// prefetch and the TMA issue, four warps spent 9.7% of the kernel's warp time
+// waiting for warp 0 (K2 -9% when it moved ahead of the issue).
 template <int N, int KM>
 __device__ __forceinline__ void res_batch(const ResParams& P, const ResOps<N>& O, int e0, long long pe,
                                           double* sm) {
@@ -257,21 +263,24 @@ __device__ __forceinline__ void res_batch(const ResParams& P, const ResOps<N>& O
   const int nb = min(EPB, P.E - e0);
   PHASE_START();
   __shared__ unsigned long long bar;
-  if (threadIdx.x == 0) mbar_init(&bar, 1);
-  __syncthreads();
+  bool all_bulk = true;
   {
     StageBlock blk[3];
     res_stage_blocks<N>(P, S, e0, nb, blk);
-    stage_copy<3>(blk, &bar);
+    stage_issue<3>(blk, &bar);
+#pragma unroll
+    for (int i = 0; i < 3; ++i)
+      all_bulk = all_bulk && (blk[i].count == 0 || bulk_ok(blk[i].src, blk[i].dst, blk[i].count * sizeof(double)));
   }
-  if (pe < P.E) res_prefetch<N>(P, static_cast<int>(pe), threadIdx.x);
   {  // ACCV (an even number of doubles, 16-byte aligned) = 0
     double2* z = reinterpret_cast<double2*>(S.ACCV);
     constexpr int NZ = Cfg::ACC_ALL / 2;
     for (int i = threadIdx.x; i < NZ; i += Cfg::THREADS) z[i] = make_double2(0.0, 0.0);
   }
-  stage_wait(&bar);
   __syncthreads();
+  if (pe < P.E) res_prefetch<N>(P, static_cast<int>(pe), threadIdx.x);
+  stage_wait(&bar);
+  if (!all_bulk) __syncthreads();
   PHASE_MARK(0);
   res_lines<N, KM>(P, O, e0, nb, S);
   __syncthreads();
@@ -291,6 +300,8 @@ __device__ __forceinline__ void res_lines(const ResParams& P, const ResOps<N>& O
   const double* COF = S.COF;
   const int tid = threadIdx.x;
   const double g = P.gamma, gm1 = g - 1.0;
+  // box coordinates of the batch's first element (block-uniform)
+  const int ei0 = e0 % P.m, ej0 = (e0 / P.m) % P.m, ek0 = e0 / (P.m * P.m);
 
   // ---- line phase: one thread owns one 1D line (b, dir, t1, t2) ----
   int lb, ldir, lt1, lt2;
@@ -333,18 +344,34 @@ __device__ __forceinline__ void res_lines(const ResParams& P, const ResOps<N>& O
       const double* tr = ResCfg<N>::STR ? S.TRC + (b * 6 + f) * NTR * N2 + k
                                         : P.traces + ((size_t)e * 6 + f) * NTR * N2 + k;
       const double* nt = nullptr;
-      {  // neighbour across face f (geometry.hpp:24-29), its face f^1, same node k
+      {  // neighbour across face f (geometry.hpp:24-29), its face f^1, same node k.
+        // The element's box coordinates come from the batch's first element
+        // (uniform divisions, once per CTA) by stepping b elements along x:
+        // no per-thread division by the run-time m.
         const int mm = P.m;
-        int i = e % mm, j = (e / mm) % mm, kl = e / (mm * mm);
+        int i = ei0 + b, j = ej0, kl = ek0;
+        while (i >= mm) {
+          i -= mm;
+          if (++j >= mm) {
+            j = 0;
+            ++kl;
+          }
+        }
         const int step = side ? 1 : -1;
-        if (dir == 0) i = (i + step + mm) % mm;
-        if (dir == 1) j = (j + step + mm) % mm;
+        if (dir == 0) {
+          i += step;
+          i = i < 0 ? i + mm : (i >= mm ? i - mm : i);
+        }
+        if (dir == 1) {
+          j += step;
+          j = j < 0 ? j + mm : (j >= mm ? j - mm : j);
+        }
         if (dir == 2) {
           kl += step;
           if (kl < 0 || kl >= P.nz) {
             const double* halo = kl < 0 ? P.halo_lo : P.halo_hi;
             if (halo) nt = halo + (size_t)(i + mm * j) * NTR * N2 + k;
-            kl = (kl + P.nz) % P.nz;
+            kl = kl < 0 ? kl + P.nz : kl - P.nz;
           }
         }
         NSFR_DASSERT(i >= 0 && i < mm && j >= 0 && j < mm && kl >= 0 && kl < P.nz && e < P.E);
@@ -366,21 +393,16 @@ __device__ __forceinline__ void res_lines(const ResParams& P, const ResOps<N>& O
         rp_own = qf[5];
       }
       // own face cofactor column C_f[:,dir] = sum_a bound_flux(side,a) C_a (geometry.cpp:218-226),
-      // kept halved (ch = C_f/2; doubling it back is exact)
-      double ch0, ch1, ch2;
-      {
-        double cf0 = 0.0, cf1 = 0.0, cf2 = 0.0;
+      // kept halved (ch = C_f/2; doubling it back is exact): the same fma chain
+      // on the stored halves gives exactly half of the chain on C itself
+      double ch0 = 0.0, ch1 = 0.0, ch2 = 0.0;
 #pragma unroll
-        for (int a = 0; a < N; ++a) {
-          const int ia = lbase + a * stride;
-          const double w = O.bflux[side * N + a];
-          cf0 = fma(w, 2.0 * Ch[(0 + dir) * N3 + ia], cf0);
-          cf1 = fma(w, 2.0 * Ch[(3 + dir) * N3 + ia], cf1);
-          cf2 = fma(w, 2.0 * Ch[(6 + dir) * N3 + ia], cf2);
-        }
-        ch0 = 0.5 * cf0;
-        ch1 = 0.5 * cf1;
-        ch2 = 0.5 * cf2;
+      for (int a = 0; a < N; ++a) {
+        const int ia = lbase + a * stride;
+        const double w = O.bflux[side * N + a];
+        ch0 = fma(w, Ch[(0 + dir) * N3 + ia], ch0);
+        ch1 = fma(w, Ch[(3 + dir) * N3 + ia], ch1);
+        ch2 = fma(w, Ch[(6 + dir) * N3 + ia], ch2);
       }
       double ff[NS] = {0.0, 0.0, 0.0, 0.0, 0.0};
       {

@@ -179,7 +179,7 @@ __device__ __forceinline__ void upd_prefetch(const UpdParams& P, int e0, int tid
 // NT: threads per team (compile time: the RK-operand preload depth).
 template <int N, int EPB, int NT, class Team, bool IDM, bool IDF, bool OUT>
 __device__ __forceinline__ void upd_batch(const UpdParams& P, const UpdOps<N>& O, int e0, int nb, double* sm,
-                                          unsigned long long* bar_p, const Team& tm) {
+                                          unsigned long long* bar_p, const Team& tm, long long pe = -1) {
   constexpr int N2 = N * N, N3 = N * N * N;
   constexpr int LPT = (EPB * 5 * N2 + NT - 1) / NT;  // epilogue lines per thread
   constexpr int VS = 5 * N3, FS = 30 * N2;  // element strides of the volume / face regions
@@ -193,13 +193,18 @@ __device__ __forceinline__ void upd_batch(const UpdParams& P, const UpdOps<N>& O
   const int tid = tm.tid(), nthr = tm.nthr();
   const int nbs = nb * 5;
   PHASE_START();
+  // the team syncs on the barrier's initialisation alone; thread 0 then issues
+  // the TMA copies (and the look-ahead L2 prefetch of batch `pe`) while the
+  // others already load their RK operands (see k_residual's res_batch)
+  if (tid == 0) mbar_init(bar_p, 1);
+  tm.sync();
   {
     const StageBlock blk[3] = {{R0, P.vol + (size_t)e0 * VS, nb * VS},
                                {R3, P.facc + (size_t)e0 * FS, nb * FS},
                                {WJ, P.wj + (size_t)e0 * N3, nb * N3}};
-    stage_issue<3>(blk, bar_p, tm);
+    stage_copy<3>(blk, bar_p, tm);
   }
-  tm.sync();
+  if (pe >= 0 && pe < P.pj.E) upd_prefetch<N>(P, static_cast<int>(pe), tid);
   // RK operands of the final pass (zeta lines, same mapping), loaded ahead so
   // their latency hides behind the passes in between
   double pre_un[LPT][N], pre_acc[LPT][N];
@@ -376,10 +381,9 @@ __global__ void __launch_bounds__(UpdCfg<N>::THREADS, UpdCfg<N>::MINB)
   constexpr int EPB = UpdCfg<N>::EPB;
   __shared__ unsigned long long bar;
   const long long pe = P.pj.e_begin + (static_cast<long long>(NSFR_BID) + ahead) * EPB;
-  if (pe < P.pj.E) upd_prefetch<N>(P, static_cast<int>(pe), threadIdx.x);
   const int e0 = P.pj.e_begin + NSFR_BID * EPB;
   upd_batch<N, EPB, UpdCfg<N>::THREADS, CtaTeam, IDM, IDF, OUT>(P, O, e0, min(EPB, P.pj.E - e0), sm, &bar,
-                                                                 CtaTeam{});
+                                                                 CtaTeam{}, pe);
 }
 
 }  // namespace nsfr_b200

@@ -397,7 +397,15 @@ def test_config3_trajectory_to_final_time(p):
     steps = sorted(cps) + ([] if partial else [gold["steps"]])
     g, got = gpu_l2_at_steps(p, steps, 2.0)
     scale = l2_state_scale(g)
-    floor = l2_trajectory_floor(p, steps, 2.0)
+    # The GPU's own kicked-run floor takes ~20 min (two more runs with a host
+    # round trip of the state per step) and never decides the gate here (it is
+    # 1e-17..2e-16, below the representability limit of 7e-15 at every
+    # checkpoint): the recorded one is used unless NSFR_TRAJ_FLOOR=1.
+    rec = _traj_gold().get(f"p{p}_gpu_floor", {}).get("floor", {})
+    if os.environ.get("NSFR_TRAJ_FLOOR") == "1" or not all(str(k) in rec for k in steps):
+        floor = l2_trajectory_floor(p, steps, 2.0)
+    else:
+        floor = {k: np.array(rec[str(k)]) for k in steps}
     for k in steps:
         want = cps[k] if k in cps else {"t": gold["t_final"], "l2": gold["l2"]}
         assert got[k][0] == pytest.approx(want["t"], abs=1e-12), (k, got[k][0], want["t"])
