@@ -85,6 +85,19 @@ __device__ __forceinline__ void vol_pairs(const double* __restrict__ Pd, const d
 }
 #undef NSFR_VOL_PAIRS_BODY
 
+// n / d for a run-time d by one high multiply: M = ceil(2^64 / d) gives the
+// exact quotient for every 32-bit n (n (M d - 2^64) < 2^64). K2 took three
+// hardware-less integer divisions per thread to place its batch in the box
+// (2.5% of its instructions, their latency ahead of the face loop).
+struct DivMagic {
+  unsigned long long M;  // 0: d = 1
+  int d;
+  static DivMagic make(int d) { return DivMagic{d <= 1 ? 0ull : ~0ull / static_cast<unsigned>(d) + 1ull, d}; }
+  __device__ __forceinline__ int div(int n) const {
+    return M ? static_cast<int>(__umul64hi(static_cast<unsigned long long>(static_cast<unsigned>(n)), M)) : n;
+  }
+};
+
 struct ResParams {
   const double* ut_vol;   // [E][6][N^3] half-scaled primitives of u~ (K1 / K3)
   const double* traces;   // [E][6 faces][NTR][N^2] primitives of u(v~) (physics.cuh)
@@ -98,6 +111,7 @@ struct ResParams {
   double gamma;
   int roe;
   int e_begin;            // first element of the launched range (a multiple of 8)
+  DivMagic dm, dmm;       // division by m and by m^2 (host-formed multipliers)
   GasC gas;               // gamma and its reciprocals (host-formed)
 };
 
@@ -173,7 +187,9 @@ __device__ __forceinline__ void res_prefetch(const ResParams& P, int e0, int tid
       if (j >= 2 * nb) break;
       const int e = e0 + j / 2, f = 4 + (j & 1), dir = 2, step = (f & 1) ? 1 : -1;
       const int mm = P.m;
-      int i = e % mm, jj = (e / mm) % mm, kl = e / (mm * mm);
+      int kl = P.dmm.div(e);
+      const int pl = e - kl * mm * mm;
+      int jj = P.dm.div(pl), i = pl - jj * mm;
       if (dir == 0) i = (i + step + mm) % mm;
       if (dir == 1) jj = (jj + step + mm) % mm;
       if (dir == 2) {
@@ -301,7 +317,7 @@ __device__ __forceinline__ void res_lines(const ResParams& P, const ResOps<N>& O
   const int tid = threadIdx.x;
   const double g = P.gamma, gm1 = g - 1.0;
   // box coordinates of the batch's first element (block-uniform)
-  const int ei0 = e0 % P.m, ej0 = (e0 / P.m) % P.m, ek0 = e0 / (P.m * P.m);
+  const int ek0 = P.dmm.div(e0), epl = e0 - ek0 * P.m * P.m, ej0 = P.dm.div(epl), ei0 = epl - ej0 * P.m;
 
   // ---- line phase: one thread owns one 1D line (b, dir, t1, t2) ----
   int lb, ldir, lt1, lt2;
@@ -448,11 +464,33 @@ __device__ __forceinline__ void res_lines(const ResParams& P, const ResOps<N>& O
         for (int s = 0; s < NS; ++s) fn[s] -= d[s];
       }
       const double cc = wt * jg;
-      // this face's row leaves registers now (facc[e][dir][s][side][k]): nothing
-      // of side 0 stays live through side 1
-      double* fa = P.facc + ((size_t)e * 3 + dir) * 10 * N2 + k + side * N2;
+      if constexpr (fuse_face(N)) {
+        // S9's face lift, done here: in the collocated flux basis the lift of this
+        // face row onto its own line is l_f(a) = bound_flux(side, a) (chi^T l_f =
+        // bound_sol_f, so (M l_f (x) M (x) M) facc = M^3 (l_f (x) facc): the rows K3
+        // lifts are vol + sum_f l_f (x) facc_f). The line's nodes belong to this
+        // thread in its direction accumulator, so the face row never leaves the
+        // SM: no facc array in HBM (12 KB per element and stage at p=4), no face
+        // passes in K3.
+        double fr[NS];
 #pragma unroll
-      for (int s = 0; s < NS; ++s) fa[s * 2 * N2] = fma(cc, fn[s], ff[s]);
+        for (int s = 0; s < NS; ++s) fr[s] = fma(cc, fn[s], ff[s]);
+        {
+          double* __restrict__ aa_p = acc + lbase;
+#pragma unroll
+          for (int a = 0; a < N; ++a) {
+            const double w = O.bflux[side * N + a];
+#pragma unroll
+            for (int s = 0; s < NS; ++s) aa_p[s * N3 + a * stride] = fma(w, fr[s], aa_p[s * N3 + a * stride]);
+          }
+        }
+      } else {
+        // this face's row leaves registers now (facc[e][dir][s][side][k]): nothing
+        // of side 0 stays live through side 1
+        double* fa = P.facc + ((size_t)e * 3 + dir) * 10 * N2 + k + side * N2;
+#pragma unroll
+        for (int s = 0; s < NS; ++s) fa[s * 2 * N2] = fma(cc, fn[s], ff[s]);
+      }
     }
   }
 }

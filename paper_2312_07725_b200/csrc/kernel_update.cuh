@@ -69,7 +69,8 @@ struct UpdCfg {
   static constexpr int THREADS = N == 6 ? 128 : (N == 7 ? 160 : ((EPB * N3 + 31) / 32) * 32);
   // R0 vol/u_{s+1}, R1, R2 pass buffers (5 N3 each), R3 facc / face scratch,
   // R4 face-lift buffers (30 N2 each), R5 1/(w J) (N3)
-  static constexpr int PER_EL = 16 * N3 + 60 * N2;
+  // fuse_face: K2 lifted the face rows into vol, no facc staging, no face-lift buffers R4
+  static constexpr int PER_EL = 16 * N3 + (fuse_face(N) ? 30 : 60) * N2;
   static constexpr int SMEM = EPB * PER_EL * 8;
   // CTAs per SM: what shared memory allows, but keep >= RMIN registers per thread
   static constexpr int RMIN = N <= 5 ? 64 : 80;
@@ -162,7 +163,7 @@ __device__ __forceinline__ void upd_prefetch(const UpdParams& P, int e0, int tid
   const size_t nb = min(EPB, P.pj.E - e0), b8 = sizeof(double);
   switch (tid) {
     case 0: l2_prefetch(P.vol + (size_t)e0 * 5 * N3, nb * 5 * N3 * b8); break;
-    case 1: l2_prefetch(P.facc + (size_t)e0 * 30 * N2, nb * 30 * N2 * b8); break;
+    case 1: if (!fuse_face(N)) l2_prefetch(P.facc + (size_t)e0 * 30 * N2, nb * 30 * N2 * b8); break;
     case 2: l2_prefetch(P.wj + (size_t)e0 * N3, nb * N3 * b8); break;
     case 3: if (P.stage >= 1) l2_prefetch(P.un + (size_t)e0 * 5 * N3, nb * 5 * N3 * b8); break;
     case 4: if (P.stage >= 2) l2_prefetch(P.acc + (size_t)e0 * 5 * N3, nb * 5 * N3 * b8); break;
@@ -187,7 +188,8 @@ __device__ __forceinline__ void upd_batch(const UpdParams& P, const UpdOps<N>& O
   double* R1 = R0 + EPB * VS;
   double* R2 = R1 + EPB * VS;
   double* R3 = R2 + EPB * VS;      // facc [b][dir][s][side][N2], later proj_core face scratch
-  double* R4 = R3 + EPB * FS;      // [b][G1 | G2 | H2] (10 N2 each)
+  constexpr bool INJ = !fuse_face(N);  // fused: the face lifts are already in vol (K2)
+  double* R4 = INJ ? R3 + EPB * FS : R3;  // [b][G1 | G2 | H2] (10 N2 each); unused when fused
   double* WJ = R4 + EPB * FS;
   const TailOps<N>& T = O.t;
   const int tid = tm.tid(), nthr = tm.nthr();
@@ -200,7 +202,7 @@ __device__ __forceinline__ void upd_batch(const UpdParams& P, const UpdOps<N>& O
   tm.sync();
   {
     const StageBlock blk[3] = {{R0, P.vol + (size_t)e0 * VS, nb * VS},
-                               {R3, P.facc + (size_t)e0 * FS, nb * FS},
+                               {R3, P.facc + (size_t)e0 * FS, INJ ? nb * FS : 0},
                                {WJ, P.wj + (size_t)e0 * N3, nb * N3}};
     stage_copy<3>(blk, bar_p, tm);
   }
@@ -237,40 +239,49 @@ __device__ __forceinline__ void upd_batch(const UpdParams& P, const UpdOps<N>& O
     // M = I: vol + b_f (x) facc_f injected per node (x, y, z faces in the pass
     // order), times 1/(w J)
     for (int it = tid; it < nbs * N3; it += nthr) {
-      const int bsi = it / N3, q = it - bsi * N3, b = bsi / 5, s = bsi - 5 * b;
-      const int i = q % N, j = (q / N) % N, k = q / N2;
-      const double* fb = R3 + b * FS + (s * 2) * N2;
+      const int bsi = it / N3, q = it - bsi * N3, b = bsi / 5;
       double v = R0[it];
-      v = fma(T.bm[i], fb[j + N * k], v);
-      v = fma(T.bm[N + i], fb[N2 + j + N * k], v);
-      v = fma(T.bm[j], fb[10 * N2 + i + N * k], v);
-      v = fma(T.bm[N + j], fb[10 * N2 + N2 + i + N * k], v);
-      v = fma(T.bm[k], fb[20 * N2 + i + N * j], v);
-      v = fma(T.bm[N + k], fb[20 * N2 + N2 + i + N * j], v);
+      if constexpr (INJ) {
+        const int s = bsi - 5 * b;
+        const int i = q % N, j = (q / N) % N, k = q / N2;
+        const double* fb = R3 + b * FS + (s * 2) * N2;
+        v = fma(T.bm[i], fb[j + N * k], v);
+        v = fma(T.bm[N + i], fb[N2 + j + N * k], v);
+        v = fma(T.bm[j], fb[10 * N2 + i + N * k], v);
+        v = fma(T.bm[N + j], fb[10 * N2 + N2 + i + N * k], v);
+        v = fma(T.bm[k], fb[20 * N2 + i + N * j], v);
+        v = fma(T.bm[N + k], fb[20 * N2 + N2 + i + N * j], v);
+      }
       R0[it] = v * WJ[b * N3 + q];
     }
     tm.sync();
   } else if (!P.dS) {
     // Pi~^T S9 in three fused passes; 1/(w J) in the last
-    tail_pass<N, 0, true, false>(T.M, T.bm, R3, FS, R0, VS, R1, VS, WJ, nbs, tid, nthr);
-    tail_face_pass<N, 0>(T.M, R3 + 10 * N2, FS, R4, FS, nb, face_vt<N>(tid, nthr, 0), nthr);
-    tail_face_pass<N, 0>(T.M, R3 + 20 * N2, FS, R4 + 10 * N2, FS, nb, face_vt<N>(tid, nthr, nb * 10 * N), nthr);
+    tail_pass<N, 0, INJ, false>(T.M, T.bm, R3, FS, R0, VS, R1, VS, WJ, nbs, tid, nthr);
+    if constexpr (INJ) {
+      tail_face_pass<N, 0>(T.M, R3 + 10 * N2, FS, R4, FS, nb, face_vt<N>(tid, nthr, 0), nthr);
+      tail_face_pass<N, 0>(T.M, R3 + 20 * N2, FS, R4 + 10 * N2, FS, nb, face_vt<N>(tid, nthr, nb * 10 * N), nthr);
+    }
     tm.sync();
-    tail_pass<N, 1, true, false>(T.M, T.bm, R4, FS, R1, VS, R2, VS, WJ, nbs, tid, nthr);
-    tail_face_pass<N, 1>(T.M, R4 + 10 * N2, FS, R4 + 20 * N2, FS, nb, face_vt<N>(tid, nthr, 0), nthr);
+    tail_pass<N, 1, INJ, false>(T.M, T.bm, R4, FS, R1, VS, R2, VS, WJ, nbs, tid, nthr);
+    if constexpr (INJ)
+      tail_face_pass<N, 1>(T.M, R4 + 10 * N2, FS, R4 + 20 * N2, FS, nb, face_vt<N>(tid, nthr, 0), nthr);
     tm.sync();
-    tail_pass<N, 2, true, true>(T.M, T.bm, R4 + 20 * N2, FS, R2, VS, R0, VS, WJ, nbs, tid, nthr);
+    tail_pass<N, 2, INJ, true>(T.M, T.bm, R4 + 20 * N2, FS, R2, VS, R0, VS, WJ, nbs, tid, nthr);
     tm.sync();
   } else {
     // entropy diagnostic: R = S9 explicitly (chi^T, bound_sol), -v_hat . R, then Pi~^T
-    tail_pass<N, 0, true, false>(T.it, T.bs, R3, FS, R0, VS, R1, VS, WJ, nbs, tid, nthr);
-    tail_face_pass<N, 0>(T.it, R3 + 10 * N2, FS, R4, FS, nb, face_vt<N>(tid, nthr, 0), nthr);
-    tail_face_pass<N, 0>(T.it, R3 + 20 * N2, FS, R4 + 10 * N2, FS, nb, face_vt<N>(tid, nthr, nb * 10 * N), nthr);
+    tail_pass<N, 0, INJ, false>(T.it, T.bs, R3, FS, R0, VS, R1, VS, WJ, nbs, tid, nthr);
+    if constexpr (INJ) {
+      tail_face_pass<N, 0>(T.it, R3 + 10 * N2, FS, R4, FS, nb, face_vt<N>(tid, nthr, 0), nthr);
+      tail_face_pass<N, 0>(T.it, R3 + 20 * N2, FS, R4 + 10 * N2, FS, nb, face_vt<N>(tid, nthr, nb * 10 * N), nthr);
+    }
     tm.sync();
-    tail_pass<N, 1, true, false>(T.it, T.bs, R4, FS, R1, VS, R2, VS, WJ, nbs, tid, nthr);
-    tail_face_pass<N, 1>(T.it, R4 + 10 * N2, FS, R4 + 20 * N2, FS, nb, face_vt<N>(tid, nthr, 0), nthr);
+    tail_pass<N, 1, INJ, false>(T.it, T.bs, R4, FS, R1, VS, R2, VS, WJ, nbs, tid, nthr);
+    if constexpr (INJ)
+      tail_face_pass<N, 1>(T.it, R4 + 10 * N2, FS, R4 + 20 * N2, FS, nb, face_vt<N>(tid, nthr, 0), nthr);
     tm.sync();
-    tail_pass<N, 2, true, false>(T.it, T.bs, R4 + 20 * N2, FS, R2, VS, R0, VS, WJ, nbs, tid, nthr);
+    tail_pass<N, 2, INJ, false>(T.it, T.bs, R4 + 20 * N2, FS, R2, VS, R0, VS, WJ, nbs, tid, nthr);
     tm.sync();
     for (int it = tid; it < nbs * N3; it += nthr) R1[it] = P.vhat[(size_t)e0 * VS + it] * R0[it];
     tm.sync();

@@ -302,6 +302,8 @@ int launch_residual(nsfr_gpu_ctx* ctx, int km, int ea, int eb) {
   P.err = ctx->d_err;
   P.E = ctx->E;
   P.m = ctx->m;
+  P.dm = DivMagic::make(ctx->m);
+  P.dmm = DivMagic::make(ctx->m * ctx->m);
   P.nz = ctx->nz;
   P.gamma = ctx->s.gamma;
   P.gas = GasC::make(ctx->s.gamma);
@@ -940,7 +942,7 @@ int nsfr_gpu_create(const nsfr_gpu_setup* setup, nsfr_gpu_ctx** out) {
   };
   if (cudaMalloc(&ctx->d_tab, sizeof(DevTables)) || alloc(&ctx->d_un, ns) || alloc(&ctx->d_vol, nscr) ||
       alloc(&ctx->d_acc, ns) || alloc(&ctx->d_rhs, ns) || alloc(&ctx->d_utv, 6 * n3) ||
-      alloc(&ctx->d_tr, ntrace) || alloc(&ctx->d_facc, ntr) || alloc(&ctx->d_cof, 9 * n3) || alloc(&ctx->d_jac, n3) ||
+      alloc(&ctx->d_tr, ntrace) || alloc(&ctx->d_facc, !ctx->dg && fuse_face(ctx->N) ? 0 : ntr) || alloc(&ctx->d_cof, 9 * n3) || alloc(&ctx->d_jac, n3) ||
       alloc(&ctx->d_wj, n3) || alloc(&ctx->d_dS, ctx->E) || alloc(&ctx->d_part, 2 * (size_t)ctx->E) ||
       alloc(&ctx->d_red, 8) || cudaMalloc(&ctx->d_step, sizeof(StepState)) ||
       cudaMalloc(&ctx->d_err, sizeof(unsigned)) ||
