@@ -146,10 +146,21 @@ struct ResCfg {
   // direction offsets DOFF) so that the same accesses cost ~1.2x
   // (tools/k2_bankmap.c anneals both against the bank model, which reproduces
   // the measured 1.65x). Results are bitwise unchanged: which lane runs a line
-  // does not enter its arithmetic.
-  static constexpr bool MAPPED = N == 5;
-  static constexpr int DOFF1 = MAPPED ? 631 : 5 * N3, DOFF2 = MAPPED ? 1264 : 10 * N3;
-  static constexpr int AS = MAPPED ? 1901 : 15 * N3;   // doubles per element of ACCV
+  // does not enter its arithmetic. Measured K2 (A/B, one session): n = 4 -12%
+  // (model 3.00x -> 2.26x: the power-of-two strides leave 4-way conflicts no
+  // lane order removes), n = 5 -3.7% (1.65x -> 1.20x), n = 6 -4.8% (1.90x ->
+  // 1.56x), n = 7 -14% (1.70x -> 1.30x).
+#ifndef NSFR_RES_MAPMASK
+#define NSFR_RES_MAPMASK 0xf0
+#endif
+  static constexpr bool MAPPED = N >= 4 && N <= 7 && ((NSFR_RES_MAPMASK >> N) & 1);
+  // paddings per degree: the smallest offsets >= the dense ones with the
+  // annealed residues mod 16 (N = 4: 0, 12, element stride 3; N = 5: 7, 0, 13;
+  // N = 6: 5, 6; N = 7: 0, 5)
+  static constexpr int DOFF1 = !MAPPED ? 5 * N3 : (N == 4 ? 320 : (N == 5 ? 631 : (N == 6 ? 1093 : 1728)));
+  static constexpr int DOFF2 = !MAPPED ? 10 * N3 : (N == 4 ? 652 : (N == 5 ? 1264 : (N == 6 ? 2182 : 3445)));
+  // doubles per element of ACCV
+  static constexpr int AS = !MAPPED ? 15 * N3 : (N == 4 ? 979 : (N == 5 ? 1901 : (N == 6 ? 3262 : 5160)));
   static constexpr int ACC_ALL = (EPB * AS + 1) / 2 * 2;  // ACCV region (even: PRIM stays 16-byte aligned)
   // ACCV (3 directions x 5 N3, padded) + node primitives (6 N3) + half cofactors (9 N3)
   // [+ own traces 6 NTR N2]
@@ -246,12 +257,51 @@ __device__ const unsigned short g_res_map5[160] = {
     0x0112, 0x1232, 0x1104, 0x0032, 0x1233, 0x1204, 0x0102, 0x0241, 0x0240, 0x1043, 0x0104, 0x1242, 0x0124, 0x0121, 0x1203, 0x1241,
     0x0040, 0x0002, 0x0043, 0x0034, 0x0010, 0x1044, 0x0000, 0x1042, 0x1000, 0x1003, 0x0011, 0x0044, 0x1040, 0x1002, 0x1001, 0x1041,
     0x1211, 0x1240, 0x1234, 0x1224, 0x1221, 0x1220, 0x1244, 0x1222, 0x1200, 0x1214, 0x1201, 0x1202, 0x1243, 0x1210, 0x1230, 0x1223};
+// N = 4, four elements per CTA: 2.26 wavefronts per ideal one (natural order 3.00)
+__device__ const unsigned short g_res_map4[192] = {
+    0x3113, 0x2122, 0x2130, 0x2133, 0x0100, 0x1100, 0x2111, 0x0030, 0x0121, 0x1101, 0x1132, 0x3013, 0x0001, 0x1020, 0x3012, 0x0022,
+    0x2121, 0x1021, 0x3020, 0x2132, 0x1010, 0x3110, 0x1113, 0x3123, 0x1012, 0x1131, 0x3132, 0x0123, 0x2002, 0x2011, 0x0002, 0x2020,
+    0x0200, 0x0201, 0x0202, 0x0203, 0x0210, 0x0211, 0x0212, 0x0213, 0x0220, 0x0221, 0x0222, 0x0223, 0x0230, 0x0231, 0x0232, 0x0233,
+    0x0021, 0x0112, 0x2033, 0x2000, 0x0103, 0x0130, 0x2100, 0x1033, 0x3112, 0x0023, 0x3133, 0x1122, 0x3121, 0x3010, 0x2123, 0x3111,
+    0x1022, 0x3033, 0x3031, 0x3002, 0x2013, 0x0011, 0x2012, 0x3030, 0x1023, 0x1031, 0x0020, 0x2030, 0x0032, 0x0013, 0x2031, 0x1000,
+    0x1200, 0x1201, 0x1202, 0x1203, 0x1210, 0x1211, 0x1212, 0x1213, 0x1220, 0x1221, 0x1222, 0x1223, 0x1230, 0x1231, 0x1232, 0x1233,
+    0x2010, 0x2102, 0x2023, 0x1112, 0x0132, 0x3120, 0x3022, 0x1123, 0x3101, 0x1030, 0x2131, 0x0113, 0x0031, 0x0111, 0x2021, 0x3023,
+    0x2120, 0x3000, 0x3011, 0x0120, 0x2112, 0x2001, 0x0003, 0x3103, 0x3102, 0x3001, 0x1013, 0x2113, 0x2003, 0x1130, 0x0010, 0x1032,
+    0x2200, 0x2201, 0x2202, 0x2203, 0x2210, 0x2211, 0x2212, 0x2213, 0x2220, 0x2221, 0x2222, 0x2223, 0x2230, 0x2231, 0x2232, 0x2233,
+    0x0012, 0x3021, 0x0033, 0x2110, 0x3122, 0x0122, 0x3003, 0x1111, 0x3131, 0x3130, 0x0133, 0x0110, 0x1001, 0x0101, 0x2032, 0x1003,
+    0x0102, 0x2101, 0x1110, 0x1120, 0x1133, 0x1103, 0x3100, 0x1102, 0x0131, 0x1121, 0x1011, 0x2022, 0x0000, 0x1002, 0x2103, 0x3032,
+    0x3200, 0x3201, 0x3202, 0x3203, 0x3210, 0x3211, 0x3212, 0x3213, 0x3220, 0x3221, 0x3222, 0x3223, 0x3230, 0x3231, 0x3232, 0x3233};
+// N = 6, one element per CTA: 1.56 (natural order 1.90)
+__device__ const unsigned short g_res_map6[128] = {
+    0x0020, 0x0114, 0x0033, 0x0140, 0x0034, 0x0101, 0x0054, 0x0105, 0x0041, 0x0125, 0x0035, 0x0015, 0x0121, 0x0144, 0x0052, 0x0230,
+    0x0005, 0x0224, 0x0145, 0x0253, 0x0143, 0x0012, 0x0055, 0x0151, 0x0104, 0x0042, 0x0115, 0x0135, 0x0153, 0x0025, 0x0202, 0x0203,
+    0x0004, 0x0040, 0xffff, 0x0023, 0x0134, 0x0050, 0x0003, 0x0152, 0x0124, 0x0122, 0x0102, 0x0002, 0x0120, 0xffff, 0x0110, 0x0013,
+    0x0132, 0x0021, 0x0044, 0x0022, 0x0000, 0x0100, 0x0112, 0x0130, 0x0154, 0x0142, 0x0053, 0x0150, 0xffff, 0x0030, 0x0051, 0x0031,
+    0x0045, 0x0010, 0x0011, 0x0141, 0x0032, 0x0014, 0x0133, 0x0043, 0x0113, 0x0131, 0x0103, 0x0024, 0x0001, 0x0123, 0x0155, 0x0111,
+    0x0243, 0x0235, 0x0254, 0x0244, 0x0231, 0x0232, 0x0214, 0x0225, 0x0200, 0x0240, 0x0210, 0x0222, 0x0241, 0x0233, 0x0223, 0x0245,
+    0x0204, 0x0215, 0x0255, 0x0221, 0x0201, 0x0250, 0x0213, 0x0242, 0x0252, 0xffff, 0x0220, 0x0251, 0x0211, 0x0205, 0x0212, 0x0234,
+    0xffff, 0xffff, 0xffff, 0xffff, 0xffff, 0xffff, 0xffff, 0xffff, 0xffff, 0xffff, 0xffff, 0xffff, 0xffff, 0xffff, 0xffff, 0xffff};
+// N = 7, one element per CTA: 1.30 (natural order 1.70)
+__device__ const unsigned short g_res_map7[160] = {
+    0x0036, 0x0060, 0x0043, 0xffff, 0x0024, 0x0032, 0x0066, 0x0011, 0x0052, 0x0026, 0x0056, 0x0041, 0x0025, 0x0053, 0x0040, 0x0064,
+    0x0021, 0x0051, 0x0002, 0x0050, 0x0044, 0x0016, 0x0035, 0x0061, 0x0034, 0x0054, 0x0030, 0x0020, 0x0033, 0x0045, 0x0062, 0x0031,
+    0x0015, 0x0022, 0x0001, 0x0005, 0x0003, 0x0065, 0x0013, 0x0063, 0x0010, 0x0006, 0x0055, 0x0014, 0x0042, 0x0012, 0x0004, 0x0046,
+    0x0142, 0x0140, 0x0110, 0x0166, 0x0100, 0x0120, 0x0150, 0x0156, 0x0163, 0x0162, 0x0121, 0x0164, 0xffff, 0x0116, 0xffff, 0xffff,
+    0x0122, 0x0141, 0x0153, 0x0133, 0x0136, 0x0102, 0x0161, 0xffff, 0x0131, 0x0135, 0x0155, 0x0112, 0x0132, 0x0146, 0x0152, 0x0160,
+    0x0023, 0x0101, 0xffff, 0x0130, 0xffff, 0x0000, 0x0145, 0xffff, 0x0123, 0x0143, 0x0222, 0x0151, 0x0115, 0xffff, 0x0165, 0xffff,
+    0x0104, 0xffff, 0x0114, 0x0111, 0x0125, 0x0154, 0x0113, 0xffff, 0x0124, 0x0106, 0x0105, 0x0144, 0x0103, 0xffff, 0x0134, 0x0126,
+    0x0255, 0x0201, 0x0200, 0x0246, 0x0241, 0x0264, 0x0252, 0x0253, 0x0243, 0x0256, 0x0260, 0x0236, 0x0203, 0x0204, 0x0240, 0x0210,
+    0x0261, 0x0206, 0x0266, 0x0263, 0x0251, 0x0232, 0x0242, 0x0235, 0x0205, 0x0223, 0x0250, 0x0221, 0x0215, 0x0211, 0x0202, 0x0212,
+    0x0234, 0x0226, 0x0244, 0x0265, 0x0214, 0x0245, 0x0220, 0x0230, 0x0213, 0x0254, 0x0233, 0x0225, 0x0262, 0x0216, 0x0231, 0x0224};
 // A global (L1-cached) table, not a __constant__ one: every lane reads its own
 // entry, which the constant cache would serialise 32 ways.
 template <int N>
 __device__ __forceinline__ unsigned res_line_map(int tid) {
-  static_assert(N == 5, "no line map for this degree");
-  return __ldg(&g_res_map5[tid]);
+  static_assert(N >= 4 && N <= 7, "no line map for this degree");
+  if constexpr (N == 4) return __ldg(&g_res_map4[tid]);
+  if constexpr (N == 5) return __ldg(&g_res_map5[tid]);
+  if constexpr (N == 6) return __ldg(&g_res_map6[tid]);
+  return __ldg(&g_res_map7[tid]);
 }
 
 template <int N, int KM>
