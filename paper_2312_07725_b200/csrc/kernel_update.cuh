@@ -39,8 +39,68 @@ struct UpdParams {
   unsigned long long* lam_out;  // OUT: adaptive_dt's lambda_max of chi^3 of that u_hat, or nullptr
 };
 
+// A centrosymmetric 1D operator (M = J M J, J the flip: every operator built
+// from a symmetric node set and basis is one) applied through its even / odd
+// halves: with se = x + Jx, so = x - Jx (first halves),
+//   y[r], y[N-1-r] = e[r] +- o[r],  e = E se (ceil(N/2) square), o = O so (floor(N/2) square),
+// E[r][a] = (M[r][a] + M[r][N-1-a]) / 2 (the middle column of an odd N as it is),
+// O[r][a] = (M[r][a] - M[r][N-1-a]) / 2. At N = 5: 13 multiply-adds + 8 additions
+// and 13 constant operands instead of 25 + 25 (each constant is a uniform load
+// in the SASS, and K3 is issue-bound).
+template <int N>
+struct SymOp {
+  static constexpr int H = N / 2, C = (N + 1) / 2;
+  double e[C * C];
+  double o[H * H];
+  // largest |M - J M J| over |M|: the caller refuses an operator that is not centrosymmetric
+  static double asymmetry(const double* M) {
+    double d = 0.0, m = 0.0;
+    for (int r = 0; r < N; ++r)
+      for (int a = 0; a < N; ++a) {
+        const double x = M[r * N + a], y = M[(N - 1 - r) * N + (N - 1 - a)];
+        d = d < (x > y ? x - y : y - x) ? (x > y ? x - y : y - x) : d;
+        m = m < (x < 0 ? -x : x) ? (x < 0 ? -x : x) : m;
+      }
+    return m > 0.0 ? d / m : 0.0;
+  }
+  static SymOp fold(const double* M) {
+    SymOp S{};
+    for (int r = 0; r < C; ++r)
+      for (int a = 0; a < C; ++a)
+        S.e[r * C + a] = (a < H) ? 0.5 * (M[r * N + a] + M[r * N + (N - 1 - a)]) : M[r * N + a];
+    for (int r = 0; r < H; ++r)
+      for (int a = 0; a < H; ++a) S.o[r * H + a] = 0.5 * (M[r * N + a] - M[r * N + (N - 1 - a)]);
+    return S;
+  }
+  __device__ __forceinline__ void apply(const double (&x)[N], double (&y)[N]) const {
+    double se[C], so[H > 0 ? H : 1];
+#pragma unroll
+    for (int a = 0; a < H; ++a) {
+      se[a] = x[a] + x[N - 1 - a];
+      so[a] = x[a] - x[N - 1 - a];
+    }
+    if (C > H) se[H] = x[H];
+#pragma unroll
+    for (int r = 0; r < C; ++r) {
+      double ev = 0.0;
+#pragma unroll
+      for (int a = 0; a < C; ++a) ev = fma(e[r * C + a], se[a], ev);
+      if (r < H) {
+        double ov = 0.0;
+#pragma unroll
+        for (int a = 0; a < H; ++a) ov = fma(o[r * H + a], so[a], ov);
+        y[r] = ev + ov;
+        y[N - 1 - r] = ev - ov;
+      } else {
+        y[r] = ev;
+      }
+    }
+  }
+};
+
 template <int N>
 struct TailOps {
+  SymOp<N> Ms, frs;      // M and fr folded (the hot path without face injection)
   double M[N * N];       // Pi~^T chi^T          (lift + project, hot path)
   double bm[2 * N];      // Pi~^T bound_sol_side
   double fr[N * N];      // final passes: Pi~ (stage 0, u_hat space) or chi Pi~ (RK stages, u_q space)
@@ -117,6 +177,28 @@ __device__ __forceinline__ void tail_pass(const double (&op)[N * N], const doubl
       if (DIV) acc = acc * wj[b * N3 + base + r * stride];  // wj holds 1/(w J)
       dst[r * stride] = acc;
     }
+  }
+}
+
+// The same line pass through a folded centrosymmetric operator (no injection).
+template <int N, int D, bool DIV>
+__device__ __forceinline__ void tail_pass_sym(const SymOp<N>& op, const double* in, int in_es, double* out,
+                                              int out_es, const double* wj, int nbs, int tid, int nthr) {
+  constexpr int N2 = N * N, N3 = N * N * N;
+  constexpr int stride = D == 0 ? 1 : (D == 1 ? N : N2);
+  for (int it = tid; it < nbs * N2; it += nthr) {
+    const int bsi = it / N2, l = it - bsi * N2;
+    const int b = bsi / 5, s = bsi - 5 * b;
+    const int l0 = l % N, l1 = l / N;
+    const int base = D == 0 ? N * (l0 + N * l1) : (D == 1 ? l0 + N2 * l1 : l0 + N * l1);
+    const double* src = in + b * in_es + s * N3 + base;
+    double x[N], y[N];
+#pragma unroll
+    for (int a = 0; a < N; ++a) x[a] = src[a * stride];
+    op.apply(x, y);
+    double* dst = out + b * out_es + s * N3 + base;
+#pragma unroll
+    for (int r = 0; r < N; ++r) dst[r * stride] = DIV ? y[r] * wj[b * N3 + base + r * stride] : y[r];
   }
 }
 
@@ -257,17 +339,22 @@ __device__ __forceinline__ void upd_batch(const UpdParams& P, const UpdOps<N>& O
     tm.sync();
   } else if (!P.dS) {
     // Pi~^T S9 in three fused passes; 1/(w J) in the last
-    tail_pass<N, 0, INJ, false>(T.M, T.bm, R3, FS, R0, VS, R1, VS, WJ, nbs, tid, nthr);
     if constexpr (INJ) {
+      tail_pass<N, 0, true, false>(T.M, T.bm, R3, FS, R0, VS, R1, VS, WJ, nbs, tid, nthr);
       tail_face_pass<N, 0>(T.M, R3 + 10 * N2, FS, R4, FS, nb, face_vt<N>(tid, nthr, 0), nthr);
       tail_face_pass<N, 0>(T.M, R3 + 20 * N2, FS, R4 + 10 * N2, FS, nb, face_vt<N>(tid, nthr, nb * 10 * N), nthr);
-    }
-    tm.sync();
-    tail_pass<N, 1, INJ, false>(T.M, T.bm, R4, FS, R1, VS, R2, VS, WJ, nbs, tid, nthr);
-    if constexpr (INJ)
+      tm.sync();
+      tail_pass<N, 1, true, false>(T.M, T.bm, R4, FS, R1, VS, R2, VS, WJ, nbs, tid, nthr);
       tail_face_pass<N, 1>(T.M, R4 + 10 * N2, FS, R4 + 20 * N2, FS, nb, face_vt<N>(tid, nthr, 0), nthr);
-    tm.sync();
-    tail_pass<N, 2, INJ, true>(T.M, T.bm, R4 + 20 * N2, FS, R2, VS, R0, VS, WJ, nbs, tid, nthr);
+      tm.sync();
+      tail_pass<N, 2, true, true>(T.M, T.bm, R4 + 20 * N2, FS, R2, VS, R0, VS, WJ, nbs, tid, nthr);
+    } else {
+      tail_pass_sym<N, 0, false>(T.Ms, R0, VS, R1, VS, WJ, nbs, tid, nthr);
+      tm.sync();
+      tail_pass_sym<N, 1, false>(T.Ms, R1, VS, R2, VS, WJ, nbs, tid, nthr);
+      tm.sync();
+      tail_pass_sym<N, 2, true>(T.Ms, R2, VS, R0, VS, WJ, nbs, tid, nthr);
+    }
     tm.sync();
   } else {
     // entropy diagnostic: R = S9 explicitly (chi^T, bound_sol), -v_hat . R, then Pi~^T
@@ -302,9 +389,9 @@ __device__ __forceinline__ void upd_batch(const UpdParams& P, const UpdOps<N>& O
   if constexpr (LATE) preload();
   // second half of S10: Pi~ along xi, eta
   if constexpr (!IDF) {
-    tail_pass<N, 0, false, false>(T.fr, T.bs, nullptr, 0, R0, VS, R1, VS, WJ, nbs, tid, nthr);
+    tail_pass_sym<N, 0, false>(T.frs, R0, VS, R1, VS, WJ, nbs, tid, nthr);
     tm.sync();
-    tail_pass<N, 1, false, false>(T.fr, T.bs, nullptr, 0, R1, VS, R2, VS, WJ, nbs, tid, nthr);
+    tail_pass_sym<N, 1, false>(T.frs, R1, VS, R2, VS, WJ, nbs, tid, nthr);
     tm.sync();
   }
   // Pi~ along zeta, negate, RK stage epilogue (zeta lines: coalesced across the
@@ -323,16 +410,13 @@ __device__ __forceinline__ void upd_batch(const UpdParams& P, const UpdOps<N>& O
     const size_t gb = (size_t)e0 * VS + (size_t)bsi * N3 + l;
     double* nxt = R0 + bsi * N3 + l;
     double kv[N];
+    if constexpr (IDF) {
 #pragma unroll
-    for (int c = 0; c < N; ++c) {
-      double z = 0.0;
-      if constexpr (IDF) {
-        z = x[c];
-      } else {
+      for (int c = 0; c < N; ++c) kv[c] = -x[c];
+    } else {
+      T.frs.apply(x, kv);
 #pragma unroll
-        for (int a = 0; a < N; ++a) z = fma(T.fr[c * N + a], x[a], z);
-      }
-      kv[c] = -z;
+      for (int c = 0; c < N; ++c) kv[c] = -kv[c];
     }
     // one (warp-uniform) stage dispatch per line, not per node
     switch (P.stage) {

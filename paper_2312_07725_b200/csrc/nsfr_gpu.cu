@@ -241,6 +241,8 @@ UpdOps<N> upd_ops(const nsfr_gpu_ctx* ctx, int stage) {
     o.it[i] = t.interp_t[i];
   }
   for (int i = 0; i < 2 * N; ++i) o.bs[i] = t.bsol[i];
+  o.Ms = SymOp<N>::fold(o.M);
+  o.frs = SymOp<N>::fold(o.fr);
   u.p = proj_ops<N>(ctx);
   return u;
 }
@@ -917,6 +919,23 @@ int nsfr_gpu_create(const nsfr_gpu_setup* setup, nsfr_gpu_ctx** out) {
   DevTables dt;
   fill_dev_tables(ctx->tab, s.tables && s.tables->interp ? s.tables : nullptr, dt);
   ctx->htab = dt;
+  if (!ctx->dg) {
+    // K3 applies M = Pi~^T chi^T and chi Pi~ / Pi~ through their even / odd halves
+    // (SymOp, kernel_update.cuh), which needs chi and Pi~ centrosymmetric: true of
+    // every symmetric node set and basis (GL / LGL, the reference's tables)
+    const int n = ctx->N;
+    double asym = 0.0, big = 0.0;
+    for (int r = 0; r < n; ++r)
+      for (int a = 0; a < n; ++a) {
+        const int i = r * n + a, j = (n - 1 - r) * n + (n - 1 - a);
+        asym = std::max({asym, std::fabs(dt.interp[i] - dt.interp[j]), std::fabs(dt.frproj[i] - dt.frproj[j])});
+        big = std::max({big, std::fabs(dt.interp[i]), std::fabs(dt.frproj[i])});
+      }
+    if (!(asym <= 1e-11 * big)) {
+      ctx->msg = "nsfr_gpu_create: the 1D operators are not centrosymmetric (asymmetric nodes or basis)";
+      return fail(NSFR_E_CONFIG);
+    }
+  }
   if (!ctx->dg && std::getenv("NSFR_NO_IDENTITY_SKIP") == nullptr) {
     double dev = 0.0;  // max |chi Pi~ - I| (n_q = n_p)
     for (int c = 0; c < ctx->N; ++c)
