@@ -542,6 +542,19 @@ def test_inadmissible_state_raises():
     assert np.isfinite(g.rhs()).all()
 
 
+def test_asymmetric_operator_tables_refused():
+    """K3 applies its 1D operators through their even / odd halves (SymOp), which
+    needs them centrosymmetric; caller tables that are not are refused at create."""
+    pkg = P()
+    tabs = np.load(os.path.join(GOLD, "tables.npz"))
+    tables = {k: np.array(tabs[f"p3_q0_dg_{k}"]) for k in ("interp", "proj", "fr_proj", "skew", "bound_flux",
+                                                            "bound_sol", "wq")}
+    pkg.GpuSolver(gpu_cfg(p=3, m=2), tables=tables).close()  # the reference's own tables pass
+    tables["interp"].flat[1] *= 1.0 + 1e-6
+    with pytest.raises(pkg.ConfigError):
+        pkg.GpuSolver(gpu_cfg(p=3, m=2), tables=tables)
+
+
 def test_degenerate_mesh_raises():
     pkg = P()
     with pytest.raises(pkg.InvalidMeshError):
