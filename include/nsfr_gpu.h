@@ -56,7 +56,11 @@ extern "C" {
 typedef struct nsfr_gpu_ctx nsfr_gpu_ctx;
 
 /* Optional caller-built 1D tables (ReferenceOperators, fr_operators.hpp:40-57),
- * row-major. When `interp` is NULL the library builds them natively. */
+ * row-major. When `interp` is NULL the library builds them natively.
+ * interp and fr_proj must be centrosymmetric (A[n-1-r][n-1-c] = A[r][c], true of
+ * every symmetric node set and basis: GL / LGL, the reference's own tables):
+ * the NSFR update kernel applies them through their even / odd halves, and
+ * nsfr_gpu_create returns NSFR_E_CONFIG otherwise. */
 typedef struct nsfr_gpu_tables {
   const double* interp;     /* basis.interp  chi(xi_v)   nq x np */
   const double* proj;       /* proj          Pi          np x nq */
