@@ -92,28 +92,38 @@ __device__ __forceinline__ void line_pass(const double (&op)[N * N], const doubl
   }
 }
 
-// Face traces of direction D: one thread per 1D line along D contracts it with
-// the two boundary rows bp[side] into fo[batch][side][N2] (line index l).
+// Face traces: one thread per 1D line contracts it with the two boundary rows
+// bp[side] into fo[batch][side][N2] (line index l).
+// The three directions in one loop: a line index (tensor bsi, l0 + N l1) names one
+// line per direction, so its index arithmetic is done once (same sums, same bits).
 template <int N, int D>
-__device__ __forceinline__ void face_contract(const double (&bp)[2 * N], const double* in, double* fo,
-                                              int nbs, int tid, int nthr) {
+__device__ __forceinline__ void face_contract_line(const double (&bp)[2 * N], const double* in, double* fo,
+                                                   int bsi, int l, int l0, int l1) {
   constexpr int N2 = N * N, N3 = N * N * N;
   constexpr int stride = D == 0 ? 1 : (D == 1 ? N : N2);
+  const int base = D == 0 ? N * (l0 + N * l1) : (D == 1 ? l0 + N2 * l1 : l0 + N * l1);
+  const double* src = in + bsi * N3 + base;
+  double x[N];
+#pragma unroll
+  for (int a = 0; a < N; ++a) x[a] = src[a * stride];
+#pragma unroll
+  for (int side = 0; side < 2; ++side) {
+    double acc = 0.0;
+#pragma unroll
+    for (int a = 0; a < N; ++a) acc = fma(bp[side * N + a], x[a], acc);
+    fo[(bsi * 2 + side) * N2 + l] = acc;
+  }
+}
+template <int N>
+__device__ __forceinline__ void face_contract_all(const double (&bp)[2 * N], const double* in, double* F0,
+                                                  double* F1, double* F2, int nbs, int tid, int nthr) {
+  constexpr int N2 = N * N;
   for (int it = tid; it < nbs * N2; it += nthr) {
     const int bsi = it / N2, l = it - bsi * N2;
     const int l0 = l % N, l1 = l / N;
-    const int base = D == 0 ? N * (l0 + N * l1) : (D == 1 ? l0 + N2 * l1 : l0 + N * l1);
-    const double* src = in + bsi * N3 + base;
-    double x[N];
-#pragma unroll
-    for (int a = 0; a < N; ++a) x[a] = src[a * stride];
-#pragma unroll
-    for (int side = 0; side < 2; ++side) {
-      double acc = 0.0;
-#pragma unroll
-      for (int a = 0; a < N; ++a) acc = fma(bp[side * N + a], x[a], acc);
-      fo[(bsi * 2 + side) * N2 + l] = acc;
-    }
+    face_contract_line<N, 0>(bp, in, F0, bsi, l, l0, l1);
+    face_contract_line<N, 1>(bp, in, F1, bsi, l, l0, l1);
+    face_contract_line<N, 2>(bp, in, F2, bsi, l, l0, l1);
   }
 }
 
@@ -186,9 +196,7 @@ __device__ __forceinline__ void proj_core(const ProjParams& P, const ProjOps<N>&
   PHASE_MARK(11);
   // S4 faces: v~_f = (bs_side (x) chi (x) chi) Pi^3 v_q = (bs_side Pi) along the
   // normal applied to v_q (chi Pi = I tangentially): one contraction per line
-  face_contract<N, 0>(O.bp, V, F0, nbs, tid, nthr);
-  face_contract<N, 1>(O.bp, V, F1, nbs, tid, nthr);
-  face_contract<N, 2>(O.bp, V, F2, nbs, tid, nthr);
+  face_contract_all<N>(O.bp, V, F0, F1, F2, nbs, tid, nthr);
   tm.sync();
   PHASE_MARK(12);
   // S5 u~ = u(v~) at the face nodes, kept as primitives (NTR values per node)

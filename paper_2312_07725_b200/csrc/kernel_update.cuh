@@ -202,6 +202,26 @@ __device__ __forceinline__ void tail_pass_sym(const SymOp<N>& op, const double* 
   }
 }
 
+// One line of that pass for a thread whose (tensor bsi, line l0 + N l1) was
+// worked out once per batch: where a batch's 5 N2 lines per element fit the
+// team in one round (n = 5), the index arithmetic of the five passes (two
+// divisions by constants each) is done once.
+template <int N, int D, bool DIV>
+__device__ __forceinline__ void tail_line_sym(const SymOp<N>& op, const double* in, double* out,
+                                              const double* wjb, int bsi, int l0, int l1) {
+  constexpr int N2 = N * N, N3 = N * N * N;
+  constexpr int stride = D == 0 ? 1 : (D == 1 ? N : N2);
+  const int base = D == 0 ? N * (l0 + N * l1) : (D == 1 ? l0 + N2 * l1 : l0 + N * l1);
+  const double* src = in + bsi * N3 + base;
+  double x[N], y[N];
+#pragma unroll
+  for (int a = 0; a < N; ++a) x[a] = src[a * stride];
+  op.apply(x, y);
+  double* dst = out + bsi * N3 + base;
+#pragma unroll
+  for (int r = 0; r < N; ++r) dst[r * stride] = DIV ? y[r] * wjb[base + r * stride] : y[r];
+}
+
 // Face-array pass (10 arrays [s][side] of N2 per element) along t1 (T=0) or t2 (T=1).
 // Callers pass a virtual thread index from face_vt. At n >= 6 the face items
 // fill the threads counted from the top of the block, i.e. those the volume
@@ -276,6 +296,11 @@ __device__ __forceinline__ void upd_batch(const UpdParams& P, const UpdOps<N>& O
   const TailOps<N>& T = O.t;
   const int tid = tm.tid(), nthr = tm.nthr();
   const int nbs = nb * 5;
+  // one line per thread and pass: its indices once per batch (tail_line_sym)
+  constexpr bool ONE = EPB * 5 * N2 <= NT && !INJ;
+  const bool on1 = tid < nbs * N2;
+  const int bsi1 = tid / N2, q0 = (tid - bsi1 * N2) % N, q1 = (tid - bsi1 * N2) / N;
+  const double* wjb1 = WJ + (bsi1 / 5) * N3;
   PHASE_START();
   // the team syncs on the barrier's initialisation alone; thread 0 then issues
   // the TMA copies (and the look-ahead L2 prefetch of batch `pe`) while the
@@ -349,11 +374,19 @@ __device__ __forceinline__ void upd_batch(const UpdParams& P, const UpdOps<N>& O
       tm.sync();
       tail_pass<N, 2, true, true>(T.M, T.bm, R4 + 20 * N2, FS, R2, VS, R0, VS, WJ, nbs, tid, nthr);
     } else {
-      tail_pass_sym<N, 0, false>(T.Ms, R0, VS, R1, VS, WJ, nbs, tid, nthr);
-      tm.sync();
-      tail_pass_sym<N, 1, false>(T.Ms, R1, VS, R2, VS, WJ, nbs, tid, nthr);
-      tm.sync();
-      tail_pass_sym<N, 2, true>(T.Ms, R2, VS, R0, VS, WJ, nbs, tid, nthr);
+      if constexpr (ONE) {
+        if (on1) tail_line_sym<N, 0, false>(T.Ms, R0, R1, wjb1, bsi1, q0, q1);
+        tm.sync();
+        if (on1) tail_line_sym<N, 1, false>(T.Ms, R1, R2, wjb1, bsi1, q0, q1);
+        tm.sync();
+        if (on1) tail_line_sym<N, 2, true>(T.Ms, R2, R0, wjb1, bsi1, q0, q1);
+      } else {
+        tail_pass_sym<N, 0, false>(T.Ms, R0, VS, R1, VS, WJ, nbs, tid, nthr);
+        tm.sync();
+        tail_pass_sym<N, 1, false>(T.Ms, R1, VS, R2, VS, WJ, nbs, tid, nthr);
+        tm.sync();
+        tail_pass_sym<N, 2, true>(T.Ms, R2, VS, R0, VS, WJ, nbs, tid, nthr);
+      }
     }
     tm.sync();
   } else {
@@ -389,10 +422,17 @@ __device__ __forceinline__ void upd_batch(const UpdParams& P, const UpdOps<N>& O
   if constexpr (LATE) preload();
   // second half of S10: Pi~ along xi, eta
   if constexpr (!IDF) {
-    tail_pass_sym<N, 0, false>(T.frs, R0, VS, R1, VS, WJ, nbs, tid, nthr);
-    tm.sync();
-    tail_pass_sym<N, 1, false>(T.frs, R1, VS, R2, VS, WJ, nbs, tid, nthr);
-    tm.sync();
+    if constexpr (ONE) {
+      if (on1) tail_line_sym<N, 0, false>(T.frs, R0, R1, wjb1, bsi1, q0, q1);
+      tm.sync();
+      if (on1) tail_line_sym<N, 1, false>(T.frs, R1, R2, wjb1, bsi1, q0, q1);
+      tm.sync();
+    } else {
+      tail_pass_sym<N, 0, false>(T.frs, R0, VS, R1, VS, WJ, nbs, tid, nthr);
+      tm.sync();
+      tail_pass_sym<N, 1, false>(T.frs, R1, VS, R2, VS, WJ, nbs, tid, nthr);
+      tm.sync();
+    }
   }
   // Pi~ along zeta, negate, RK stage epilogue (zeta lines: coalesced across the
   // warp); u_{s+1} also lands in R0 for the projection below
