@@ -2,9 +2,11 @@
 //   S6  volume Hadamard flux differencing   (sumfac.hpp:48-94, 0.5*skew -> skew(a,b), D2)
 //   S7  hybrid surface-volume Hadamard      (sumfac.hpp:110-157, own face cofactor, D1)
 //   S8  EC + Roe face flux vs the neighbour's trace (euler.cpp:142-162, 229-301; D3)
-// Output: the volume rows vol = sum over directions [E][5][N^3] and the face
-// rows facc [E][3 dir][5][2 side][N^2]; S9 lifting, S10 and the RK update run
-// in K3 (kernel_update.cuh), fused with the next stage's entropy projection.
+// Output: the volume rows vol = sum over directions [E][5][N^3], with the face
+// rows already lifted onto their lines (fuse_face, n = 4..7: vol + sum_f l_f (x)
+// facc_f); at n = 3 the face rows facc [E][3 dir][5][2 side][N^2] separately.
+// The rest of S9, S10 and the RK update run in K3 (kernel_update.cuh), fused
+// with the next stage's entropy projection.
 //
 // Thread mapping. One thread per 1D line (dir, t1, t2) of an element does
 // every two-point evaluation touching that line: the n(n-1)/2 volume pairs,

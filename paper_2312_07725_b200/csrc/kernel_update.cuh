@@ -1,6 +1,7 @@
 // K3: the rest of the residual, the RK4 stage update and the NEXT stage's
 // entropy projection, fused:
-//   S9  chi^T lifting of the volume rows (K2's vol) and face rows (K2's facc)
+//   S9  chi^T lifting of the volume rows (K2's vol; its face rows are already in
+//       them for n = 4..7, fuse_face, else K2's facc is lifted here too)
 //   S10 weight-adjusted inverse -Pi~ (W J)^-1 Pi~^T R (fr_operators.cpp:280-309, D6)
 //   RK  classical RK4 stage update (D4)
 //   S1-S5 of u_{s+1} (kernel_project.cuh::proj_core) straight from shared memory,
@@ -9,8 +10,9 @@
 //
 // S9 and the first half of S10 are both tensor products, so
 //   Pi~^T^3 R = M^3 vol + sum_f (b_f (x) M (x) M) facc_f,  M = Pi~^T chi^T, b_f = Pi~^T bs_f
-// runs as three LINE passes with the face lifts injected into the pass of
-// their normal direction, the 1/(w J) scaling fused into the last one, then
+// runs as three LINE passes (fused: M^3 of K2's vol + sum_f l_f (x) facc_f,
+// b_f = M l_f; else the face lifts injected into the pass of their normal
+// direction), the 1/(w J) scaling fused into the last one, then
 // three Pi~ passes with the RK update fused into the last. (The entropy
 // diagnostic needs R itself: that path lifts with chi^T first.)
 //
