@@ -204,10 +204,14 @@ __device__ __forceinline__ void tail_pass_sym(const SymOp<N>& op, const double* 
   }
 }
 
+#ifndef NSFR_UPD_HOIST_MAX
+#define NSFR_UPD_HOIST_MAX 2
+#endif
+#define NSFR_UPD_LINES(j) _Pragma("unroll") for (int j = 0; j < LPT; ++j)
 // One line of that pass for a thread whose (tensor bsi, line l0 + N l1) was
-// worked out once per batch: where a batch's 5 N2 lines per element fit the
-// team in one round (n = 5), the index arithmetic of the five passes (two
-// divisions by constants each) is done once.
+// worked out once per batch: the index arithmetic of the five passes (two
+// divisions by constants each) is done once for the thread's one or two lines
+// (measured K3: n = 5 -3.5%, n = 4 -6.7%, n = 6 -1.8%).
 template <int N, int D, bool DIV>
 __device__ __forceinline__ void tail_line_sym(const SymOp<N>& op, const double* in, double* out,
                                               const double* wjb, int bsi, int l0, int l1) {
@@ -298,11 +302,20 @@ __device__ __forceinline__ void upd_batch(const UpdParams& P, const UpdOps<N>& O
   const TailOps<N>& T = O.t;
   const int tid = tm.tid(), nthr = tm.nthr();
   const int nbs = nb * 5;
-  // one line per thread and pass: its indices once per batch (tail_line_sym)
-  constexpr bool ONE = EPB * 5 * N2 <= NT && !INJ;
-  const bool on1 = tid < nbs * N2;
-  const int bsi1 = tid / N2, q0 = (tid - bsi1 * N2) % N, q1 = (tid - bsi1 * N2) / N;
-  const double* wjb1 = WJ + (bsi1 / 5) * N3;
+  // a thread's line(s) of every pass: the indices once per batch (tail_line_sym)
+  constexpr bool ONE = !INJ && NSFR_UPD_HOIST_MAX >= LPT;
+  bool on1[LPT];
+  int bsi1[LPT], q0[LPT], q1[LPT];
+  const double* wjb1[LPT];
+#pragma unroll
+  for (int j = 0; j < LPT; ++j) {
+    const int it = tid + j * NT;
+    on1[j] = it < nbs * N2;
+    bsi1[j] = it / N2;
+    q0[j] = (it - bsi1[j] * N2) % N;
+    q1[j] = (it - bsi1[j] * N2) / N;
+    wjb1[j] = WJ + (bsi1[j] / 5) * N3;
+  }
   PHASE_START();
   // the team syncs on the barrier's initialisation alone; thread 0 then issues
   // the TMA copies (and the look-ahead L2 prefetch of batch `pe`) while the
@@ -377,11 +390,11 @@ __device__ __forceinline__ void upd_batch(const UpdParams& P, const UpdOps<N>& O
       tail_pass<N, 2, true, true>(T.M, T.bm, R4 + 20 * N2, FS, R2, VS, R0, VS, WJ, nbs, tid, nthr);
     } else {
       if constexpr (ONE) {
-        if (on1) tail_line_sym<N, 0, false>(T.Ms, R0, R1, wjb1, bsi1, q0, q1);
+        NSFR_UPD_LINES(j) if (on1[j]) tail_line_sym<N, 0, false>(T.Ms, R0, R1, wjb1[j], bsi1[j], q0[j], q1[j]);
         tm.sync();
-        if (on1) tail_line_sym<N, 1, false>(T.Ms, R1, R2, wjb1, bsi1, q0, q1);
+        NSFR_UPD_LINES(j) if (on1[j]) tail_line_sym<N, 1, false>(T.Ms, R1, R2, wjb1[j], bsi1[j], q0[j], q1[j]);
         tm.sync();
-        if (on1) tail_line_sym<N, 2, true>(T.Ms, R2, R0, wjb1, bsi1, q0, q1);
+        NSFR_UPD_LINES(j) if (on1[j]) tail_line_sym<N, 2, true>(T.Ms, R2, R0, wjb1[j], bsi1[j], q0[j], q1[j]);
       } else {
         tail_pass_sym<N, 0, false>(T.Ms, R0, VS, R1, VS, WJ, nbs, tid, nthr);
         tm.sync();
@@ -425,9 +438,9 @@ __device__ __forceinline__ void upd_batch(const UpdParams& P, const UpdOps<N>& O
   // second half of S10: Pi~ along xi, eta
   if constexpr (!IDF) {
     if constexpr (ONE) {
-      if (on1) tail_line_sym<N, 0, false>(T.frs, R0, R1, wjb1, bsi1, q0, q1);
+      NSFR_UPD_LINES(j) if (on1[j]) tail_line_sym<N, 0, false>(T.frs, R0, R1, wjb1[j], bsi1[j], q0[j], q1[j]);
       tm.sync();
-      if (on1) tail_line_sym<N, 1, false>(T.frs, R1, R2, wjb1, bsi1, q0, q1);
+      NSFR_UPD_LINES(j) if (on1[j]) tail_line_sym<N, 1, false>(T.frs, R1, R2, wjb1[j], bsi1[j], q0[j], q1[j]);
       tm.sync();
     } else {
       tail_pass_sym<N, 0, false>(T.frs, R0, VS, R1, VS, WJ, nbs, tid, nthr);
