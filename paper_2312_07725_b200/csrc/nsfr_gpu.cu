@@ -147,12 +147,14 @@ int set_attrs(nsfr_gpu_ctx* ctx) {
   CK(cudaOccupancyMaxActiveBlocksPerMultiprocessor(&bp, k_project<N>, ProjCfg<N>::THREADS, ProjCfg<N>::SMEM));
   CK(cudaOccupancyMaxActiveBlocksPerMultiprocessor(&br, k_residual<N>, ResCfg<N>::THREADS, ResCfg<N>::SMEM));
   CK(cudaOccupancyMaxActiveBlocksPerMultiprocessor(&bu, k_update<N>, UpdCfg<N>::THREADS, UpdCfg<N>::SMEM));
-  // Look-ahead L2 prefetch distance in resident waves. Measured (64^3/48^3,
-  // A/B in one session): a quarter wave helps at p=4 (K2 -0.7%, K3 -0.8% vs
-  // one wave), none is best at p=3 (K2 -5%) and p=5 (K2 -2%).
+  // Look-ahead L2 prefetch distance in resident waves. Measured (A/B in one
+  // session, round 1): a quarter wave helps at p=4 (K2 -0.7%, K3 -0.8% vs one
+  // wave), none is best at p=3 (K2 -5%). Re-swept with the round-2 kernels
+  // (fused face lift; 0 / 0.25 / 0.5 / 1 wave): p=4 within 0.3% either way,
+  // p=3 none still best, p=5 a quarter wave -2.5% per step (K3 -7.8%).
   // NSFR_PF_WAVES overrides, NSFR_NO_PREFETCH=1 disables.
   const char* w = std::getenv("NSFR_PF_WAVES");
-  const double waves = w ? std::atof(w) : (N == 5 ? 0.25 : 0.0);
+  const double waves = w ? std::atof(w) : (N == 5 || N == 6 ? 0.25 : 0.0);
   const bool pf = std::getenv("NSFR_NO_PREFETCH") == nullptr && waves > 0.0;
   auto ahead = [&](int blocks) { return pf ? static_cast<int>(waves * sms * std::max(blocks, 1)) : (1 << 30); };
   ctx->ahead_proj = ahead(bp);
