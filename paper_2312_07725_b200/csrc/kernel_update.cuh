@@ -128,7 +128,13 @@ struct UpdCfg {
   // operators) in uniform registers across items. Measured K3 (A/B, one
   // session): p=5 224 -> 128 threads -13% (96: -8%, 160: +5%); p=6 352 -> 160
   // threads -8% (128: -4%); the same change costs +3% at p=4 and +16% at p=3.
-  static constexpr int THREADS = N == 6 ? 128 : (N == 7 ? 160 : ((EPB * N3 + 31) / 32) * 32);
+#ifndef NSFR_UPD_T6
+#define NSFR_UPD_T6 128
+#endif
+#ifndef NSFR_UPD_T7
+#define NSFR_UPD_T7 160
+#endif
+  static constexpr int THREADS = N == 6 ? NSFR_UPD_T6 : (N == 7 ? NSFR_UPD_T7 : ((EPB * N3 + 31) / 32) * 32);
   // R0 vol/u_{s+1}, R1, R2 pass buffers (5 N3 each), R3 facc / face scratch,
   // R4 face-lift buffers (30 N2 each), R5 1/(w J) (N3)
   // fuse_face: K2 lifted the face rows into vol, no facc staging, no face-lift buffers R4
