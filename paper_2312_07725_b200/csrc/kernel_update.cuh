@@ -128,11 +128,14 @@ struct UpdCfg {
   // operators) in uniform registers across items. Measured K3 (A/B, one
   // session): p=5 224 -> 128 threads -13% (96: -8%, 160: +5%); p=6 352 -> 160
   // threads -8% (128: -4%); the same change costs +3% at p=4 and +16% at p=3.
+  // (re-swept with the round-2 kernels: n = 6 96 / 128 / 192 / 224 threads ->
+  // K3 3.18 / 3.08 / 3.41 / 3.61 ms at 64^3; n = 7 128 / 160 / 256 threads ->
+  // 1.31 / 1.30 / 1.21 ms at 40^3 with c_DG, 1.57 / 1.56 / 1.53 ms with a c > 0)
 #ifndef NSFR_UPD_T6
 #define NSFR_UPD_T6 128
 #endif
 #ifndef NSFR_UPD_T7
-#define NSFR_UPD_T7 160
+#define NSFR_UPD_T7 256
 #endif
   static constexpr int THREADS = N == 6 ? NSFR_UPD_T6 : (N == 7 ? NSFR_UPD_T7 : ((EPB * N3 + 31) / 32) * 32);
   // R0 vol/u_{s+1}, R1, R2 pass buffers (5 N3 each), R3 facc / face scratch,

@@ -8,7 +8,8 @@ from paper_2312_07725_b200 import C_PLUS, GpuSolver, SolverConfig  # noqa: E402
 
 sizes = [(int(a), int(b)) for a, b in (s.split("x") for s in (sys.argv[1:] or ["4x64"]))]
 for p, m in sizes:
-    g = GpuSolver(SolverConfig(p=p, m=m, c1d=C_PLUS.get(p, 0.0)))
+    # NSFR_PROBE_C: a c value for degrees without a c_+ preset (general K3 variant instead of the c_DG one)
+    g = GpuSolver(SolverConfig(p=p, m=m, c1d=C_PLUS.get(p, float(os.environ.get("NSFR_PROBE_C", "0")))))
     g.init_case()
     g.advance(2)
     ms = g.time_steps(4)
